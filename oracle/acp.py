@@ -1,0 +1,216 @@
+"""ACP: Algorithms 2-4 of PAPER §3 (oracle; test infrastructure only).
+
+Restated step by step in the paper's order and notation:
+  chebyshev_nodes   PAPER.md:517-520   eps~_c = (e1+eN)/2 + (e1-eN)/2 cos(pi(c-1/2)/N_c)
+  lagrange_weights  PAPER.md:524-527   Eq. LagPoly
+  srft_sketch       PAPER.md:597-604, 618-620  Alg. 2 step 1 applied to G (Remark 1),
+                    real form (reading R5): G~ = [Re G^_nu1, Im G^_nu1, Re G^_nu2, ...]
+  sketch_matrix     PAPER.md:550-553, 619  rows of M~ = Kronecker(row of G~, row of Psi)
+  qrcp              PAPER.md:606-607   Alg. 2 steps 2-3 (greedy max-norm column pivoting,
+                    norms recomputed exactly, first index on ties; stop at
+                    |R_{N+1,N+1}| < eps |R_11|)
+  interpolation_vectors PAPER.md:608-613  Alg. 2 step 4: Xi^T = R11^{-1} R_{1:N,:} Pi^{-1}
+  compressed_W      PAPER.md:622-634   Eq. eqncompressU (direct solves) + Eq. eqnW (2f prefactor, R2)
+  acp_dyson         PAPER.md:717-795   change of variable (Eq. dyson2), adaptive compression
+                    (Eq. dyson3), SMW update (Eq. dyson4), Alg. 4 with a fixed number of
+                    outer iterations (reading R7).
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Callable, List
+
+import numpy as np
+import scipy.linalg as sla
+
+from .model import Model
+from .response import project_Q, projected_operator
+
+
+def chebyshev_nodes(e1: float, eN: float, Nc: int) -> np.ndarray:
+    """Chebyshev nodes mapped to [e1, eN], c = 1..N_c."""
+    c = np.arange(1, Nc + 1, dtype=np.float64)
+    theta = np.pi * (c - 0.5) / Nc
+    return 0.5 * (e1 + eN) + 0.5 * (e1 - eN) * np.cos(theta)
+
+
+def lagrange_weights(nodes: np.ndarray, e: np.ndarray) -> np.ndarray:
+    """L[i, c] = prod_{c' != c} (e_i - node_c') / (node_c - node_c') (Eq. LagPoly)."""
+    e = np.atleast_1d(np.asarray(e, dtype=np.float64))
+    Nc = len(nodes)
+    L = np.ones((len(e), Nc))
+    for c in range(Nc):
+        for cp in range(Nc):
+            if cp != c:
+                L[:, c] *= (e - nodes[cp]) / (nodes[c] - nodes[cp])
+    return L
+
+
+def srft_sketch(G: np.ndarray, theta: np.ndarray, nu: np.ndarray) -> np.ndarray:
+    """Real SRFT sketch of the columns of G (Alg. 2 step 1 via Remark 1; reading R5).
+
+    G^_nu = sum_{I=1}^{n} exp(-2 pi i I nu / n) eta_I g_I, eta_I = exp(2 pi i theta_I),
+    for the subsampled nu; returns [Re G^_nu1, Im G^_nu1, Re G^_nu2, Im G^_nu2, ...].
+    """
+    n = G.shape[1]
+    I = np.arange(1, n + 1, dtype=np.float64)
+    cols = []
+    for v in nu:
+        w = np.exp(-2j * np.pi * I * float(v) / n) * np.exp(2j * np.pi * theta)
+        Gh = G @ w
+        cols.append(Gh.real)
+        cols.append(Gh.imag)
+    return np.stack(cols, axis=1)
+
+
+def sketch_matrix(Psi: np.ndarray, Gt: np.ndarray) -> np.ndarray:
+    """M~ (Ng x N_occ*r): column i + q*N_occ is psi_i (.) g~_q (PAPER.md:336 stacked index, 619)."""
+    Ng, No = Psi.shape
+    r = Gt.shape[1]
+    M = np.empty((Ng, No * r))
+    for q in range(r):
+        M[:, q * No:(q + 1) * No] = Psi * Gt[:, q:q + 1]
+    return M
+
+
+@dataclasses.dataclass
+class QRCP:
+    perm: np.ndarray     # column permutation (Pi~), perm[j] = original column at position j
+    rdiag: np.ndarray    # |R~_jj| for the steps taken
+    R: np.ndarray        # (N_mu, n) rows of R~ in permuted column order
+    n_mu: int
+
+
+def qrcp(A: np.ndarray, eps: float, k_max: int | None = None, n_fixed: int | None = None) -> QRCP:
+    """Pivoted QR A Pi = Q R with |R_jj| non-increasing, greedy max-norm pivots.
+
+    Stops at the first j with |R_jj| < eps |R_11| (Alg. 2 step 3), or after
+    n_fixed steps if given (Table 1 style fixed N_mu).
+    """
+    A = np.array(A, dtype=np.float64, copy=True)
+    m, n = A.shape
+    kmax = min(m, n) if k_max is None else min(m, n, k_max)
+    if n_fixed is not None:
+        kmax = min(kmax, n_fixed)
+    perm = np.arange(n)
+    rdiag = []
+    r11 = None
+    n_mu = kmax
+    for j in range(kmax):
+        sub = A[j:, j:]
+        norms2 = np.einsum("ij,ij->j", sub, sub)
+        p = j + int(np.argmax(norms2))
+        rjj = float(np.sqrt(norms2[p - j]))
+        if r11 is None:
+            r11 = rjj
+        if n_fixed is None and rjj < eps * r11:
+            n_mu = j
+            break
+        if p != j:
+            A[:, [j, p]] = A[:, [p, j]]
+            perm[[j, p]] = perm[[p, j]]
+        x = A[j:, j].copy()
+        alpha = -np.copysign(rjj, x[0]) if x[0] != 0 else -rjj
+        v = x
+        v[0] -= alpha
+        vn = np.linalg.norm(v)
+        if vn > 0:
+            v /= vn
+            A[j:, j:] -= 2.0 * np.outer(v, v @ A[j:, j:])
+        A[j + 1:, j] = 0.0
+        rdiag.append(rjj)
+    R = np.triu(A[:n_mu, :])
+    return QRCP(perm=perm, rdiag=np.asarray(rdiag[:n_mu]), R=R, n_mu=n_mu)
+
+
+def interpolation_vectors(qr: QRCP, Ng: int):
+    """Alg. 2 step 4: Xi^T = R11^{-1} R_{1:N_mu,:} Pi^{-1}.
+
+    Returns (S, Xi): S[mu] = r_mu (grid index of the mu-th selected row),
+    Xi (Ng x N_mu) with Xi[S, :] = I.
+    """
+    N = qr.n_mu
+    T = sla.solve_triangular(qr.R[:, :N], qr.R, lower=False)
+    Xi = np.zeros((Ng, N))
+    Xi[qr.perm, :] = T.T
+    return qr.perm[:N].copy(), Xi
+
+
+def compress(model: Model, Psi: np.ndarray, Gp: np.ndarray, theta, nu, eps: float,
+             n_fixed: int | None = None):
+    """Alg. 2 with Remark 1 on M_ij = psi_i (.) g'_j.  Returns (S, Xi, qr)."""
+    Gt = srft_sketch(Gp, theta, nu)
+    Mt = sketch_matrix(Psi, Gt)
+    qr = qrcp(Mt.T, eps, n_fixed=n_fixed)
+    S, Xi = interpolation_vectors(qr, model.Ng)
+    return S, Xi, qr
+
+
+def compressed_W(model: Model, H: np.ndarray, Psi: np.ndarray, eps_occ: np.ndarray,
+                 S: np.ndarray, Xi: np.ndarray, Nc: int, return_zeta: bool = False):
+    """Alg. 3 steps 2-3: solve Eq. eqncompressU directly, build W by Eq. eqnW.
+
+    W_mu = 2 f sum_i psi_i (.) ( sum_c zeta~_{c mu} l_c(eps_i) ) psi_i(r_mu).
+    """
+    nodes = chebyshev_nodes(eps_occ[0], eps_occ[-1], Nc)
+    Lw = lagrange_weights(nodes, eps_occ)            # (N_occ, Nc)
+    rhs = project_Q(model, Psi, Xi)                  # Q xi_mu
+    W = np.zeros_like(Xi)
+    zetas = []
+    for c in range(Nc):
+        A = projected_operator(model, H, Psi, nodes[c])
+        Z = np.linalg.solve(A, rhs)                  # zeta~_{c mu}, all mu
+        if return_zeta:
+            zetas.append(Z)
+        Phi_c = Psi @ (Lw[:, c:c + 1] * Psi[S, :].T)  # sum_i psi_i l_c(eps_i) psi_i(r_mu)
+        W += 2.0 * model.f * Z * Phi_c
+    if return_zeta:
+        return W, nodes, np.stack(zetas)
+    return W
+
+
+@dataclasses.dataclass
+class ACPResult:
+    U: np.ndarray                       # chi G approximation (Ng x dN_A)
+    n_mu: List[int]
+    S: List[np.ndarray]
+    diff: List[float]                   # ||U~^{k+1} - U~^k||_F
+    W: List[np.ndarray]
+    Y: List[np.ndarray]
+
+
+def smw_update(model: Model, G: np.ndarray, W: np.ndarray, S: np.ndarray):
+    """Eq. dyson4: U~^{k+1} = B + W (I - Pi^T v W)^{-1} Pi^T v B.
+
+    With v B = G this is U^{k+1} = U~^{k+1} - B = W Y, Y = (I - (vW)(S,:))^{-1} G(S,:),
+    and the next compression input v U~^{k+1} = G + (vW) Y.
+    """
+    KW = model.yukawa(W)
+    A = np.eye(len(S)) - KW[S, :]
+    Y = np.linalg.solve(A, G[S, :])
+    return W @ Y, G + KW @ Y, Y
+
+
+def acp_dyson(model: Model, H: np.ndarray, Psi: np.ndarray, eps_occ: np.ndarray,
+              G: np.ndarray, Nc: int, n_outer: int, id_eps: float,
+              draws: Callable[[int, int], tuple], n_fixed: int | None = None) -> ACPResult:
+    """Alg. 4 with a fixed number of outer iterations.
+
+    draws(k, n_cols) -> (theta, nu): the SRFT randomness of outer iteration k.
+    """
+    Gp = G.copy()                      # v U~^0 = v B = G
+    U_prev = np.zeros_like(G)
+    res = ACPResult(U=None, n_mu=[], S=[], diff=[], W=[], Y=[])
+    for k in range(n_outer):
+        theta, nu = draws(k, G.shape[1])
+        S, Xi, qr = compress(model, Psi, Gp, theta, nu, id_eps, n_fixed=n_fixed)
+        W = compressed_W(model, H, Psi, eps_occ, S, Xi, Nc)
+        U, Gp, Y = smw_update(model, G, W, S)
+        res.diff.append(float(np.linalg.norm(U - U_prev)))
+        res.n_mu.append(len(S))
+        res.S.append(S)
+        res.W.append(W)
+        res.Y.append(Y)
+        U_prev = U
+    res.U = U_prev
+    return res
