@@ -1,0 +1,194 @@
+// common.cuh -- shared declarations of the B200 ACP library (internal).
+//
+// Context, error handling, workspace and launch accounting.  All kernels are
+// written for sm_100a (B200); fp64 throughout.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/acp_b200.h"
+
+namespace acp {
+
+struct Error : public std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define ACP_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::acp::Error(ACP_ERR_CUDA, std::string(#call) + ": " +                 \
+                                                 cudaGetErrorString(e_) + " @" +         \
+                                                 __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+#define ACP_REQUIRE(cond, msg)                                                           \
+    do {                                                                                 \
+        if (!(cond)) throw ::acp::Error(ACP_ERR_INVALID, std::string(msg));              \
+    } while (0)
+
+// FFT plan for one 1D length (Stockham autosort, radices 8/4/2/5/3).
+struct FftPlan {
+    int N = 0;
+    int npass = 0;
+    int radix[24] = {0};
+};
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace acp
+
+struct acp_context {
+    acp_system sys{};
+    int device = 0;
+    int dim = 1;
+    int Ng = 0;
+    double dV = 0.0, Omega = 0.0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    long long launches = 0;
+
+    acp::FftPlan plan;
+    double2* d_tw = nullptr;     // exp(-2 pi i m / N), m < N
+    double* d_k2 = nullptr;      // |k|^2 per FFT bin (numpy fft order)
+    double* d_kodd = nullptr;    // k_0 per bin with the Nyquist entry zeroed (odd multipliers)
+    double* d_kfull = nullptr;   // k_0 per bin (full)
+    double* d_khat = nullptr;    // Yukawa symbol 4 pi / (eps0 (|k|^2 + kappa^2))
+    double* d_mult = nullptr;    // scratch multiplier table (N)
+
+    std::map<std::string, acp::DevBuf> bufs;
+
+    // Workspace of at least `bytes` bytes under `name` (contents not preserved on growth).
+    void* ws(const std::string& name, size_t bytes) {
+        acp::DevBuf& b = bufs[name];
+        if (b.bytes < bytes) {
+            if (b.ptr) cudaFree(b.ptr);
+            b.ptr = nullptr;
+            b.bytes = 0;
+            size_t nb = bytes < 256 ? 256 : bytes;
+            cudaError_t e = cudaMalloc(&b.ptr, nb);
+            if (e != cudaSuccess)
+                throw acp::Error(ACP_ERR_ALLOC, "cudaMalloc(" + std::to_string(nb) + ") for " + name +
+                                                    ": " + cudaGetErrorString(e));
+            b.bytes = nb;
+        }
+        return b.ptr;
+    }
+    double* wsd(const std::string& name, size_t n) { return static_cast<double*>(ws(name, n * sizeof(double))); }
+    int* wsi(const std::string& name, size_t n) { return static_cast<int*>(ws(name, n * sizeof(int))); }
+};
+
+namespace acp {
+
+// Record one kernel launch (call right after <<<>>>); checks launch errors.
+inline void launched(acp_context* ctx, int n = 1) {
+    ctx->launches += n;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(ACP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+inline void sync(acp_context* ctx) { ACP_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---- fft.cu -------------------------------------------------------------
+FftPlan make_plan(int N);
+void fft_init(acp_context* ctx);
+void fft_free(acp_context* ctx);
+
+// Which Fourier multiplier a Fourier-operator launch uses.
+enum MultKind { MULT_KINETIC = 0, MULT_YUKAWA = 1, MULT_PRECOND = 2, MULT_NONE = 3 };
+
+struct FopArgs {
+    const double* X = nullptr;     // input columns (ld = Ng)
+    double* Y = nullptr;           // output columns (ld = Ng); may alias X only if dots unused
+    int n = 0;                     // number of columns
+    const double* mult = nullptr;  // real multiplier per bin (already scaled by 1/N), or null
+    const double* diag = nullptr;  // pointwise potential (Ng) or null
+    const double* shift = nullptr; // per-column shift or null
+    const int* active = nullptr;   // per-column activity flags or null
+    double* dots = nullptr;        // per column: [0] x.y [1] x.x  (stride 2) or null
+};
+// Y = IFFT(mult * FFT(X)) + (diag - shift_j) (.) X, two real columns per complex FFT.
+void fourier_op(acp_context* ctx, const FopArgs& a);
+// Fill ctx->d_mult with a multiplier of the given kind (scaled by 1/N); returns it.
+const double* multiplier(acp_context* ctx, MultKind kind, double tau);
+// Real grid functions from Hermitian spectra given as complex coefficients per bin:
+// out_j = (Ng/Omega) IFFT(spec_j)  (spec: Ng x n complex, bin-major per column).
+void ifft_hermitian(acp_context* ctx, const double2* spec, int n, double* out);
+// Spectrum out(k) = sum_a x(a) e^{-i k r_a} of one real column.
+void real_spectrum(acp_context* ctx, const double* x, double2* out);
+// Spectra of g_{I,a} (n = d*N_A columns) at positions R (device, N_A*d).
+void spectrum_G(acp_context* ctx, const double* d_R, double2* spec);
+// Spectrum of the total pseudocharge m.
+void spectrum_m(acp_context* ctx, const double* d_R, double2* spec);
+
+// ---- gemm.cu ------------------------------------------------------------
+// C (m x n, ld m) = alpha A^T B, A: K x m (lda), B: K x n (ldb); split-K partials reduced in order.
+void gemm_tn(acp_context* ctx, int K, int m, int n, double alpha, const double* A, int lda,
+             const double* B, int ldb, double* C);
+// Partials only: Cp[z] (m x n) for the z-th K chunk of `kchunk` rows; returns the split count.
+// The split pattern depends only on (K, kchunk), so per-column results do not depend on n.
+int gemm_tn_partial(acp_context* ctx, int K, int m, int n, const double* A, int lda,
+                    const double* B, int ldb, double* Cp, int kchunk);
+int gemm_tn_splits(int K, int m, int n);
+// C = beta C + alpha A B,  A: M x K (lda), B: K x n (ldb), C: M x n (ldc).
+void gemm_nn(acp_context* ctx, int M, int K, int n, double alpha, const double* A, int lda,
+             const double* B, int ldb, double beta, double* C, int ldc);
+
+// ---- pcg.cu -------------------------------------------------------------
+struct PcgStats {
+    int max_iter = 0;
+    long long total_iter = 0;
+    double max_rel_res = 0.0;
+    int n_solved = 0;
+};
+// Batched projected Sternheimer solve for columns j = c*nmu_p + mu:
+// Q(H - shift_c)Q x = Q rhs_mu (rhs already in range(Q)).
+void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const double* V,
+                       const double* d_shift_c, int n_c, const double* rhs, int nmu_p,
+                       double tol, int max_iter, double tau, double* X, PcgStats* st);
+void apply_chi0(acp_context* ctx, const double* Psi, const double* eps, const double* V,
+                const int* S, const double* Xi, int n_mu, int mu_begin, int mu_end, int n_cheb,
+                double tol, int max_iter, double* W, PcgStats* st);
+
+// ---- qrcp.cu ------------------------------------------------------------
+int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols,
+             const double* h_theta, const int* h_nu, int r_half, double id_eps, int n_fixed,
+             int n_mu_max, int* S, double* Xi);
+
+// ---- dense.cu -----------------------------------------------------------
+// Solve A X = B in place (A: n x n col-major, B: n x nrhs col-major), partial pivoting.
+void lu_solve(acp_context* ctx, double* A, int n, double* B, int nrhs);
+// Symmetric eigenvalues (and optionally vectors) of A (n x n col-major, destroyed) by Jacobi.
+void sym_eig(acp_context* ctx, double* A, int n, double* w, double* V);
+// Cholesky A = L L^T in place (lower), returns false if not SPD.
+void cholesky(acp_context* ctx, double* A, int n);
+
+// ---- dyson / phonon / scf ----------------------------------------------
+void dyson(acp_context* ctx, const double* Psi, const double* eps, const double* V, const double* G,
+           const acp_dyson_opts& o, const double* h_theta, const int* h_nu, double* U, double* h_info);
+void dynamical_matrix(acp_context* ctx, const double* h_R, const double* rho, const double* G,
+                      const double* U, const double* h_masses, double* h_D, double* h_lambda);
+void ground_state(acp_context* ctx, const double* h_R, const acp_scf_opts& o, double* Psi,
+                  double* eps, double* rho, double* V, double* G, double* h_info);
+void perturbations(acp_context* ctx, const double* h_R, double* G);
+
+// ---- small device helpers ----------------------------------------------
+void fill(acp_context* ctx, double* p, size_t n, double v);
+void copy_cols(acp_context* ctx, double* dst, const double* src, size_t n);
+
+}  // namespace acp

@@ -1,0 +1,145 @@
+// gemm.cu -- FP64 DMMA GEMMs: split-K A^T B (projection coefficients) and A B (+ beta C).
+#include "gemm.cuh"
+
+namespace acp {
+
+constexpr int TN_BM = 32, TN_BN = 32, TN_BK = 32;
+
+// Cp[z] (m x n) = A(:, m)^T B(:, n) over the z-th K chunk.  A: K x m (lda), B: K x n (ldb).
+__global__ void __launch_bounds__(128) k_gemm_tn(int K, int m, int n, const double* __restrict__ A, int lda,
+                                                 const double* __restrict__ B, int ldb, int kchunk,
+                                                 double* __restrict__ Cp) {
+    __shared__ double As[TN_BM][TN_BK + 4];
+    __shared__ double Bs[TN_BN][TN_BK + 4];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int n0 = blockIdx.x * TN_BN, m0 = blockIdx.y * TN_BM;
+    const int kb = blockIdx.z * kchunk;
+    const int ke = min(K, kb + kchunk);
+    double acc[2][2][2] = {};
+    for (int k0 = kb; k0 < ke; k0 += TN_BK) {
+        for (int idx = tid; idx < TN_BM * TN_BK; idx += 128) {
+            const int mm = idx / TN_BK, kk = idx % TN_BK;
+            const int gm = m0 + mm, gk = k0 + kk;
+            As[mm][kk] = (gm < m && gk < ke) ? A[(size_t)gm * lda + gk] : 0.0;
+        }
+        for (int idx = tid; idx < TN_BN * TN_BK; idx += 128) {
+            const int nn = idx / TN_BK, kk = idx % TN_BK;
+            const int gn = n0 + nn, gk = k0 + kk;
+            Bs[nn][kk] = (gn < n && gk < ke) ? B[(size_t)gn * ldb + gk] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < TN_BK; ks += 4) {
+            double af[2], bf[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) af[i] = As[wm * 16 + i * 8 + g][ks + t];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) bf[j] = Bs[wn * 16 + j * 8 + g][ks + t];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();
+    }
+    double* C = Cp + (size_t)blockIdx.z * m * n;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = m0 + wm * 16 + i * 8 + g;
+                const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
+                if (row < m && col < n) C[(size_t)col * m + row] = acc[i][j][e];
+            }
+}
+
+__global__ void k_reduce_splits(size_t total, int splits, double alpha, const double* __restrict__ Cp,
+                                double* __restrict__ C) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += Cp[(size_t)z * total + i];
+    C[i] = alpha * s;
+}
+
+int gemm_tn_splits(int K, int m, int n) {
+    const int tiles = cdiv(m, TN_BM) * cdiv(n, TN_BN);
+    int s = 296 / (tiles > 0 ? tiles : 1);
+    int smax = K / 256;
+    if (s > smax) s = smax;
+    if (s > 64) s = 64;
+    if (s < 1) s = 1;
+    return s;
+}
+
+int gemm_tn_partial(acp_context* ctx, int K, int m, int n, const double* A, int lda, const double* B, int ldb,
+                    double* Cp, int kchunk) {
+    kchunk = cdiv(kchunk, TN_BK) * TN_BK;
+    const int splits = cdiv(K, kchunk);
+    dim3 grid(cdiv(n, TN_BN), cdiv(m, TN_BM), splits);
+    k_gemm_tn<<<grid, 128, 0, ctx->stream>>>(K, m, n, A, lda, B, ldb, kchunk, Cp);
+    launched(ctx);
+    return splits;
+}
+
+void gemm_tn(acp_context* ctx, int K, int m, int n, double alpha, const double* A, int lda, const double* B,
+             int ldb, double* C) {
+    if (m <= 0 || n <= 0) return;
+    const int s0 = gemm_tn_splits(K, m, n);
+    const int kchunk = cdiv(cdiv(K, s0), TN_BK) * TN_BK;
+    double* Cp = ctx->wsd("gemm_tn_part", (size_t)cdiv(K, kchunk) * m * n);
+    int splits = gemm_tn_partial(ctx, K, m, n, A, lda, B, ldb, Cp, kchunk);
+    size_t total = (size_t)m * n;
+    k_reduce_splits<<<cdiv(total, 256), 256, 0, ctx->stream>>>(total, splits, alpha, Cp, C);
+    launched(ctx);
+}
+
+struct EpAxpby {
+    double alpha, beta;
+    double* C;
+    int ldc;
+    __device__ __forceinline__ void operator()(int r, int c, double acc) const {
+        double* p = C + (size_t)c * ldc + r;
+        *p = (beta == 0.0 ? 0.0 : beta * *p) + alpha * acc;
+    }
+};
+
+__global__ void __launch_bounds__(128) k_gemm_nn(int M, int K, int n, const double* __restrict__ A, int lda,
+                                                 const double* __restrict__ B, int ldb, EpAxpby ep) {
+    nn_tile(M, K, n, A, lda, B, ldb, blockIdx.x * NN_BM, blockIdx.y * NN_BN, ep);
+}
+
+void gemm_nn(acp_context* ctx, int M, int K, int n, double alpha, const double* A, int lda, const double* B,
+             int ldb, double beta, double* C, int ldc) {
+    if (M <= 0 || n <= 0) return;
+    EpAxpby ep{alpha, beta, C, ldc};
+    dim3 grid(cdiv(M, NN_BM), cdiv(n, NN_BN));
+    k_gemm_nn<<<grid, 128, 0, ctx->stream>>>(M, K, n, A, lda, B, ldb, ep);
+    launched(ctx);
+}
+
+// ---- small helpers ---------------------------------------------------------
+__global__ void k_fill(double* p, size_t n, double v) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+void fill(acp_context* ctx, double* p, size_t n, double v) {
+    if (!n) return;
+    k_fill<<<cdiv(n, 256), 256, 0, ctx->stream>>>(p, n, v);
+    launched(ctx);
+}
+__global__ void k_copy(double* __restrict__ d, const double* __restrict__ s, size_t n) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) d[i] = s[i];
+}
+void copy_cols(acp_context* ctx, double* dst, const double* src, size_t n) {
+    if (!n) return;
+    k_copy<<<cdiv(n, 256), 256, 0, ctx->stream>>>(dst, src, n);
+    launched(ctx);
+}
+
+}  // namespace acp

@@ -1,0 +1,384 @@
+// pcg.cu -- batched, projected Sternheimer solves (Eq. eqncompressU) and W (Eq. eqnW).
+//
+// Q(eps~_c - H)Q zeta~_{c mu} = Q xi_mu for all (c, mu).  The solver
+// works on the equivalent SPD system Q(H - eps~_c)Q x = -Q xi on range(Q) with
+// preconditioned CG (PAPER.md:426 leaves the solver open; H - eps~_c is positive
+// on range(Q) because every node lies in [eps_1, eps_Nocc] below the gap).
+// Preconditioner: z = Q M r, M = IFFT (|k|^2/2 + tau)^{-1} FFT (Fourier diagonal).
+//
+// One CG iteration over the whole batch = 8 launches captured in a CUDA graph:
+//   K1 y = (H - eps_c) p  (+ p.y)          K2 C  = dV Psi^T y (split-K DMMA)
+//   S  alpha = rz / p.y  (split reduce)     K3 Ap = y - Psi C ; x += alpha p ; r -= alpha Ap
+//   K1 zh = M r (+ r.zh, r.r)               K2 Cz = dV Psi^T zh
+//   S  convergence / beta                   K3 p = (zh - Psi Cz) + beta p
+// p.y equals p.Q(H-eps)Q p and r.zh equals r.z because p, r stay in range(Q).
+// Per-column activity flags freeze converged columns; every reduction has a
+// fixed order, so results do not depend on scheduling.
+#include "gemm.cuh"
+
+#include <cmath>
+
+namespace acp {
+
+// Chebyshev nodes on [eps_1, eps_N] and Lagrange weights
+// L[i + c*n_occ] = prod_{c' != c} (eps_i - node_c') / (node_c - node_c').
+__global__ void k_cheb(const double* __restrict__ eps, int n_occ, int nc, double* __restrict__ nodes,
+                       double* __restrict__ L) {
+    __shared__ double sn[256];
+    const double e1 = eps[0], eN = eps[n_occ - 1];
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+        const double th = ((double)c + 0.5) / (double)nc;  // theta_c / pi, c = 1..Nc -> (c - 1/2)/Nc
+        const double v = 0.5 * (e1 + eN) + 0.5 * (e1 - eN) * cospi(th);
+        sn[c] = v;
+        nodes[c] = v;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n_occ * nc; idx += blockDim.x) {
+        const int i = idx % n_occ, c = idx / n_occ;
+        double l = 1.0;
+        for (int cp = 0; cp < nc; ++cp)
+            if (cp != c) l *= (eps[i] - sn[cp]) / (sn[c] - sn[cp]);
+        L[idx] = l;
+    }
+}
+
+__global__ void k_batch_shift(const double* __restrict__ nodes, int nc, int nmu_p, double* __restrict__ shift) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nc * nmu_p) shift[j] = nodes[j / nmu_p];
+}
+
+// R[:, c*nmu_p + mu] = rhs[:, mu]; X = 0.
+__global__ void k_pcg_init(int Ng, int nc, int nmu_p, const double* __restrict__ rhs, double* __restrict__ R,
+                           double* __restrict__ X) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    size_t tot = (size_t)Ng * nc * nmu_p;
+    if (i >= tot) return;
+    size_t col = i / Ng, r = i % Ng;
+    int mu = (int)(col % nmu_p);
+    R[i] = rhs[(size_t)mu * Ng + r];
+    X[i] = 0.0;
+}
+
+enum { SC_INIT = 0, SC_ALPHA = 1, SC_BETA = 2 };
+
+struct PcgScal {
+    double* rz;      // r.z (current)
+    double* bb;      // ||b||^2
+    double* alpha;
+    double* beta;
+    double* res;     // final relative residual
+    int* active;
+    int* iters;
+    const double* dots;  // from K1: [2j] x.y, [2j+1] x.x
+};
+
+// C = dV * sum_z Cp[z]  (n_occ x n), plus the per-column scalar recurrences.
+__global__ void k_pcg_scalars(int mode, int n_occ, int n, int splits, double dV, const double* __restrict__ Cp,
+                              double* __restrict__ C, PcgScal s, double tol2, int n_valid_mu, int nmu_p) {
+    const size_t tot = (size_t)n_occ * n;
+    size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < tot) {
+        double acc = 0.0;
+        for (int z = 0; z < splits; ++z) acc += Cp[(size_t)z * tot + idx];
+        C[idx] = dV * acc;
+    }
+    if (idx < (size_t)n) {
+        const int j = (int)idx;
+        if (mode == SC_INIT) {
+            const double rz = s.dots[2 * j], bb = s.dots[2 * j + 1];
+            const bool valid = (j % nmu_p) < n_valid_mu && bb > 0.0;
+            s.rz[j] = rz;
+            s.bb[j] = bb;
+            s.active[j] = valid ? 1 : 0;
+            s.iters[j] = 0;
+            s.res[j] = 0.0;
+            s.alpha[j] = 0.0;
+            s.beta[j] = 0.0;
+        } else if (mode == SC_ALPHA) {
+            if (s.active[j]) s.alpha[j] = s.rz[j] / s.dots[2 * j];
+        } else {
+            if (s.active[j]) {
+                const double rzn = s.dots[2 * j], rr = s.dots[2 * j + 1];
+                s.iters[j] += 1;
+                s.res[j] = sqrt(rr / s.bb[j]);
+                if (rr <= tol2 * s.bb[j]) {
+                    s.active[j] = 0;
+                } else {
+                    s.beta[j] = rzn / s.rz[j];
+                    s.rz[j] = rzn;
+                }
+            }
+        }
+    }
+}
+
+// K3 after H p: Ap = Y - Psi C;  X += alpha P;  R -= alpha Ap.
+struct EpAlpha {
+    const double* Y;
+    const double* P;
+    double* X;
+    double* R;
+    const double* alpha;
+    const int* active;
+    int ld;
+    __device__ __forceinline__ void operator()(int r, int c, double acc) const {
+        if (!active[c]) return;
+        const size_t o = (size_t)c * ld + r;
+        const double a = alpha[c];
+        const double ap = Y[o] - acc;
+        X[o] += a * P[o];
+        R[o] -= a * ap;
+    }
+};
+// K3 after M r: Z = Zh - Psi Cz;  P = Z + beta P (or P = Z at init).
+struct EpBeta {
+    const double* Zh;
+    double* P;
+    const double* beta;
+    const int* active;
+    int ld;
+    int init;
+    __device__ __forceinline__ void operator()(int r, int c, double acc) const {
+        if (!active[c]) return;
+        const size_t o = (size_t)c * ld + r;
+        const double z = Zh[o] - acc;
+        P[o] = init ? z : z + beta[c] * P[o];
+    }
+};
+
+template <class Ep>
+__global__ void __launch_bounds__(128) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
+                                                    const double* __restrict__ B, int ldb, Ep ep) {
+    // skip tiles whose columns are all inactive (uniform per CTA)
+    const int n0 = blockIdx.y * NN_BN;
+    __shared__ int any;
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int c = n0; c < min(n, n0 + NN_BN); ++c) a |= ep.active[c];
+        any = a;
+    }
+    __syncthreads();
+    if (!any) return;
+    nn_tile(M, K, n, A, lda, B, ldb, blockIdx.x * NN_BM, n0, ep);
+}
+
+__global__ void k_count_active(const int* __restrict__ active, int n, int* __restrict__ out) {
+    __shared__ int red[32];
+    int s = 0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) s += active[j];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        *out = t;
+    }
+}
+
+// W(:, mu) = 2f sum_c X(:, c*nmu_p + mu) (.) Phi_c(:, mu),
+// Phi_c(alpha, mu) = sum_i Psi(alpha, i) L(i, c) Psi(r_mu, i)   (Eq. eqnW).
+constexpr int W_MAXC = 32;
+__global__ void __launch_bounds__(128) k_build_W(int Ng, int n_occ, int nc, int nmu_p, int mu_count,
+                                                 const double* __restrict__ Psi, const double* __restrict__ L,
+                                                 const int* __restrict__ S, int mu_begin,
+                                                 const double* __restrict__ X, double pref,
+                                                 double* __restrict__ W) {
+    extern __shared__ double LS[];  // nc x n_occ : L(i,c) Psi(r_mu, i)
+    const int mu = blockIdx.y;
+    const int smu = S[mu_begin + mu];
+    for (int idx = threadIdx.x; idx < nc * n_occ; idx += blockDim.x) {
+        const int i = idx % n_occ, c = idx / n_occ;
+        LS[idx] = L[c * n_occ + i] * Psi[(size_t)i * Ng + smu];
+    }
+    __syncthreads();
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= Ng) return;
+    double phi[W_MAXC];
+#pragma unroll
+    for (int c = 0; c < W_MAXC; ++c) phi[c] = 0.0;
+    for (int i = 0; i < n_occ; ++i) {
+        const double p = Psi[(size_t)i * Ng + a];
+#pragma unroll
+        for (int c = 0; c < W_MAXC; ++c)
+            if (c < nc) phi[c] += p * LS[c * n_occ + i];
+    }
+    double w = 0.0;
+#pragma unroll
+    for (int c = 0; c < W_MAXC; ++c)
+        if (c < nc) w += X[(size_t)(c * nmu_p + mu) * Ng + a] * phi[c];
+    W[(size_t)(mu_begin + mu) * Ng + a] = pref * w;
+}
+
+void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const double* V, const double* d_shift_c,
+                       int n_c, const double* rhs, int nmu_p, double tol, int max_iter, double tau, double* X,
+                       PcgStats* st) {
+    const int Ng = ctx->Ng;
+    const int n = n_c * nmu_p;
+    if (n == 0) return;
+    double* R = ctx->wsd("pcg_R", (size_t)Ng * n);
+    double* P = ctx->wsd("pcg_P", (size_t)Ng * n);
+    double* Y = ctx->wsd("pcg_Y", (size_t)Ng * n);
+    double* shift = ctx->wsd("pcg_shift", n);
+    double* dots = ctx->wsd("pcg_dots", 2 * (size_t)n);
+    double* C = ctx->wsd("pcg_C", (size_t)n_occ * n);
+    const int kchunk = 512;  // fixed split pattern: per-column results independent of the batch size
+    const int max_splits = cdiv(Ng, kchunk);
+    double* Cp = ctx->wsd("pcg_Cp", (size_t)max_splits * n_occ * n);
+    PcgScal s;
+    s.rz = ctx->wsd("pcg_rz", n);
+    s.bb = ctx->wsd("pcg_bb", n);
+    s.alpha = ctx->wsd("pcg_alpha", n);
+    s.beta = ctx->wsd("pcg_beta", n);
+    s.res = ctx->wsd("pcg_res", n);
+    s.active = ctx->wsi("pcg_active", n);
+    s.iters = ctx->wsi("pcg_iters", n);
+    s.dots = dots;
+    int* d_nact = ctx->wsi("pcg_nact", 1);
+    int* h_nact = nullptr;
+    ACP_CUDA(cudaMallocHost(&h_nact, sizeof(int)));
+
+    const double* mH = multiplier(ctx, MULT_KINETIC, 0.0);
+    double* mHc = ctx->wsd("pcg_multH", Ng);
+    copy_cols(ctx, mHc, mH, Ng);
+    const double* mP0 = multiplier(ctx, MULT_PRECOND, tau);
+    double* mP = ctx->wsd("pcg_multP", Ng);
+    copy_cols(ctx, mP, mP0, Ng);
+
+    const int nvalid = nmu_p;  // columns beyond the caller's count are zero RHS -> inactive by bb = 0
+    k_batch_shift<<<cdiv(n, 256), 256, 0, ctx->stream>>>(d_shift_c, n_c, nmu_p, shift);
+    launched(ctx);
+    {
+        size_t tot = (size_t)Ng * n;
+        k_pcg_init<<<cdiv(tot, 256), 256, 0, ctx->stream>>>(Ng, n_c, nmu_p, rhs, R, X);
+        launched(ctx);
+    }
+    const double tol2 = tol * tol;
+    const int sc_threads = 256;
+    const int sc_blocks = cdiv((size_t)n_occ * n > (size_t)n ? (size_t)n_occ * n : (size_t)n, sc_threads);
+    dim3 ugrid(cdiv(Ng, NN_BM), cdiv(n, NN_BN));
+
+    auto precond_half = [&](int mode) {
+        FopArgs f;
+        f.X = R;
+        f.Y = Y;
+        f.n = n;
+        f.mult = mP;
+        f.active = (mode == SC_INIT) ? nullptr : s.active;
+        f.dots = dots;
+        fourier_op(ctx, f);
+        int splits = gemm_tn_partial(ctx, Ng, n_occ, n, Psi, Ng, Y, Ng, Cp, kchunk);
+        k_pcg_scalars<<<sc_blocks, sc_threads, 0, ctx->stream>>>(mode, n_occ, n, splits, ctx->dV, Cp, C, s, tol2,
+                                                                  nvalid, nmu_p);
+        launched(ctx);
+        EpBeta ep{Y, P, s.beta, s.active, Ng, mode == SC_INIT ? 1 : 0};
+        k_pcg_update<EpBeta><<<ugrid, 128, 0, ctx->stream>>>(Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
+        launched(ctx);
+    };
+    auto hamiltonian_half = [&]() {
+        FopArgs f;
+        f.X = P;
+        f.Y = Y;
+        f.n = n;
+        f.mult = mHc;
+        f.diag = V;
+        f.shift = shift;
+        f.active = s.active;
+        f.dots = dots;
+        fourier_op(ctx, f);
+        int splits = gemm_tn_partial(ctx, Ng, n_occ, n, Psi, Ng, Y, Ng, Cp, kchunk);
+        k_pcg_scalars<<<sc_blocks, sc_threads, 0, ctx->stream>>>(SC_ALPHA, n_occ, n, splits, ctx->dV, Cp, C, s,
+                                                                  tol2, nvalid, nmu_p);
+        launched(ctx);
+        EpAlpha ep{Y, P, X, R, s.alpha, s.active, Ng};
+        k_pcg_update<EpAlpha><<<ugrid, 128, 0, ctx->stream>>>(Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
+        launched(ctx);
+    };
+
+    // r0 = b, z0 = Q M r0, p0 = z0
+    precond_half(SC_INIT);
+
+    // Capture `chunk` iterations into one graph and replay until converged.
+    const int chunk = 4;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    long long before = ctx->launches;
+    ACP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    for (int it = 0; it < chunk; ++it) {
+        hamiltonian_half();
+        precond_half(SC_BETA);
+    }
+    k_count_active<<<1, 256, 0, ctx->stream>>>(s.active, n, d_nact);
+    launched(ctx);
+    ACP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+    const long long per_replay = ctx->launches - before;
+    ctx->launches = before;
+    ACP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    int done_iter = 0;
+    bool converged = false;
+    while (done_iter < max_iter) {
+        ACP_CUDA(cudaGraphLaunch(exec, ctx->stream));
+        ctx->launches += per_replay;
+        done_iter += chunk;
+        ACP_CUDA(cudaMemcpyAsync(h_nact, d_nact, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (*h_nact == 0) {
+            converged = true;
+            break;
+        }
+    }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    cudaFreeHost(h_nact);
+    if (st) {
+        std::vector<int> it(n);
+        std::vector<double> res(n), bb(n);
+        ACP_CUDA(cudaMemcpy(it.data(), s.iters, n * sizeof(int), cudaMemcpyDeviceToHost));
+        ACP_CUDA(cudaMemcpy(res.data(), s.res, n * sizeof(double), cudaMemcpyDeviceToHost));
+        ACP_CUDA(cudaMemcpy(bb.data(), s.bb, n * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int j = 0; j < n; ++j) {
+            if (bb[j] <= 0.0) continue;
+            st->n_solved += 1;
+            st->total_iter += it[j];
+            if (it[j] > st->max_iter) st->max_iter = it[j];
+            if (res[j] > st->max_rel_res) st->max_rel_res = res[j];
+        }
+    }
+    if (!converged)
+        throw Error(ACP_ERR_NOT_CONVERGED, "Sternheimer PCG did not converge in " + std::to_string(max_iter) +
+                                               " iterations");
+}
+
+void apply_chi0(acp_context* ctx, const double* Psi, const double* eps, const double* V, const int* S,
+                const double* Xi, int n_mu, int mu_begin, int mu_end, int n_cheb, double tol, int max_iter,
+                double* W, PcgStats* st) {
+    const int Ng = ctx->Ng;
+    const int n_occ = ctx->sys.n_occ;
+    ACP_REQUIRE(0 <= mu_begin && mu_begin <= mu_end && mu_end <= n_mu, "invalid mu range");
+    ACP_REQUIRE(n_cheb >= 1 && n_cheb <= W_MAXC, "n_cheb must be in [1, 32]");
+    ACP_REQUIRE(n_occ <= 256 && n_cheb <= 256, "n_occ too large");
+    const int cnt = mu_end - mu_begin;
+    if (cnt == 0) return;
+    const int nmu_p = (cnt + 1) / 2 * 2;
+    double* nodes = ctx->wsd("chi_nodes", n_cheb);
+    double* L = ctx->wsd("chi_L", (size_t)n_occ * n_cheb);
+    k_cheb<<<1, 256, 0, ctx->stream>>>(eps, n_occ, n_cheb, nodes, L);
+    launched(ctx);
+    // rhs_mu = -Q xi_mu  (Q xi = xi - Psi dV Psi^T xi), padded with a zero column.
+    double* rhs = ctx->wsd("chi_rhs", (size_t)Ng * nmu_p);
+    double* Cb = ctx->wsd("chi_Cb", (size_t)n_occ * nmu_p);
+    if (nmu_p != cnt) fill(ctx, rhs + (size_t)cnt * Ng, Ng, 0.0);
+    copy_cols(ctx, rhs, Xi + (size_t)mu_begin * Ng, (size_t)cnt * Ng);
+    gemm_tn(ctx, Ng, n_occ, cnt, ctx->dV, Psi, Ng, rhs, Ng, Cb);
+    gemm_nn(ctx, Ng, n_occ, cnt, 1.0, Psi, Ng, Cb, n_occ, -1.0, rhs, Ng);
+    double* X = ctx->wsd("chi_X", (size_t)Ng * n_cheb * nmu_p);
+    const double tau = 0.05;
+    sternheimer_batch(ctx, Psi, n_occ, V, nodes, n_cheb, rhs, nmu_p, tol, max_iter, tau, X, st);
+    dim3 grid(cdiv(Ng, 128), cnt);
+    size_t smem = (size_t)n_cheb * n_occ * sizeof(double);
+    k_build_W<<<grid, 128, smem, ctx->stream>>>(Ng, n_occ, n_cheb, nmu_p, cnt, Psi, L, S, mu_begin, X,
+                                                2.0 * ctx->sys.occ, W);
+    launched(ctx);
+}
+
+}  // namespace acp

@@ -1,0 +1,215 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element.
+
+Tolerances: building blocks 1e-12 relative (pure fp64 rounding);
+Sternheimer-derived quantities are limited by the CG tolerance (1e-11 relative
+residual) times the conditioning of Q(H - eps)Q on range(Q) -> 1e-9 relative on
+W and U; the acceptance bar of BASELINE.json:north_star is 1e-8 relative on D and
+1e-7 relative on the phonon eigenvalues.  Integer outputs (QRCP pivots) are bit-exact.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from workloads import atom_positions, get_config, sketch_draws  # noqa: E402
+from workloads.configs import small_config  # noqa: E402
+from oracle.model import Model  # noqa: E402
+from oracle.scf import scf  # noqa: E402
+from oracle import acp as oacp, phonon as ophonon, response as ors  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def T(x, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda").contiguous()
+
+
+class Sys:
+    """Oracle ground state + everything the GPU calls need, for one config."""
+
+    def __init__(self, cfg):
+        from paper_1605_08021_b200 import Context
+        self.cfg = cfg
+        self.R = atom_positions(cfg)
+        self.m = Model(cfg, self.R)
+        self.gs = scf(self.m, tol=cfg.scf_tol)
+        self.H = self.m.hamiltonian_dense(self.gs.V)
+        self.G = self.m.G_matrix()
+        self.ctx = Context.from_config(cfg)
+        self.Psi_t = T(self.gs.Psi.T)
+        self.eps_t = T(self.gs.eps)
+        self.V_t = T(self.gs.V)
+        self.rho_t = T(self.gs.rho)
+        self.G_t = T(self.G.T)
+
+    def draws(self, k, n):
+        return sketch_draws(self.cfg.seed, k, n, self.cfg.sketch_r)
+
+
+_cache = {}
+
+
+def system(name):
+    if name not in _cache:
+        cfg = small_config() if name == "tiny4" else get_config(name)
+        _cache[name] = Sys(cfg)
+    return _cache[name]
+
+
+@pytest.fixture(scope="module", params=["tiny4", "c0_1d_tiny"])
+def sysx(request):
+    return system(request.param)
+
+
+# ---------------------------------------------------------------- building blocks
+def test_fourier_operators(sysx):
+    s = sysx
+    rng = np.random.default_rng(11)
+    for ncol in (1, 2, 5):          # odd counts exercise the unpaired tail column
+        X = rng.standard_normal((s.m.Ng, ncol))
+        Xt = T(X.T)
+        Y = s.ctx.fourier_apply(Xt, 0).cpu().numpy().T
+        assert rel(Y, s.m.kinetic(X)) < 1e-12
+        Y = s.ctx.fourier_apply(Xt, 1).cpu().numpy().T
+        assert rel(Y, s.m.yukawa(X)) < 1e-12
+        shifts = rng.uniform(-0.1, 0.1, ncol)
+        Y = s.ctx.fourier_apply(Xt, 0, diag=s.V_t, shift=T(shifts)).cpu().numpy().T
+        ref = s.m.kinetic(X) + (s.gs.V[:, None] - shifts[None, :]) * X
+        assert rel(Y, ref) < 1e-12
+        assert rel(Y, (s.H @ X) - shifts[None, :] * X) < 1e-11
+
+
+def test_gemms(sysx):
+    s = sysx
+    rng = np.random.default_rng(12)
+    for n in (1, 7, 33, 70):
+        Y = rng.standard_normal((s.m.Ng, n))
+        C = s.ctx.gemm_tn(s.Psi_t, T(Y.T), alpha=s.m.dV).cpu().numpy().T
+        assert rel(C, s.m.dV * s.gs.Psi.T @ Y) < 1e-12
+        Cm = rng.standard_normal((s.cfg.n_occ, n))
+        Z0 = rng.standard_normal((s.m.Ng, n))
+        Z = s.ctx.gemm_nn(s.Psi_t, T(Cm.T), C=T(Z0.T), alpha=-1.0, beta=1.0).cpu().numpy().T
+        assert rel(Z, Z0 - s.gs.Psi @ Cm) < 1e-12
+
+
+def test_perturbation_matrix(sysx):
+    s = sysx
+    G = s.ctx.perturbations(s.R).cpu().numpy().T
+    assert rel(G, s.G) < 1e-12
+
+
+# ---------------------------------------------------------------- Alg. 2
+def test_compress_pivots_bit_exact(sysx):
+    s = sysx
+    for k in range(2):
+        th, nu = s.draws(k, s.G.shape[1])
+        S_o, Xi_o, qr = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+        S_g, Xi_g, n = s.ctx.compress(s.Psi_t, s.G_t, th, nu, id_eps=s.cfg.id_eps)
+        assert n == len(S_o)
+        assert np.array_equal(S_g.cpu().numpy(), S_o)
+        assert rel(Xi_g.cpu().numpy().T, Xi_o) < 1e-9
+        # fixed-N_mu mode (Table 1 style), odd count
+        nf = max(3, (len(S_o) // 2) | 1)
+        S_o2, Xi_o2, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, 0.0, n_fixed=nf)
+        S_g2, Xi_g2, n2 = s.ctx.compress(s.Psi_t, s.G_t, th, nu, n_mu_fixed=nf)
+        assert n2 == nf and np.array_equal(S_g2.cpu().numpy(), S_o2)
+        assert rel(Xi_g2.cpu().numpy().T, Xi_o2) < 1e-9
+
+
+# ---------------------------------------------------------------- Alg. 3
+def test_apply_chi0_matches_direct_solves(sysx):
+    s = sysx
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    W_o = oacp.compressed_W(s.m, s.H, s.gs.Psi, s.gs.eps[: s.cfg.n_occ], S_o, Xi_o, s.cfg.n_cheb)
+    W_g, info = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, T(S_o, torch.int32), T(Xi_o.T), s.cfg.n_cheb,
+                                 cg_tol=s.cfg.cg_tol)
+    assert info["n_solved"] == s.cfg.n_cheb * len(S_o)
+    assert info["max_rel_res"] <= s.cfg.cg_tol
+    assert rel(W_g.cpu().numpy().T, W_o) < 1e-9
+
+
+def test_apply_chi0_sharding_is_bitwise(sysx):
+    """RHS sharding across GPUs (even shard sizes) reproduces the unsharded W bit for bit."""
+    s = sysx
+    th, nu = s.draws(1, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    St, Xt = T(S_o, torch.int32), T(Xi_o.T)
+    W_full, _ = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    n = len(S_o)
+    cut = (n // 2) & ~1
+    W_sh = torch.zeros_like(W_full)
+    s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb, mu_range=(0, cut), W=W_sh)
+    s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb, mu_range=(cut, n), W=W_sh)
+    assert torch.equal(W_full, W_sh)
+
+
+# ---------------------------------------------------------------- Alg. 4 + D
+def _dyson_parity(s, n_outer=None):
+    cfg = s.cfg
+    n_outer = n_outer or cfg.n_outer
+    res = oacp.acp_dyson(s.m, s.H, s.gs.Psi, s.gs.eps[: cfg.n_occ], s.G, cfg.n_cheb, n_outer, cfg.id_eps,
+                         s.draws)
+    D_o = ophonon.dynamical_matrix(s.m, s.gs.rho, s.G, res.U)
+    lam_o = np.linalg.eigvalsh(D_o)
+    n = s.G.shape[1]
+    th = np.stack([s.draws(k, n)[0] for k in range(n_outer)])
+    nu = np.stack([s.draws(k, n)[1] for k in range(n_outer)])
+    U_g, info = s.ctx.dyson(s.Psi_t, s.eps_t, s.V_t, s.G_t, cfg.n_cheb, n_outer, th, nu, id_eps=cfg.id_eps,
+                            cg_tol=cfg.cg_tol)
+    assert info["n_mu"] == res.n_mu
+    D_g, lam_g = s.ctx.dynamical_matrix(s.R, s.rho_t, s.G_t, U_g)
+    return res, D_o, lam_o, U_g.cpu().numpy().T, D_g, lam_g, info
+
+
+def test_dyson_and_dynamical_matrix(sysx):
+    s = sysx
+    res, D_o, lam_o, U_g, D_g, lam_g, info = _dyson_parity(s)
+    assert rel(U_g, res.U) < 1e-9
+    assert rel(D_g, D_o) < 1e-8                       # north-star bar
+    assert np.abs(lam_g - lam_o).max() / np.abs(lam_o).max() < 1e-7
+    assert np.allclose(info["diff"], res.diff, rtol=1e-6, atol=1e-12)
+
+
+def test_dynamical_matrix_terms_exact(sysx):
+    """D assembly alone (given the oracle's U): pure rounding."""
+    s = sysx
+    U = ors.dyson_dense(s.m, ors.chi0_adler_wiser_matrix(s.m, s.H, s.cfg.n_occ), s.G)
+    D_o = ophonon.dynamical_matrix(s.m, s.gs.rho, s.G, U)
+    D_g, lam_g = s.ctx.dynamical_matrix(s.R, s.rho_t, s.G_t, T(U.T))
+    assert rel(D_g, D_o) < 1e-11
+    assert np.abs(lam_g - np.linalg.eigvalsh(D_o)).max() < 1e-12 * np.abs(lam_g).max()
+    D4, _ = s.ctx.dynamical_matrix(s.R, s.rho_t, s.G_t, T(U.T), masses=4.0 * np.ones(s.m.NA))
+    assert rel(D4, D_o / 4) < 1e-11
+
+
+# ---------------------------------------------------------------- ground state
+def test_ground_state(sysx):
+    s = sysx
+    out = s.ctx.ground_state(s.R, scf_tol=s.cfg.scf_tol)
+    n = s.cfg.n_occ
+    eps_g = out["eps"].cpu().numpy()
+    assert np.abs(eps_g[: n + 1] - s.gs.eps[: n + 1]).max() < 1e-9
+    assert rel(out["rho"].cpu().numpy(), s.gs.rho) < 1e-9
+    assert rel(out["V"].cpu().numpy(), s.gs.V) < 1e-9
+    assert rel(out["G"].cpu().numpy().T, s.G) < 1e-12
+    Psi = out["Psi"].cpu().numpy().T
+    assert np.abs(s.m.dV * Psi.T @ Psi - np.eye(n)).max() < 1e-10
+
+
+# ---------------------------------------------------------------- full size (bench config)
+@pytest.mark.slow
+def test_bench_config_end_to_end():
+    """configs[1] at full size in the configuration bench.py times: GPU ground state ->
+    GPU Alg. 4 -> GPU D, against the oracle's own pipeline."""
+    s = system("c1_1d_insulator")
+    res, D_o, lam_o, U_g, D_g, lam_g, info = _dyson_parity(s)
+    assert rel(D_g, D_o) < 1e-8
+    assert np.abs(lam_g - lam_o).max() / np.abs(lam_o).max() < 1e-7
+    out = s.ctx.ground_state(s.R, scf_tol=s.cfg.scf_tol)
+    assert rel(out["rho"].cpu().numpy(), s.gs.rho) < 1e-9
