@@ -1,0 +1,343 @@
+"""bench.py -- time the ACP hot path (Alg. 4 + dynamical matrix) on B200.
+
+One STEP = the whole hot path on one synthetic system: n_outer outer iterations of
+Alg. 4 (compress with SRFT + QRCP, N_c x N_mu projected Sternheimer solves, W,
+SMW update) followed by the dynamical-matrix assembly and its eigenvalues.  The
+ground state is prepared once, untimed (it is the input of the hot path).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl acp|reference]
+
+Metric (BASELINE.json): Sternheimer solves/s (whole job), with time-to-D in ms
+and the roofline fraction of the dominant kernel.  Multi-GPU runs (torchrun) shard
+the mu-columns of every outer iteration across ranks and all-gather W over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ACP dynamical-matrix time-to-solution; Sternheimer solves/s; % HBM roofline"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    d = json.load(open(p)) if os.path.exists(p) else {}
+    hbm = d.get("hbm_gbs")
+    bf16 = d.get("bf16_tflops")
+    src = "measured (MEASURED_PEAKS.json)"
+    if hbm is None:
+        hbm, bf16, src = 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+    # FP64 tensor (DMMA) peak: measured bf16 x guide nominal ratio 45 TF / 2250 TF
+    fp64 = bf16 * 45.0 / 2250.0
+    return dict(hbm_gbs=hbm, fp64_tflops=fp64, src=src)
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.15)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]), "samples": len(rows),
+                "reasons": reasons}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ oracle (reference arm / cpu baseline)
+def oracle_sample(cfg, R, outer_k: int = 0, state=None):
+    """One outer iteration of the oracle's Alg. 4 (compress + direct compressed solves + W + SMW)."""
+    from workloads import sketch_draws
+    from oracle.model import Model
+    from oracle.scf import scf
+    from oracle import acp as oacp
+    if state is None:
+        m = Model(cfg, R)
+        gs = scf(m, tol=cfg.scf_tol)
+        state = dict(m=m, gs=gs, H=m.hamiltonian_dense(gs.V), G=m.G_matrix())
+    m, gs, H, G = state["m"], state["gs"], state["H"], state["G"]
+    th, nu = sketch_draws(cfg.seed, outer_k, G.shape[1], cfg.sketch_r)
+    t0 = time.perf_counter()
+    S, Xi, _ = oacp.compress(m, gs.Psi, G, th, nu, cfg.id_eps)
+    W = oacp.compressed_W(m, H, gs.Psi, gs.eps[: cfg.n_occ], S, Xi, cfg.n_cheb)
+    oacp.smw_update(m, G, W, S)
+    dt = time.perf_counter() - t0
+    return dt, cfg.n_cheb * len(S), state
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d.get("num_threads", 1) for d in threadpool_info() if d.get("user_api") == "blas"]
+        return int(max(n)) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from workloads import atom_positions
+    R = atom_positions(cfg)
+    state = None
+    for _ in range(args.warmup):
+        _, _, state = oracle_sample(cfg, R, 0, state)
+    tot_t, tot_s = 0.0, 0
+    for k in range(args.steps):
+        dt, ns, state = oracle_sample(cfg, R, k % cfg.n_outer, state)
+        tot_t += dt
+        tot_s += ns
+    v = tot_s / tot_t
+    cores = blas_threads()
+    sample = f"one outer iteration of Alg. 4 per step (compress + {cfg.n_cheb} x N_mu direct solves + W + SMW)"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg.name},
+            "cpu_baseline": {"value": v, "unit": "solves/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_acp(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from workloads import atom_positions, sketch_draws
+    from paper_1605_08021_b200 import Context
+    from paper_1605_08021_b200.parallel import dyson_sharded
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    ctx = Context.from_config(cfg, device=local)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream)
+    R = atom_positions(cfg)
+    t0 = time.perf_counter()
+    gs = ctx.ground_state(R, scf_tol=cfg.scf_tol)
+    t_gs = time.perf_counter() - t0
+    n = cfg.n_pert
+    dr = [sketch_draws(cfg.seed, k, n, cfg.sketch_r) for k in range(cfg.n_outer)]
+    th = np.stack([d[0] for d in dr])
+    nu = np.stack([d[1] for d in dr])
+    Psi, eps, V, rho, G = gs["Psi"], gs["eps"], gs["V"], gs["rho"], gs["G"]
+    flush = torch.empty(2 * L2_BYTES // 8, dtype=torch.float64, device=dev)
+
+    def step():
+        if world > 1:
+            U, info = dyson_sharded(ctx, Psi, eps, V, G, cfg.n_cheb, cfg.n_outer, lambda k: dr[k], cfg.id_eps,
+                                    cfg.cg_tol)
+            solves = info["local_solves"]
+            t = torch.tensor([solves], device=dev)
+            dist.all_reduce(t)
+            solves = int(t.item())
+            info = dict(total_solves=solves, n_mu=info["n_mu"])
+        else:
+            U, info = ctx.dyson(Psi, eps, V, G, cfg.n_cheb, cfg.n_outer, th, nu, id_eps=cfg.id_eps,
+                                cg_tol=cfg.cg_tol)
+        D, lam = ctx.dynamical_matrix(R, rho, G, U)
+        return info, D, lam
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    # ---- timed region: device time per step (CUDA events on the launching stream), L2 flushed between steps
+    clocks = ClockSampler(local)
+    launches0 = ctx.kernel_launches
+    times = []
+    solves = 0
+    info = None
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.nvtx.range_push("acp_step")
+        e0.record(stream)
+        info, D, lam = step()
+        e1.record(stream)
+        torch.cuda.nvtx.range_pop()
+        barrier()
+        times.append(e0.elapsed_time(e1))
+        solves += info["total_solves"]
+    launches = ctx.kernel_launches - launches0
+    clk = clocks.stop()
+    t_ms = float(np.sum(times))
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = solves / (t_ms / 1e3)
+
+    # ---- e2e through the public API with HOST buffers (pinned), copies inside the timed region
+    host = {k: v.cpu().pin_memory() for k, v in dict(Psi=Psi, eps=eps, V=V, rho=rho, G=G).items()}
+    dev_in = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
+    h2d = int(sum(v.numel() * v.element_size() for v in host.values()))
+    d2h = 8 * (n * n + n)
+    e2e_ms = 0.0
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for k in host:
+                dev_in[k].copy_(host[k], non_blocking=True)
+        if world > 1:
+            U, inf2 = dyson_sharded(ctx, dev_in["Psi"], dev_in["eps"], dev_in["V"], dev_in["G"], cfg.n_cheb,
+                                    cfg.n_outer, lambda k: dr[k], cfg.id_eps, cfg.cg_tol)
+        else:
+            U, inf2 = ctx.dyson(dev_in["Psi"], dev_in["eps"], dev_in["V"], dev_in["G"], cfg.n_cheb, cfg.n_outer,
+                                th, nu, id_eps=cfg.id_eps, cg_tol=cfg.cg_tol)
+        D2, lam2 = ctx.dynamical_matrix(R, dev_in["rho"], dev_in["G"], U)   # D, lambda land in host memory
+        e1.record(stream)
+        barrier()
+        e2e_ms += e0.elapsed_time(e1)
+    e2e_ms /= e2e_steps
+    e2e_value = (solves / args.steps) / (e2e_ms / 1e3)
+
+    # ---- live roofline of the hot kernels (same shapes as inside the step)
+    peaks = _peaks()
+    n_mu = info["n_mu"][0]
+    ncols = cfg.n_cheb * ((n_mu + 1) // 2 * 2)
+    X = torch.randn(ncols, ctx.Ng, dtype=torch.float64, device=dev)
+    Y = torch.zeros_like(X)
+    kern = {}
+    reps = 50
+    for which, name in [(0, "K1_fourier_op"), (1, "K2_gemm_tn"), (2, "K3_pcg_update")]:
+        ctx.kernel_bench(which, Psi, V, X, Y, 5)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.kernel_bench(which, Psi, V, X, Y, reps)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        us = 1e3 * e0.elapsed_time(e1) / reps
+        Ng, No = ctx.Ng, cfg.n_occ
+        if which == 0:
+            byts = 16.0 * Ng * ncols
+            kern[name] = dict(bound="hbm", us=us, bytes=byts, achieved=byts / us / 1e3, unit="GB/s",
+                              peak=peaks["hbm_gbs"])
+        elif which == 1:
+            fl = 2.0 * Ng * No * ncols
+            kern[name] = dict(bound="tensor", us=us, flops=fl, achieved=fl / us / 1e6, unit="TFLOP/s",
+                              peak=peaks["fp64_tflops"])
+        else:
+            byts = 24.0 * Ng * ncols
+            kern[name] = dict(bound="hbm", us=us, bytes=byts, achieved=byts / us / 1e3, unit="GB/s",
+                              peak=peaks["hbm_gbs"])
+        kern[name]["frac"] = kern[name]["achieved"] / kern[name]["peak"]
+    dom_name = os.environ.get("ACP_DOMINANT_KERNEL", "K1_fourier_op")
+    dom = kern[dom_name]
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(dom_name)
+    roofline = {"kernel": dom_name, "bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
+                "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic, "peak_source": peaks["src"],
+                "units_per_launch": ncols, "per_unit": ("16*N_g bytes" if dom["bound"] == "hbm" and
+                                                        dom_name.startswith("K1") else
+                                                        "24*N_g bytes" if dom["bound"] == "hbm" else
+                                                        "2*N_g*N_occ flops")}
+
+    # ---- CPU baseline: the oracle, bounded sample, rank 0 at N = 1 only
+    cpu = None
+    if world == 1 and rank == 0 and not args.skip_cpu:
+        dt, ns, _ = oracle_sample(cfg, R, 0)
+        cpu = {"value": ns / dt, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
+               "sample": f"one outer iteration of Alg. 4 ({ns} direct compressed solves + compress + W + SMW), "
+                         f"{dt:.1f} s; ground state untimed"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "time_to_D_ms": t_ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": cfg.name, "N_g": ctx.Ng, "N_A": cfg.n_atoms, "N_occ": cfg.n_occ,
+                           "N_c": cfg.n_cheb, "n_outer": cfg.n_outer, "id_eps": cfg.id_eps, "r": cfg.sketch_r,
+                           "cg_tol": cfg.cg_tol, "n_mu": info["n_mu"], "solves_per_step": solves // args.steps,
+                           "l2": "flushed (256 MiB write) between timed steps",
+                           "ground_state_s": round(t_gs, 2), "parallelism": f"rhs-shard x{world}"},
+                "roofline": roofline, "kernels": kern, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": "solves/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h},
+                "gpu_launches": int(launches), "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1_1d_insulator")
+    ap.add_argument("--impl", default="acp", choices=["acp", "reference"])
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    from workloads import get_config
+    cfg = get_config(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_acp(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -158,6 +158,14 @@ int acp_dyson(acp_context* ctx, const double* d_Psi, const double* d_eps, const 
               const double* d_G, const acp_dyson_opts* opts,
               const double* h_theta, const int* h_nu, double* d_U, double* h_info);
 
+/* One SMW update of Eq. dyson4 for a given compressed operator
+ * chi0~ = W Pi^T (used by the multi-GPU driver after W is all-gathered):
+ *   Y = (I - (K W)(S,:))^{-1} G(S,:)   (N_mu x N_mu LU with partial pivoting),
+ *   d_U = W Y (= U^{k+1} = U~^{k+1} - B),   d_Gp = G + (K W) Y (= v U~^{k+1}; may be NULL).
+ * d_G: N_g x dN_A;  d_S: N_mu int32;  d_W: N_g x N_mu.  ACP_ERR_SINGULAR if the core is singular. */
+int acp_smw_update(acp_context* ctx, const double* d_G, const int* d_S, const double* d_W, int n_mu,
+                   double* d_U, double* d_Gp);
+
 /* ------------------------------------------------------------------------ */
 /* 5. Dynamical matrix (Eqs. SecDeriv/chiterm):
  *    D = (g^T chi g) + delta_IJ int rho d2V_I + d2E_II, divided by sqrt(M_I M_J),
@@ -184,6 +192,18 @@ int acp_gemm_tn(acp_context* ctx, int K, int m, int n, double alpha, const doubl
 /* C (M x n, ld ldc) = beta * C + alpha * A B  with A: M x K (ld lda), B: K x n (ld ldb). */
 int acp_gemm_nn(acp_context* ctx, int M, int K, int n, double alpha, const double* d_A, int lda,
                 const double* d_B, int ldb, double beta, double* d_C, int ldc);
+
+/* Enqueue `reps` back-to-back launches of one hot-path kernel on the context
+ * stream and return WITHOUT synchronising, so the caller can bracket them with
+ * its own CUDA events on that stream (bench.py's live roofline timing).
+ *   which = 0: K1 Fourier operator y = (H - 0) x on n_cols columns (d_X -> d_Y, potential d_V)
+ *           1: K2 split-K DMMA projection Psi^T X (partials into workspace)
+ *           2: K3 fused update Y <- (X - Psi C) + beta Y (NN DMMA tile + PCG epilogue)
+ * d_Psi: N_g x n_occ; d_X, d_Y: N_g x n_cols. */
+int acp_kernel_bench(acp_context* ctx, int which, const double* d_Psi, const double* d_V, const double* d_X,
+                     int n_cols, double* d_Y, int reps);
+/* Stream the library launches on (cudaStream_t as void*). */
+void* acp_get_stream(const acp_context* ctx);
 
 #ifdef __cplusplus
 }

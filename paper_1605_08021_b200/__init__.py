@@ -3,8 +3,18 @@
 Lin, Xu & Ying, arXiv 1605.08021.  The numerical work lives in the in-tree CUDA
 library ``libacp_b200.so`` (sources under ``csrc/``, C ABI in
 ``include/acp_b200.h``); ``acp.py`` is a thin ctypes binding with the same
-call names.  There is no CPU fallback.
+call names.  There is no CPU fallback: the binding raises ImportError when
+the library is missing.  (Loaded lazily so that ``python -m
+paper_1605_08021_b200.build`` can run before the library exists.)
 """
-from .acp import AcpError, Context, EXPORTED, LIB_PATH, version  # noqa: F401
+_EXPORTS = ("AcpError", "Context", "EXPORTED", "LIB_PATH", "version")
 
-__all__ = ["AcpError", "Context", "EXPORTED", "LIB_PATH", "version"]
+
+def __getattr__(name):
+    if name in _EXPORTS:
+        from . import acp
+        return getattr(acp, name)
+    raise AttributeError(name)
+
+
+__all__ = list(_EXPORTS)

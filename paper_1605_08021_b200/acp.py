@@ -66,10 +66,13 @@ _sig = {
     "acp_apply_chi0": [_V, _V, _V, _V, _V, _V, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                        ctypes.c_double, ctypes.c_int, _V, _dp],
     "acp_dyson": [_V, _V, _V, _V, _V, ctypes.POINTER(acp_dyson_opts), _dp, _ip, _V, _dp],
+    "acp_smw_update": [_V, _V, _V, _V, ctypes.c_int, _V, _V],
     "acp_dynamical_matrix": [_V, _dp, _V, _V, _V, _dp, _dp, _dp],
     "acp_fourier_apply": [_V, _V, ctypes.c_int, ctypes.c_int, ctypes.c_double, _V, _V, _V],
     "acp_gemm_tn": [_V, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, _V, ctypes.c_int, _V,
                     ctypes.c_int, _V],
+    "acp_kernel_bench": [_V, ctypes.c_int, _V, _V, _V, ctypes.c_int, _V, ctypes.c_int],
+    "acp_get_stream": [_V],
     "acp_gemm_nn": [_V, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, _V, ctypes.c_int, _V,
                     ctypes.c_int, ctypes.c_double, _V, ctypes.c_int],
 }
@@ -80,6 +83,7 @@ for _name, _args in _sig.items():
 _lib.acp_last_error.restype = ctypes.c_char_p
 _lib.acp_version.restype = ctypes.c_char_p
 _lib.acp_kernel_launches.restype = ctypes.c_longlong
+_lib.acp_get_stream.restype = ctypes.c_void_p
 
 EXPORTED = list(_sig)
 
@@ -231,6 +235,17 @@ class Context:
                        max_rel_res=float(info[3]), n_mu=[int(x) for x in per[:, 0]],
                        diff=[float(x) for x in per[:, 1]], cg_iter=[int(x) for x in per[:, 2]])
 
+    def smw_update(self, G, S, W, U=None, Gp=None):
+        """Eq. dyson4: returns (U, Gp) with U = W Y, Gp = G + (K W) Y."""
+        self._pre()
+        if U is None:
+            U = self._empty(self.n_pert, self.Ng)
+        if Gp is None:
+            Gp = self._empty(self.n_pert, self.Ng)
+        self._check(_lib.acp_smw_update(self._h, _ptr(G), _ptr(S.contiguous()), _ptr(W), W.shape[0], _ptr(U),
+                                        _ptr(Gp)), "acp_smw_update")
+        return U, Gp
+
     # -- 5. dynamical matrix --------------------------------------------
     def dynamical_matrix(self, R, rho, G, U, masses=None):
         self._pre()
@@ -245,6 +260,17 @@ class Context:
                                               D.ctypes.data_as(_dp), lam.ctypes.data_as(_dp)),
                     "acp_dynamical_matrix")
         return D.T.copy(), lam  # column-major -> row-major (D is symmetric anyway)
+
+    # -- streams / timing -------------------------------------------------
+    def set_stream(self, stream: Optional["torch.cuda.Stream"]):
+        """Launch on `stream` (a non-default torch stream, so graphs can be captured)."""
+        self._check(_lib.acp_set_stream(self._h, None if stream is None else ctypes.c_void_p(stream.cuda_stream)),
+                    "acp_set_stream")
+
+    def kernel_bench(self, which: int, Psi, V, X, Y, reps: int):
+        """Enqueue `reps` launches of hot kernel `which` (0: K1, 1: K2, 2: K3); no sync."""
+        self._check(_lib.acp_kernel_bench(self._h, which, _ptr(Psi), _ptr(V), _ptr(X), X.shape[0], _ptr(Y), reps),
+                    "acp_kernel_bench")
 
     # -- building blocks ------------------------------------------------
     def fourier_apply(self, X, which: int, tau: float = 0.0, diag=None, shift=None):

@@ -137,6 +137,15 @@ int acp_dyson(acp_context* ctx, const double* d_Psi, const double* d_eps, const 
     return guarded(ctx, [&] { acp::dyson(ctx, d_Psi, d_eps, d_V, d_G, *opts, h_theta, h_nu, d_U, h_info); });
 }
 
+int acp_smw_update(acp_context* ctx, const double* d_G, const int* d_S, const double* d_W, int n_mu, double* d_U,
+                   double* d_Gp) {
+    if (!ctx || !d_G || !d_S || !d_W || !d_U || n_mu < 1) return ACP_ERR_INVALID;
+    return guarded(ctx, [&] {
+        acp::smw_update(ctx, d_G, d_S, d_W, n_mu, d_U, d_Gp);
+        acp::sync(ctx);
+    });
+}
+
 int acp_dynamical_matrix(acp_context* ctx, const double* h_R, const double* d_rho, const double* d_G,
                          const double* d_U, const double* h_masses, double* h_D, double* h_lambda) {
     if (!ctx || !h_R || !d_rho || !d_G || !d_U || !h_D) return ACP_ERR_INVALID;
@@ -177,5 +186,14 @@ int acp_gemm_nn(acp_context* ctx, int M, int K, int n, double alpha, const doubl
         acp::sync(ctx);
     });
 }
+
+int acp_kernel_bench(acp_context* ctx, int which, const double* d_Psi, const double* d_V, const double* d_X,
+                     int n_cols, double* d_Y, int reps) {
+    if (!ctx || !d_Psi || !d_V || !d_X || !d_Y || n_cols < 1 || reps < 1 || which < 0 || which > 2)
+        return ACP_ERR_INVALID;
+    return guarded(ctx, [&] { acp::kernel_bench(ctx, which, d_Psi, d_V, d_X, n_cols, d_Y, reps); });
+}
+
+void* acp_get_stream(const acp_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 }  // extern "C"

@@ -165,6 +165,9 @@ void apply_chi0(acp_context* ctx, const double* Psi, const double* eps, const do
                 const int* S, const double* Xi, int n_mu, int mu_begin, int mu_end, int n_cheb,
                 double tol, int max_iter, double* W, PcgStats* st);
 
+void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* V, const double* X, int n,
+                  double* Y, int reps);
+
 // ---- qrcp.cu ------------------------------------------------------------
 int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols,
              const double* h_theta, const int* h_nu, int r_half, double id_eps, int n_fixed,
@@ -179,6 +182,7 @@ void sym_eig(acp_context* ctx, double* A, int n, double* w, double* V);
 void cholesky(acp_context* ctx, double* A, int n);
 
 // ---- dyson / phonon / scf ----------------------------------------------
+void smw_update(acp_context* ctx, const double* G, const int* S, const double* W, int N, double* U, double* Gp);
 void dyson(acp_context* ctx, const double* Psi, const double* eps, const double* V, const double* G,
            const acp_dyson_opts& o, const double* h_theta, const int* h_nu, double* U, double* h_info);
 void dynamical_matrix(acp_context* ctx, const double* h_R, const double* rho, const double* G,

@@ -53,6 +53,31 @@ static double diff_norm(acp_context* ctx, const double* a, const double* b, size
     return std::sqrt(s);
 }
 
+// Eq. dyson4 given W (N_g x N) and S:  Y = (I - (K W)(S,:))^{-1} G(S,:),  U = W Y,  Gp = G + (K W) Y.
+void smw_update(acp_context* ctx, const double* G, const int* S, const double* W, int N, double* U, double* Gp) {
+    const int Ng = ctx->Ng;
+    const int n = ctx->dim * ctx->sys.n_atoms;
+    double* KW = ctx->wsd("dy_KW", (size_t)Ng * N);
+    double* A = ctx->wsd("dy_A", (size_t)N * N);
+    double* Y = ctx->wsd("dy_Y", (size_t)N * n);
+    double* mK = ctx->wsd("dy_multK", Ng);
+    copy_cols(ctx, mK, multiplier(ctx, MULT_YUKAWA, 0.0), Ng);
+    FopArgs f;
+    f.X = W;
+    f.Y = KW;
+    f.n = N;
+    f.mult = mK;
+    fourier_op(ctx, f);
+    k_smw_gather<<<dim3(cdiv(N, 128), N > n ? N : n), 128, 0, ctx->stream>>>(Ng, N, n, S, KW, G, A, Y);
+    launched(ctx);
+    lu_solve(ctx, A, N, Y, n);
+    gemm_nn(ctx, Ng, N, n, 1.0, W, Ng, Y, N, 0.0, U, Ng);
+    if (Gp) {
+        copy_cols(ctx, Gp, G, (size_t)Ng * n);
+        gemm_nn(ctx, Ng, N, n, 1.0, KW, Ng, Y, N, 1.0, Gp, Ng);
+    }
+}
+
 void dyson(acp_context* ctx, const double* Psi, const double* eps, const double* V, const double* G,
            const acp_dyson_opts& o, const double* h_theta, const int* h_nu, double* U, double* h_info) {
     const int Ng = ctx->Ng;
@@ -66,14 +91,8 @@ void dyson(acp_context* ctx, const double* Psi, const double* eps, const double*
     int* S = ctx->wsi("dy_S", nmu_max);
     double* Xi = ctx->wsd("dy_Xi", (size_t)Ng * nmu_max);
     double* W = ctx->wsd("dy_W", (size_t)Ng * nmu_max);
-    double* KW = ctx->wsd("dy_KW", (size_t)Ng * nmu_max);
-    double* A = ctx->wsd("dy_A", (size_t)nmu_max * nmu_max);
-    double* Y = ctx->wsd("dy_Y", (size_t)nmu_max * n);
     copy_cols(ctx, Gp, G, (size_t)Ng * n);
     fill(ctx, Uprev, (size_t)Ng * n, 0.0);
-    const double* mK = multiplier(ctx, MULT_YUKAWA, 0.0);
-    double* mKc = ctx->wsd("dy_multK", Ng);
-    copy_cols(ctx, mKc, mK, Ng);
     long long total_solves = 0, total_it = 0;
     int max_it = 0;
     double max_res = 0.0;
@@ -82,18 +101,7 @@ void dyson(acp_context* ctx, const double* Psi, const double* eps, const double*
                                o.id_eps, o.n_mu_fixed, nmu_max, S, Xi);
         PcgStats st;
         apply_chi0(ctx, Psi, eps, V, S, Xi, N, 0, N, o.n_cheb, o.cg_tol, o.max_cg_iter, W, &st);
-        FopArgs f;
-        f.X = W;
-        f.Y = KW;
-        f.n = N;
-        f.mult = mKc;
-        fourier_op(ctx, f);
-        k_smw_gather<<<dim3(cdiv(N, 128), N > n ? N : n), 128, 0, ctx->stream>>>(Ng, N, n, S, KW, G, A, Y);
-        launched(ctx);
-        lu_solve(ctx, A, N, Y, n);
-        gemm_nn(ctx, Ng, N, n, 1.0, W, Ng, Y, N, 0.0, U, Ng);
-        copy_cols(ctx, Gp, G, (size_t)Ng * n);
-        gemm_nn(ctx, Ng, N, n, 1.0, KW, Ng, Y, N, 1.0, Gp, Ng);
+        smw_update(ctx, G, S, W, N, U, Gp);
         const double dn = diff_norm(ctx, U, Uprev, (size_t)Ng * n);
         copy_cols(ctx, Uprev, U, (size_t)Ng * n);
         total_solves += st.n_solved;

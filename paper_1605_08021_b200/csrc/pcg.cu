@@ -381,4 +381,45 @@ void apply_chi0(acp_context* ctx, const double* Psi, const double* eps, const do
     launched(ctx);
 }
 
+void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* V, const double* X, int n,
+                  double* Y, int reps) {
+    const int Ng = ctx->Ng, n_occ = ctx->sys.n_occ;
+    const int kchunk = 512;
+    double* Cp = ctx->wsd("kb_Cp", (size_t)cdiv(Ng, kchunk) * n_occ * n);
+    double* C = ctx->wsd("kb_C", (size_t)n_occ * n);
+    double* beta = ctx->wsd("kb_beta", n);
+    int* active = ctx->wsi("kb_active", n);
+    double* mH = ctx->wsd("kb_multH", Ng);
+    copy_cols(ctx, mH, multiplier(ctx, MULT_KINETIC, 0.0), Ng);
+    fill(ctx, C, (size_t)n_occ * n, 1e-3);
+    fill(ctx, beta, n, 0.5);
+    ACP_CUDA(cudaMemsetAsync(active, 0, n * sizeof(int), ctx->stream));
+    // all columns active
+    {
+        std::vector<int> ones(n, 1);
+        ACP_CUDA(cudaMemcpyAsync(active, ones.data(), n * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+        ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    for (int r = 0; r < reps; ++r) {
+        if (which == 0) {
+            FopArgs f;
+            f.X = X;
+            f.Y = Y;
+            f.n = n;
+            f.mult = mH;
+            f.diag = V;
+            f.active = active;
+            f.dots = nullptr;
+            fourier_op(ctx, f);
+        } else if (which == 1) {
+            gemm_tn_partial(ctx, Ng, n_occ, n, Psi, Ng, X, Ng, Cp, kchunk);
+        } else {
+            EpBeta ep{X, Y, beta, active, Ng, 0};
+            dim3 ugrid(cdiv(Ng, NN_BM), cdiv(n, NN_BN));
+            k_pcg_update<EpBeta><<<ugrid, 128, 0, ctx->stream>>>(Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
+            launched(ctx);
+        }
+    }
+}
+
 }  // namespace acp

@@ -10,6 +10,8 @@
 #include "gemm.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -339,7 +341,9 @@ void ground_state(acp_context* ctx, const double* h_R, const acp_scf_opts& o, do
     double* fres = ctx->wsd("gs_f", Ng);
     double* rout = ctx->wsd("gs_rout", Ng);
     double* diff = ctx->wsd("gs_diff", Ng);
-    int nh = 0;  // entries in history (ring of hist+1 slots, oldest first)
+    const bool debug = getenv("ACP_DEBUG") != nullptr;
+    long passes_total = 0;
+    std::vector<int> order;  // history slots, oldest first (ring of hist+1 slots)
     double err = 1e300;
     int it = 0;
     for (it = 1; it <= o.max_scf_iter; ++it) {
@@ -358,19 +362,29 @@ void ground_state(acp_context* ctx, const double* h_R, const acp_scf_opts& o, do
         const double etol = std::max(o.eig_tol, std::min(1e-4, 1e-2 * err));
         copy_cols(ctx, E.Y, E.X, tot);
         E.rayleigh_ritz(V, E.Y);
+        double rprev = 1e300;
         for (int pass = 0; pass < 400; ++pass) {
             double rmax = 0.0;
-            for (int j = 0; j <= n_occ && j < nb; ++j) rmax = std::max(rmax, std::sqrt(E.hres[j] * ctx->dV));
+            for (int j = 0; j < n_occ; ++j) rmax = std::max(rmax, std::sqrt(E.hres[j] * ctx->dV));
             if (rmax <= etol) break;
+            if (rmax > 0.9 * rprev && rmax < 1e-11) break;  // rounding floor reached
+            rprev = rmax;
             const double a = E.hw[nb - 1];
             const double a0 = E.hw[0];
             E.filter(V, 40, a, b, a0);
+            ++passes_total;
             E.rayleigh_ritz(V, E.Y);
         }
         // rho_out
         k_density<<<cdiv(Ng, 256), 256, 0, ctx->stream>>>(Ng, n_occ, ctx->sys.occ, E.X, rout);
         launched(ctx);
         err = std::sqrt(reduce(ctx, rout, rin, Ng, 2) / reduce(ctx, rin, nullptr, Ng, 1));
+        if (debug) {
+            double rmax = 0.0;
+            for (int j = 0; j <= n_occ && j < nb; ++j) rmax = std::max(rmax, std::sqrt(E.hres[j] * ctx->dV));
+            fprintf(stderr, "[acp scf] it %4d  res %.3e  eig-res(occ+lumo) %.2e  passes %ld  gap %.6f\n", it, err, rmax,
+                    passes_total, E.hw[n_occ] - E.hw[n_occ - 1]);
+        }
         if (err <= o.scf_tol) break;
         // f = Kerker(rho_out - rho_in)
         axpby(ctx, Ng, 1.0, rout, 0.0, diff);
@@ -381,25 +395,31 @@ void ground_state(acp_context* ctx, const double* h_R, const acp_scf_opts& o, do
         fp.n = 1;
         fp.mult = multKer;
         fourier_op(ctx, fp);
-        // push (rin, f) into history
-        if (nh == hist + 1) {
-            // drop oldest: shift columns left
-            copy_cols(ctx, Xh, Xh + Ng, (size_t)Ng * hist);
-            copy_cols(ctx, Fh, Fh + Ng, (size_t)Ng * hist);
-            nh = hist;
+        // push (rin, f) into the history ring (slot order kept on the host; no overlapping copies)
+        int slot;
+        if ((int)order.size() == hist + 1) {
+            slot = order.front();
+            order.erase(order.begin());
+        } else {
+            slot = (int)order.size();
         }
-        copy_cols(ctx, Xh + (size_t)nh * Ng, rin, Ng);
-        copy_cols(ctx, Fh + (size_t)nh * Ng, fres, Ng);
-        nh += 1;
+        order.push_back(slot);
+        copy_cols(ctx, Xh + (size_t)slot * Ng, rin, Ng);
+        copy_cols(ctx, Fh + (size_t)slot * Ng, fres, Ng);
+        const int nh = (int)order.size();
         if (nh >= 2) {
             const int k = nh - 1;
             for (int i = 0; i < k; ++i) {
-                axpby(ctx, Ng, 1.0, Xh + (size_t)(i + 1) * Ng, 0.0, dX + (size_t)i * Ng);
-                axpby(ctx, Ng, -1.0, Xh + (size_t)i * Ng, 1.0, dX + (size_t)i * Ng);
-                axpby(ctx, Ng, 1.0, Fh + (size_t)(i + 1) * Ng, 0.0, dF + (size_t)i * Ng);
-                axpby(ctx, Ng, -1.0, Fh + (size_t)i * Ng, 1.0, dF + (size_t)i * Ng);
+                const double* x1 = Xh + (size_t)order[i + 1] * Ng;
+                const double* x0 = Xh + (size_t)order[i] * Ng;
+                const double* f1 = Fh + (size_t)order[i + 1] * Ng;
+                const double* f0 = Fh + (size_t)order[i] * Ng;
+                axpby(ctx, Ng, 1.0, x1, 0.0, dX + (size_t)i * Ng);
+                axpby(ctx, Ng, -1.0, x0, 1.0, dX + (size_t)i * Ng);
+                axpby(ctx, Ng, 1.0, f1, 0.0, dF + (size_t)i * Ng);
+                axpby(ctx, Ng, -1.0, f0, 1.0, dF + (size_t)i * Ng);
             }
-            // normal equations (dF^T dF + reg) gamma = dF^T f
+            // least squares min ||f - dF gamma|| via the normal equations, regularised
             gemm_tn(ctx, Ng, k, k, 1.0, dF, Ng, dF, Ng, Gm);
             gemm_tn(ctx, Ng, k, 1, 1.0, dF, Ng, fres, Ng, gv);
             std::vector<double> hG((size_t)k * k);
@@ -422,8 +442,11 @@ void ground_state(acp_context* ctx, const double* h_R, const acp_scf_opts& o, do
         launched(ctx);
     }
     if (err > o.scf_tol)
-        throw Error(ACP_ERR_NOT_CONVERGED, "SCF residual " + std::to_string(err) + " after " +
-                                               std::to_string(o.max_scf_iter) + " iterations");
+    {
+        char buf[160];
+        snprintf(buf, sizeof(buf), "SCF residual %.3e after %d iterations (tol %.1e)", err, o.max_scf_iter, o.scf_tol);
+        throw Error(ACP_ERR_NOT_CONVERGED, buf);
+    }
     copy_cols(ctx, Psi, E.X, (size_t)Ng * n_occ);
     copy_cols(ctx, eps, E.w, nb);
     copy_cols(ctx, rho, rout, Ng);
