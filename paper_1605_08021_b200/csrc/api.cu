@@ -53,6 +53,7 @@ int acp_create(const acp_system* sys, int device, acp_context** out) {
         ACP_CUDA(cudaSetDevice(device));
         ACP_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
         ctx->stream = ctx->own_stream;
+        ACP_CUDA(cudaMallocHost(&ctx->pinned, 4096));
         acp::fft_init(ctx);
     } catch (const Error& e) {
         int code = e.code;
@@ -67,9 +68,12 @@ int acp_destroy(acp_context* ctx) {
     if (!ctx) return ACP_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     for (auto& kv : ctx->bufs)
         if (kv.second.ptr) cudaFree(kv.second.ptr);
     acp::fft_free(ctx);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return ACP_OK;

@@ -70,6 +70,14 @@ struct acp_context {
     double* d_mult = nullptr;    // scratch multiplier table (N)
 
     std::map<std::string, acp::DevBuf> bufs;
+    void* pinned = nullptr;  // 4 KiB pinned host scratch for small device->host reads
+
+    // Instantiated CUDA graphs keyed by (kernel sequence, shapes, pointers): re-used across calls.
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        long long launches = 0;
+    };
+    std::map<std::string, GraphEntry> graphs;
 
     // Workspace of at least `bytes` bytes under `name` (contents not preserved on growth).
     void* ws(const std::string& name, size_t bytes) {
@@ -103,6 +111,37 @@ inline void launched(acp_context* ctx, int n = 1) {
 inline void sync(acp_context* ctx) { ACP_CUDA(cudaStreamSynchronize(ctx->stream)); }
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// Capture `body` (a sequence of launches on ctx->stream) into a graph once per key and return
+// the instantiated executable.  The key must encode every shape and pointer the launches use.
+template <class F>
+cudaGraphExec_t graph_cached(acp_context* ctx, const std::string& key, F&& body) {
+    auto it = ctx->graphs.find(key);
+    if (it != ctx->graphs.end()) return it->second.exec;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t e = nullptr;
+    const long long before = ctx->launches;
+    ACP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        body();
+    } catch (...) {
+        cudaStreamEndCapture(ctx->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    ACP_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    ACP_CUDA(cudaGraphInstantiate(&e, g, 0));
+    cudaGraphDestroy(g);
+    auto& ent = ctx->graphs[key];
+    ent.exec = e;
+    ent.launches = ctx->launches - before;
+    ctx->launches = before;
+    return e;
+}
+inline void graph_launch(acp_context* ctx, const std::string& key, cudaGraphExec_t e) {
+    ACP_CUDA(cudaGraphLaunch(e, ctx->stream));
+    ctx->launches += ctx->graphs[key].launches;
+}
 
 // ---- fft.cu -------------------------------------------------------------
 FftPlan make_plan(int N);

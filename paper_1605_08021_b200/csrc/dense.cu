@@ -42,17 +42,27 @@ __device__ __forceinline__ void block_argmax_abs(double val, int idx, double* sv
     __syncthreads();
 }
 
-// In-place LU with partial pivoting of A (n x n col-major) applied to B (n x nrhs), then back substitution.
-__global__ void __launch_bounds__(1024) k_lu_solve(double* __restrict__ A, int n, double* __restrict__ B, int nrhs,
-                                                   int* __restrict__ status) {
+// LU with partial pivoting of A (n x n col-major) applied to B (n x nrhs), then back substitution.
+// The working copy of A lives in shared memory when it fits (n <= 160), else in place in global
+// memory.  Only U is kept (B is eliminated alongside), so each step is: pivot search, row swap,
+// rank-1 update with l_ik = A_ik / A_kk formed on the fly -- two barriers per column.
+__global__ void __launch_bounds__(1024) k_lu_solve(double* __restrict__ Ag, int n, double* __restrict__ B, int nrhs,
+                                                   int use_smem, int* __restrict__ status) {
+    extern __shared__ double lsm[];
     __shared__ double sv[32];
     __shared__ int si[32];
     const int tid = threadIdx.x, nt = blockDim.x;
+    double* A = Ag;
+    if (use_smem) {
+        A = lsm;
+        for (long long e = tid; e < (long long)n * n; e += nt) A[e] = Ag[e];
+        __syncthreads();
+    }
     for (int k = 0; k < n; ++k) {
         double bv = -1.0;
         int bi = 1 << 30;
         for (int i = k + tid; i < n; i += nt) {
-            double a = fabs(A[(size_t)k * n + i]);
+            const double a = fabs(A[(size_t)k * n + i]);
             if (a > bv) {
                 bv = a;
                 bi = i;
@@ -66,68 +76,76 @@ __global__ void __launch_bounds__(1024) k_lu_solve(double* __restrict__ A, int n
             return;
         }
         if (p != k) {
-            for (int j = tid; j < n; j += nt) {
-                double t = A[(size_t)j * n + k];
-                A[(size_t)j * n + k] = A[(size_t)j * n + p];
-                A[(size_t)j * n + p] = t;
+            for (int j = tid; j < n + nrhs; j += nt) {
+                double* base = (j < n) ? A + (size_t)j * n : B + (size_t)(j - n) * n;
+                const double t = base[k];
+                base[k] = base[p];
+                base[p] = t;
             }
-            for (int j = tid; j < nrhs; j += nt) {
-                double t = B[(size_t)j * n + k];
-                B[(size_t)j * n + k] = B[(size_t)j * n + p];
-                B[(size_t)j * n + p] = t;
-            }
+            __syncthreads();
         }
-        __syncthreads();
         const double piv = A[(size_t)k * n + k];
-        for (int i = k + 1 + tid; i < n; i += nt) A[(size_t)k * n + i] /= piv;
-        __syncthreads();
-        const int rows = n - k - 1;
-        const int cols = n - k - 1 + nrhs;
-        for (long long e = tid; e < (long long)rows * cols; e += nt) {
-            const int i = k + 1 + (int)(e % rows);
-            const int jj = (int)(e / rows);
-            const double l = A[(size_t)k * n + i];
-            if (jj < n - k - 1) {
-                const int j = k + 1 + jj;
-                A[(size_t)j * n + i] -= l * A[(size_t)j * n + k];
-            } else {
-                const int j = jj - (n - k - 1);
-                B[(size_t)j * n + i] -= l * B[(size_t)j * n + k];
-            }
+        // rank-1 update: warps over columns (trailing A columns, then B columns), lanes over rows
+        const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+        const int ncols = (n - k - 1) + nrhs;
+        for (int jj = warp; jj < ncols; jj += nwarp) {
+            double* colj = (jj < n - k - 1) ? A + (size_t)(k + 1 + jj) * n : B + (size_t)(jj - (n - k - 1)) * n;
+            const double akj = colj[k];
+            for (int i = k + 1 + lane; i < n; i += 32) colj[i] -= (A[(size_t)k * n + i] / piv) * akj;
         }
         __syncthreads();
     }
-    for (int k = n - 1; k >= 0; --k) {
-        const double d = A[(size_t)k * n + k];
-        for (int j = tid; j < nrhs; j += nt) B[(size_t)j * n + k] /= d;
-        __syncthreads();
-        for (long long e = tid; e < (long long)k * nrhs; e += nt) {
-            const int i = (int)(e % k), j = (int)(e / k);
-            B[(size_t)j * n + i] -= A[(size_t)k * n + i] * B[(size_t)j * n + k];
+    // back substitution: warps over right-hand sides, lanes over rows
+    {
+        const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+        for (int k = n - 1; k >= 0; --k) {
+            const double d = A[(size_t)k * n + k];
+            for (int j = warp; j < nrhs; j += nwarp) {
+                double* bj = B + (size_t)j * n;
+                const double x = bj[k] / d;
+                __syncwarp();
+                if (lane == 0) bj[k] = x;
+                for (int i = lane; i < k; i += 32) bj[i] -= A[(size_t)k * n + i] * x;
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
     if (tid == 0) *status = 0;
 }
 
 void lu_solve(acp_context* ctx, double* A, int n, double* B, int nrhs) {
     int* st = ctx->wsi("lu_status", 1);
-    k_lu_solve<<<1, 1024, 0, ctx->stream>>>(A, n, B, nrhs, st);
+    const size_t bytes = (size_t)n * n * sizeof(double);
+    const int use_smem = bytes <= 200 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        ACP_CUDA(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    k_lu_solve<<<1, 1024, use_smem ? bytes : 0, ctx->stream>>>(A, n, B, nrhs, use_smem, st);
     launched(ctx);
-    int h = 0;
-    ACP_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    int* hp = static_cast<int*>(ctx->pinned);
+    ACP_CUDA(cudaMemcpyAsync(hp, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int h = *hp;
     if (h != 0) throw Error(ACP_ERR_SINGULAR, "singular matrix in LU solve (n = " + std::to_string(n) + ")");
 }
 
 // Cyclic (round-robin ordered) Jacobi: A (n x n col-major, symmetric) -> eigenvalues w (ascending),
 // eigenvectors V (n x n col-major) if V != nullptr.  Work arrays in global memory.
-__global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, int n, double* __restrict__ V,
+__global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ Ag, int n, double* __restrict__ V,
                                                  double* __restrict__ w, int* __restrict__ order,
-                                                 double* __restrict__ rot, int max_sweeps) {
+                                                 double* __restrict__ rot, int max_sweeps, int use_smem) {
+    extern __shared__ double jsm[];
     __shared__ double red[32];
     __shared__ int s_done;
     const int tid = threadIdx.x, nt = blockDim.x;
+    double* A = Ag;
+    if (use_smem) {
+        A = jsm;
+        for (long long e = tid; e < (long long)n * n; e += nt) A[e] = Ag[e];
+        __syncthreads();
+    }
     const int m = (n % 2) ? n + 1 : n;  // padded size for the tournament (index n is a dummy)
     if (V)
         for (long long e = tid; e < (long long)n * n; e += nt) V[e] = ((e % n) == (e / n)) ? 1.0 : 0.0;
@@ -136,12 +154,12 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, int n, 
     for (int sweep = 0; sweep < max_sweeps; ++sweep) {
         // off-diagonal and total Frobenius norms
         double off = 0.0, tot = 0.0;
-        for (long long e = tid; e < (long long)n * n; e += nt) {
-            const int i = (int)(e % n), j = (int)(e / n);
-            const double a = A[e];
-            tot += a * a;
-            if (i != j) off += a * a;
-        }
+        for (int j = tid >> 5; j < n; j += nt >> 5)
+            for (int i = tid & 31; i < n; i += 32) {
+                const double a = A[(size_t)j * n + i];
+                tot += a * a;
+                if (i != j) off += a * a;
+            }
         for (int o = 16; o > 0; o >>= 1) {
             off += __shfl_xor_sync(0xffffffffu, off, o);
             tot += __shfl_xor_sync(0xffffffffu, tot, o);
@@ -161,7 +179,9 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, int n, 
         if (tid == 0) {
             double s = 0.0;
             for (int i = 0; i < nt / 32; ++i) s += red[i];
-            s_done = (offs <= 1e-32 * s) ? 1 : 0;
+            // converged when the off-diagonal Frobenius norm is below 1e-13 of the total:
+            // eigenvalue errors are second order in it (<= 1e-26 relative)
+            s_done = (offs <= 1e-26 * s) ? 1 : 0;
         }
         __syncthreads();
         if (s_done) break;
@@ -192,9 +212,9 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, int n, 
                 rot[4 * k + 3] = q;
             }
             __syncthreads();
-            // columns: A <- A J
-            for (long long e = tid; e < (long long)np * n; e += nt) {
-                const int k = (int)(e / n), i = (int)(e % n);
+            // columns: A <- A J   (warps over pairs, lanes over rows)
+            for (int k = tid >> 5; k < np; k += nt >> 5)
+                for (int i = tid & 31; i < n; i += 32) {
                 const int p = (int)rot[4 * k + 2], q = (int)rot[4 * k + 3];
                 if (q >= n) continue;
                 const double c = rot[4 * k], s = rot[4 * k + 1];
@@ -209,8 +229,8 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, int n, 
             }
             __syncthreads();
             // rows: A <- J^T A
-            for (long long e = tid; e < (long long)np * n; e += nt) {
-                const int k = (int)(e / n), j = (int)(e % n);
+            for (int k = tid >> 5; k < np; k += nt >> 5)
+                for (int j = tid & 31; j < n; j += 32) {
                 const int p = (int)rot[4 * k + 2], q = (int)rot[4 * k + 3];
                 if (q >= n) continue;
                 const double c = rot[4 * k], s = rot[4 * k + 1];
@@ -253,7 +273,14 @@ void sym_eig(acp_context* ctx, double* A, int n, double* w, double* V) {
     double* Vt = V ? ctx->wsd("eig_Vt", (size_t)n * n) : nullptr;
     int* order = ctx->wsi("eig_order", n + 2);
     double* rot = ctx->wsd("eig_rot", 4 * (size_t)(n / 2 + 2));
-    k_jacobi<<<1, 1024, 0, ctx->stream>>>(A, n, Vt, w, order, rot, 60);
+    const size_t bytes = (size_t)n * n * sizeof(double);
+    const int use_smem = bytes <= 200 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        ACP_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    k_jacobi<<<1, 1024, use_smem ? bytes : 0, ctx->stream>>>(A, n, Vt, w, order, rot, 40, use_smem);
     launched(ctx);
     if (V) {
         k_permute_cols<<<cdiv((long long)n * n, 256), 256, 0, ctx->stream>>>(n, Vt, order, V);

@@ -89,6 +89,7 @@ int gemm_tn_partial(acp_context* ctx, int K, int m, int n, const double* A, int 
 void gemm_tn(acp_context* ctx, int K, int m, int n, double alpha, const double* A, int lda, const double* B,
              int ldb, double* C) {
     if (m <= 0 || n <= 0) return;
+    if (launch_tn_cluster(ctx, K, m, n, alpha, A, lda, B, ldb, C, m, NoHook{})) return;
     const int s0 = gemm_tn_splits(K, m, n);
     const int kchunk = cdiv(cdiv(K, s0), TN_BK) * TN_BK;
     double* Cp = ctx->wsd("gemm_tn_part", (size_t)cdiv(K, kchunk) * m * n);

@@ -6,6 +6,8 @@
 // are genuine dense contractions and run here.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace acp {
@@ -74,6 +76,169 @@ __device__ __forceinline__ void nn_tile(int M, int K, int n, const double* __res
                 const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
                 if (row < M && col < n) ep(row, col, acc[i][j][e]);
             }
+}
+
+// ---------------------------------------------------------------------------
+// Split-K TN GEMM with the K-split reduced through distributed shared memory.
+//   C(m x n, ld ldc) = alpha * A(:, m)^T B(:, n),  A: K x m (lda), B: K x n (ldb).
+// One thread-block cluster of CS CTAs (cluster rank = K chunk) computes one BM x 32
+// output tile; every CTA accumulates its K chunk with DMMA (cp.async double-buffered
+// operand tiles), parks the partial tile in its shared memory, and after a cluster
+// barrier each rank sums a slice of the tile over all CS ranks IN RANK ORDER through
+// DSMEM.  No global partials, no atomics: the result depends only on (K, CS), not on n.
+// `hook(col)` runs once per output column (rank 0, m-tile 0) after the tile is final.
+constexpr int TC_BN = 32, TC_BK = 32, TC_PAD = 4;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+struct NoHook {
+    __device__ __forceinline__ void operator()(int) const {}
+};
+
+template <int BM>
+constexpr size_t tn_cluster_smem() {
+    return (size_t)2 * (BM + TC_BN) * (TC_BK + TC_PAD) * sizeof(double);
+}
+
+template <int BM, class Hook>
+__global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const double* __restrict__ A, int lda,
+                                                    const double* __restrict__ B, int ldb, int kchunk, double alpha,
+                                                    double* __restrict__ C, int ldc, Hook hook) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) double tsm[];
+    constexpr int LD = TC_BK + TC_PAD;
+    double* As = tsm;                         // [2][BM][LD]
+    double* Bs = tsm + 2 * BM * LD;           // [2][BN][LD]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp & 1, wn = warp >> 1;
+    constexpr int WTM = BM / 2;               // warp tile rows (16 or 32)
+    constexpr int TI = WTM / 8;               // DMMA tiles along m per warp
+    const int CS = gridDim.x;
+    const int rank = blockIdx.x;              // == cluster rank (cluster = (CS,1,1))
+    const int n0 = blockIdx.y * TC_BN, m0 = blockIdx.z * BM;
+    const int kb = rank * kchunk;
+    const int ke = min(K, kb + kchunk);
+    const int nk = ke > kb ? (ke - kb + TC_BK - 1) / TC_BK : 0;
+
+    auto load_stage = [&](int s, int k0) {
+        double* as = As + s * BM * LD;
+        double* bs = Bs + s * TC_BN * LD;
+        for (int c = tid; c < BM * (TC_BK / 2); c += 128) {
+            const int row = c / (TC_BK / 2), kk = 2 * (c % (TC_BK / 2));
+            const int gm = m0 + row, gk = k0 + kk;
+            const bool v = gm < m && gk < ke;
+            cp_async16(as + row * LD + kk, v ? (const void*)(A + (size_t)gm * lda + gk) : (const void*)A, v);
+        }
+        for (int c = tid; c < TC_BN * (TC_BK / 2); c += 128) {
+            const int col = c / (TC_BK / 2), kk = 2 * (c % (TC_BK / 2));
+            const int gn = n0 + col, gk = k0 + kk;
+            const bool v = gn < n && gk < ke;
+            cp_async16(bs + col * LD + kk, v ? (const void*)(B + (size_t)gn * ldb + gk) : (const void*)B, v);
+        }
+    };
+
+    double acc[TI][2][2];
+#pragma unroll
+    for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    if (nk > 0) load_stage(0, kb);
+    cp_async_commit();
+    for (int it = 0; it < nk; ++it) {
+        if (it + 1 < nk) load_stage((it + 1) & 1, kb + (it + 1) * TC_BK);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double* as = As + (it & 1) * BM * LD;
+        const double* bs = Bs + (it & 1) * TC_BN * LD;
+#pragma unroll
+        for (int ks = 0; ks < TC_BK; ks += 4) {
+            double af[TI], bf[2];
+#pragma unroll
+            for (int i = 0; i < TI; ++i) af[i] = as[(wm * WTM + i * 8 + g) * LD + ks + t];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) bf[j] = bs[(wn * 16 + j * 8 + g) * LD + ks + t];
+#pragma unroll
+            for (int i = 0; i < TI; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    // park the partial tile: Cs[row][col], row-major with LDC
+    constexpr int LDC = TC_BN + 1;
+    double* Cs = tsm;
+#pragma unroll
+    for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                Cs[(wm * WTM + i * 8 + g) * LDC + wn * 16 + j * 8 + 2 * t + e] = acc[i][j][e];
+    cluster.sync();
+    // rank r finalises elements e = r, r + CS, ... (column-major walk for coalesced stores)
+    for (int e = rank * 128 + tid; e < BM * TC_BN; e += CS * 128) {
+        const int row = e % BM, col = e / BM;
+        double s = 0.0;
+        for (int q = 0; q < CS; ++q) s += cluster.map_shared_rank(Cs, q)[row * LDC + col];
+        const int gm = m0 + row, gn = n0 + col;
+        if (gm < m && gn < n) C[(size_t)gn * ldc + gm] = alpha * s;
+    }
+    if (rank == 0 && blockIdx.z == 0 && tid < TC_BN && n0 + tid < n) hook(n0 + tid);
+    cluster.sync();
+}
+
+// Host launcher: returns false if the operand layout does not allow 16-byte cp.async.
+template <class Hook>
+bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, const double* A, int lda, const double* B,
+                       int ldb, double* C, int ldc, Hook hook) {
+    if ((K & 1) || (lda & 1) || (ldb & 1) || (((uintptr_t)A | (uintptr_t)B) & 15)) return false;
+    int CS = cdiv(K, 160);
+    if (CS > 8) CS = 8;
+    if (CS < 1) CS = 1;
+    int kchunk = cdiv(cdiv(K, CS), TC_BK) * TC_BK;
+    CS = cdiv(K, kchunk);
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(128, 1, 1);
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (m <= 32) {
+        cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
+        cfg.dynamicSmemBytes = tn_cluster_smem<32>();
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
+    } else {
+        cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 64));
+        cfg.dynamicSmemBytes = tn_cluster_smem<64>();
+        static bool attr64 = false;
+        if (!attr64) {
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<64, Hook>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)tn_cluster_smem<64>()));
+            attr64 = true;
+        }
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<64, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
+    }
+    launched(ctx);
+    return true;
 }
 
 }  // namespace acp

@@ -17,6 +17,7 @@
 #include "gemm.cuh"
 
 #include <cmath>
+#include <cstdio>
 
 namespace acp {
 
@@ -72,18 +73,14 @@ struct PcgScal {
     const double* dots;  // from K1: [2j] x.y, [2j+1] x.x
 };
 
-// C = dV * sum_z Cp[z]  (n_occ x n), plus the per-column scalar recurrences.
-__global__ void k_pcg_scalars(int mode, int n_occ, int n, int splits, double dV, const double* __restrict__ Cp,
-                              double* __restrict__ C, PcgScal s, double tol2, int n_valid_mu, int nmu_p) {
-    const size_t tot = (size_t)n_occ * n;
-    size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx < tot) {
-        double acc = 0.0;
-        for (int z = 0; z < splits; ++z) acc += Cp[(size_t)z * tot + idx];
-        C[idx] = dV * acc;
-    }
-    if (idx < (size_t)n) {
-        const int j = (int)idx;
+// Per-column CG scalar recurrences, run once per column inside the K2 GEMM (hook).
+struct ScalHook {
+    int mode;
+    PcgScal s;
+    double tol2;
+    int n_valid_mu;
+    int nmu_p;
+    __device__ __forceinline__ void operator()(int j) const {
         if (mode == SC_INIT) {
             const double rz = s.dots[2 * j], bb = s.dots[2 * j + 1];
             const bool valid = (j % nmu_p) < n_valid_mu && bb > 0.0;
@@ -110,7 +107,7 @@ __global__ void k_pcg_scalars(int mode, int n_occ, int n, int splits, double dV,
             }
         }
     }
-}
+};
 
 // K3 after H p: Ap = Y - Psi C;  X += alpha P;  R -= alpha Ap.
 struct EpAlpha {
@@ -222,9 +219,6 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     double* shift = ctx->wsd("pcg_shift", n);
     double* dots = ctx->wsd("pcg_dots", 2 * (size_t)n);
     double* C = ctx->wsd("pcg_C", (size_t)n_occ * n);
-    const int kchunk = 512;  // fixed split pattern: per-column results independent of the batch size
-    const int max_splits = cdiv(Ng, kchunk);
-    double* Cp = ctx->wsd("pcg_Cp", (size_t)max_splits * n_occ * n);
     PcgScal s;
     s.rz = ctx->wsd("pcg_rz", n);
     s.bb = ctx->wsd("pcg_bb", n);
@@ -235,8 +229,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     s.iters = ctx->wsi("pcg_iters", n);
     s.dots = dots;
     int* d_nact = ctx->wsi("pcg_nact", 1);
-    int* h_nact = nullptr;
-    ACP_CUDA(cudaMallocHost(&h_nact, sizeof(int)));
+    int* h_nact = static_cast<int*>(ctx->pinned);
 
     const double* mH = multiplier(ctx, MULT_KINETIC, 0.0);
     double* mHc = ctx->wsd("pcg_multH", Ng);
@@ -254,8 +247,6 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         launched(ctx);
     }
     const double tol2 = tol * tol;
-    const int sc_threads = 256;
-    const int sc_blocks = cdiv((size_t)n_occ * n > (size_t)n ? (size_t)n_occ * n : (size_t)n, sc_threads);
     dim3 ugrid(cdiv(Ng, NN_BM), cdiv(n, NN_BN));
 
     auto precond_half = [&](int mode) {
@@ -267,10 +258,9 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         f.active = (mode == SC_INIT) ? nullptr : s.active;
         f.dots = dots;
         fourier_op(ctx, f);
-        int splits = gemm_tn_partial(ctx, Ng, n_occ, n, Psi, Ng, Y, Ng, Cp, kchunk);
-        k_pcg_scalars<<<sc_blocks, sc_threads, 0, ctx->stream>>>(mode, n_occ, n, splits, ctx->dV, Cp, C, s, tol2,
-                                                                  nvalid, nmu_p);
-        launched(ctx);
+        ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ,
+                                      ScalHook{mode, s, tol2, nvalid, nmu_p}),
+                    "projection GEMM needs an even grid");
         EpBeta ep{Y, P, s.beta, s.active, Ng, mode == SC_INIT ? 1 : 0};
         k_pcg_update<EpBeta><<<ugrid, 128, 0, ctx->stream>>>(Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
         launched(ctx);
@@ -286,10 +276,9 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         f.active = s.active;
         f.dots = dots;
         fourier_op(ctx, f);
-        int splits = gemm_tn_partial(ctx, Ng, n_occ, n, Psi, Ng, Y, Ng, Cp, kchunk);
-        k_pcg_scalars<<<sc_blocks, sc_threads, 0, ctx->stream>>>(SC_ALPHA, n_occ, n, splits, ctx->dV, Cp, C, s,
-                                                                  tol2, nvalid, nmu_p);
-        launched(ctx);
+        ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ,
+                                      ScalHook{SC_ALPHA, s, tol2, nvalid, nmu_p}),
+                    "projection GEMM needs an even grid");
         EpAlpha ep{Y, P, X, R, s.alpha, s.active, Ng};
         k_pcg_update<EpAlpha><<<ugrid, 128, 0, ctx->stream>>>(Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
         launched(ctx);
@@ -298,27 +287,24 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     // r0 = b, z0 = Q M r0, p0 = z0
     precond_half(SC_INIT);
 
-    // Capture `chunk` iterations into one graph and replay until converged.
+    // `chunk` iterations captured once into a cached graph, replayed until every column converged.
     const int chunk = 4;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    long long before = ctx->launches;
-    ACP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    for (int it = 0; it < chunk; ++it) {
-        hamiltonian_half();
-        precond_half(SC_BETA);
-    }
-    k_count_active<<<1, 256, 0, ctx->stream>>>(s.active, n, d_nact);
-    launched(ctx);
-    ACP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
-    const long long per_replay = ctx->launches - before;
-    ctx->launches = before;
-    ACP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    char key[512];
+    snprintf(key, sizeof(key), "pcg:%d:%d:%d:%d:%d:%.17g:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p", Ng, n, n_occ,
+             nmu_p, nvalid, tol2, (void*)Psi, (void*)V, (void*)R, (void*)P, (void*)Y, (void*)X, (void*)C,
+             (void*)shift, (void*)dots, (void*)s.rz, (void*)s.active, (void*)mHc, (void*)mP, (void*)d_nact);
+    cudaGraphExec_t exec = graph_cached(ctx, key, [&]() {
+        for (int it = 0; it < chunk; ++it) {
+            hamiltonian_half();
+            precond_half(SC_BETA);
+        }
+        k_count_active<<<1, 256, 0, ctx->stream>>>(s.active, n, d_nact);
+        launched(ctx);
+    });
     int done_iter = 0;
     bool converged = false;
     while (done_iter < max_iter) {
-        ACP_CUDA(cudaGraphLaunch(exec, ctx->stream));
-        ctx->launches += per_replay;
+        graph_launch(ctx, key, exec);
         done_iter += chunk;
         ACP_CUDA(cudaMemcpyAsync(h_nact, d_nact, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         ACP_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -327,9 +313,6 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
             break;
         }
     }
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    cudaFreeHost(h_nact);
     if (st) {
         std::vector<int> it(n);
         std::vector<double> res(n), bb(n);
@@ -384,8 +367,6 @@ void apply_chi0(acp_context* ctx, const double* Psi, const double* eps, const do
 void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* V, const double* X, int n,
                   double* Y, int reps) {
     const int Ng = ctx->Ng, n_occ = ctx->sys.n_occ;
-    const int kchunk = 512;
-    double* Cp = ctx->wsd("kb_Cp", (size_t)cdiv(Ng, kchunk) * n_occ * n);
     double* C = ctx->wsd("kb_C", (size_t)n_occ * n);
     double* beta = ctx->wsd("kb_beta", n);
     int* active = ctx->wsi("kb_active", n);
@@ -412,7 +393,7 @@ void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* 
             f.dots = nullptr;
             fourier_op(ctx, f);
         } else if (which == 1) {
-            gemm_tn_partial(ctx, Ng, n_occ, n, Psi, Ng, X, Ng, Cp, kchunk);
+            launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, X, Ng, C, n_occ, NoHook{});
         } else {
             EpBeta ep{X, Y, beta, active, Ng, 0};
             dim3 ugrid(cdiv(Ng, NN_BM), cdiv(n, NN_BN));

@@ -3,13 +3,17 @@
 //  K4  G~ = G' Omega            real SRFT of the perturbation columns (DMMA GEMM)
 //  K5  M~^T(i + q N_occ, a) = psi_i(a) G~(a, q)   Kronecker rows
 //  K6  pivoted QR of M~^T: greedy max-norm pivot among the remaining columns
-//      (first index on ties), Householder reflection, trailing update with exact
-//      norm recomputation; device-resident (the step index lives in device memory,
-//      chunks of steps are replayed from one CUDA graph, no host round trip per pivot)
-//  K7  Xi^T = R11^{-1} R_{1:N,:} Pi^{-1} by back substitution + scatter.
+//      (lowest position on ties), Householder reflection, trailing update with exact
+//      norm recomputation -- ONE persistent cooperative kernel, columns resident in
+//      shared memory, one grid barrier per pivot (see k_qrcp_persistent)
+//  K7  Xi^T = R11^{-1} R_{1:N,:} Pi^{-1}: warp-per-column back
+//      substitution + scatter.
+#include <cooperative_groups.h>
+
 #include "gemm.cuh"
 
 #include <cmath>
+#include <cstdio>
 
 namespace acp {
 
@@ -54,183 +58,264 @@ __global__ void __launch_bounds__(256) k_kron_rows(int Ng, int n_occ, int r, con
     }
 }
 
-struct QrState {
-    int step;      // next pivot step j
-    int stop;      // 1 when finished
-    int n_mu;      // selected count (valid when stop)
-    int kmax;
-    double r11;    // |R_11|
+// ---------------------------------------------------------------------------
+// Persistent pivoted QR: ONE cooperative launch for the whole factorisation.
+// CTA b owns the grid-point columns [b*cpb, (b+1)*cpb) for the entire run (in shared memory
+// when they fit, else in place in global memory/L2); columns never move -- a position map
+// reproduces the swap semantics of column-pivoted QR (ties -> lowest current position).
+// Per step j there is exactly one grid barrier:
+//   every CTA publishes its best candidate (norm^2, position, column) and a copy of that
+//   column's rows j..m-1 (double-buffered by step parity), grid.sync(), then every CTA
+//   redundantly selects the same winner, builds the same Householder vector from the
+//   published copy, and updates its own remaining columns (exact norm recomputation).
+struct QrSlot {
+    double n2;
+    int pos;
+    int col;
 };
 
-// norms2[c] = sum_{i >= 0} A[i, c]^2  (warp per column)
-__global__ void k_qr_norms(int m, int Ng, const double* __restrict__ A, double* __restrict__ norms2) {
-    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, l = threadIdx.x & 31;
-    if (w >= Ng) return;
-    const double* col = A + (size_t)w * m;
-    double s = 0.0;
-    for (int i = l; i < m; i += 32) s += col[i] * col[i];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (l == 0) norms2[w] = s;
-}
-
-// Single CTA: pivot selection, threshold test, column swap, Householder vector.
-__global__ void __launch_bounds__(1024) k_qr_pivot(int m, int Ng, double* __restrict__ A, double* __restrict__ norms2,
-                                                   int* __restrict__ perm, double* __restrict__ v, double* __restrict__ tau,
-                                                   double* __restrict__ rdiag, QrState* st, double eps, int fixed) {
-    __shared__ double sval[32];
-    __shared__ int sidx[32];
-    __shared__ int s_p;
-    __shared__ double s_red[32];
-    if (st->stop) return;
-    const int j = st->step;
-    if (j >= st->kmax) {
-        if (threadIdx.x == 0) {
-            st->stop = 1;
-            st->n_mu = st->kmax;
-        }
-        return;
-    }
-    // argmax over c in [j, Ng), first index on ties
-    double best = -1.0;
-    int bi = Ng;
-    for (int c = j + threadIdx.x; c < Ng; c += blockDim.x) {
-        double x = norms2[c];
-        if (x > best) {  // strictly greater keeps the lowest index within this thread (c increasing)
-            best = x;
-            bi = c;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-            best = ob;
-            bi = oi;
-        }
-    }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) {
-        sval[w] = best;
-        sidx[w] = bi;
-    }
+template <bool SMEM>
+__global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* __restrict__ Ag, int kmax, double eps,
+                                                         int fixed, QrSlot* __restrict__ slots,
+                                                         double* __restrict__ cand, int* __restrict__ perm,
+                                                         double* __restrict__ rdiag, int* __restrict__ out_nmu) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double qsm[];
+    __shared__ double red_d[32];
+    __shared__ int red_i[32];
+    __shared__ int red_j[32];
+    __shared__ int s_lc;
+    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    const int cpb = (Ng + G - 1) / G;
+    const int c0 = b * cpb;
+    const int nc = max(0, min(Ng, c0 + cpb) - c0);
+    double* cols = qsm;
+    double* v = qsm + (SMEM ? (size_t)cpb * m : 0);
+    double* n2 = v + m;
+    int* pos = reinterpret_cast<int*>(n2 + cpb);
+    int* dn = pos + cpb;
+    auto colp = [&](int lc) -> double* { return SMEM ? cols + (size_t)lc * m : Ag + (size_t)(c0 + lc) * m; };
+    if (SMEM)
+        for (int e = tid; e < nc * m; e += blockDim.x) cols[e] = Ag[(size_t)c0 * m + e];
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double b = -1.0;
-        int idx = Ng;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i)
-            if (sval[i] > b || (sval[i] == b && sidx[i] < idx)) {
-                b = sval[i];
-                idx = sidx[i];
-            }
-        const double rjj = sqrt(b);
-        if (j == 0) st->r11 = rjj;
-        int stop = 0;
-        if (fixed <= 0 && rjj < eps * st->r11) stop = 1;
-        if (rjj == 0.0) stop = 1;
-        if (stop) {
-            st->stop = 1;
-            st->n_mu = j;
-            s_p = -1;
-        } else {
-            s_p = idx;
-        }
-    }
-    __syncthreads();
-    const int p = s_p;
-    if (p < 0) return;
-    if (p != j) {
-        double* cj = A + (size_t)j * m;
-        double* cp = A + (size_t)p * m;
-        for (int i = threadIdx.x; i < m; i += blockDim.x) {
-            double t = cj[i];
-            cj[i] = cp[i];
-            cp[i] = t;
-        }
-        if (threadIdx.x == 0) {
-            int t = perm[j];
-            perm[j] = perm[p];
-            perm[p] = t;
-            double u = norms2[j];
-            norms2[j] = norms2[p];
-            norms2[p] = u;
-        }
-    }
-    __syncthreads();
-    // Householder: x = A[j:m, j]
-    double* cj = A + (size_t)j * m;
-    double s = 0.0;
-    for (int i = j + threadIdx.x; i < m; i += blockDim.x) s += cj[i] * cj[i];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (l == 0) s_red[w] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += s_red[i];
-        s_red[0] = t;
-    }
-    __syncthreads();
-    const double xn2 = s_red[0];
-    const double xn = sqrt(xn2);
-    const double x0 = cj[j];
-    const double alpha = (x0 >= 0.0) ? -xn : xn;
-    const double v0 = x0 - alpha;
-    const double vn2 = xn2 - x0 * x0 + v0 * v0;
-    for (int i = j + threadIdx.x; i < m; i += blockDim.x) v[i] = (i == j) ? v0 : cj[i];
-    __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) cj[i] = 0.0;
-    if (threadIdx.x == 0) {
-        cj[j] = alpha;
-        *tau = (vn2 > 0.0) ? 2.0 / vn2 : 0.0;
-        rdiag[j] = xn;
-    }
-}
-
-// Trailing update for columns c > j (warp per column): A[j:,c] -= tau v (v^T A[j:,c]); new norms (rows > j).
-__global__ void __launch_bounds__(256) k_qr_update(int m, int Ng, double* __restrict__ A, double* __restrict__ norms2,
-                                                   const double* __restrict__ v, const double* __restrict__ tau,
-                                                   QrState* st) {
-    if (st->stop) return;
-    const int j = st->step;
-    const int wpb = blockDim.x >> 5;
-    const int l = threadIdx.x & 31;
-    const double t = *tau;
-    for (int c = j + 1 + blockIdx.x * wpb + (threadIdx.x >> 5); c < Ng; c += gridDim.x * wpb) {
-        double* col = A + (size_t)c * m;
+    for (int lc = warp; lc < nc; lc += nwarp) {
+        const double* c = colp(lc);
         double s = 0.0;
-        for (int i = j + l; i < m; i += 32) s += v[i] * col[i];
+        for (int i = lane; i < m; i += 32) s += c[i] * c[i];
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        const double f = t * s;
-        double nn = 0.0;
-        for (int i = j + l; i < m; i += 32) {
-            double x = col[i] - f * v[i];
-            col[i] = x;
-            if (i > j) nn += x * x;
+        if (lane == 0) {
+            n2[lc] = s;
+            pos[lc] = c0 + lc;
+            dn[lc] = 0;
         }
-        for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
-        if (l == 0) norms2[c] = nn;
     }
+    __syncthreads();
+    double r11 = 0.0;
+    int N = kmax;
+    for (int j = 0; j < kmax; ++j) {
+        const int buf = j & 1;
+        // ---- local candidate: max n2, ties -> lowest position
+        if (warp == 0) {
+            double bn = -1.0;
+            int bp = 1 << 30, bl = -1;
+            for (int lc = lane; lc < nc; lc += 32) {
+                if (dn[lc]) continue;
+                const double x = n2[lc];
+                if (x > bn || (x == bn && pos[lc] < bp)) {
+                    bn = x;
+                    bp = pos[lc];
+                    bl = lc;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                if (on > bn || (on == bn && op < bp)) {
+                    bn = on;
+                    bp = op;
+                    bl = ol;
+                }
+            }
+            if (lane == 0) {
+                s_lc = bl;
+                QrSlot sl;
+                sl.n2 = bn;
+                sl.pos = bp;
+                sl.col = bl >= 0 ? c0 + bl : -1;
+                slots[buf * G + b] = sl;
+            }
+        }
+        __syncthreads();
+        if (s_lc >= 0) {
+            const double* c = colp(s_lc);
+            double* dst = cand + ((size_t)buf * G + b) * m;
+            for (int i = j + tid; i < m; i += blockDim.x) dst[i] = c[i];
+        }
+        __threadfence();
+        grid.sync();
+        // ---- global winner (identical in every CTA)
+        double bn = -1.0;
+        int bp = 1 << 30, bs = -1;
+        for (int s = tid; s < G; s += blockDim.x) {
+            // L2 reads (ld.cg): the slots were written by other CTAs; L1 is not coherent
+            const double sn = __ldcg(&slots[buf * G + s].n2);
+            const int sp = __ldcg(&slots[buf * G + s].pos);
+            const int sc = __ldcg(&slots[buf * G + s].col);
+            if (sc >= 0 && (sn > bn || (sn == bn && sp < bp))) {
+                bn = sn;
+                bp = sp;
+                bs = s;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+            const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+            if (on > bn || (on == bn && op < bp)) {
+                bn = on;
+                bp = op;
+                bs = os;
+            }
+        }
+        if (lane == 0) {
+            red_d[warp] = bn;
+            red_i[warp] = bp;
+            red_j[warp] = bs;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < nwarp; ++w)
+                if (red_d[w] > red_d[0] || (red_d[w] == red_d[0] && red_i[w] < red_i[0])) {
+                    red_d[0] = red_d[w];
+                    red_i[0] = red_i[w];
+                    red_j[0] = red_j[w];
+                }
+        }
+        __syncthreads();
+        const double wn2 = red_d[0];
+        const int pw = red_i[0], ws = red_j[0];
+        const double rjj = sqrt(fmax(wn2, 0.0));
+        if (j == 0) r11 = rjj;
+        if (ws < 0 || rjj == 0.0 || (fixed <= 0 && rjj < eps * r11)) {
+            N = j;
+            break;
+        }
+        const int cw = __ldcg(&slots[buf * G + ws].col);
+        // ---- Householder vector from the published copy of the winner column
+        const double* x = cand + ((size_t)buf * G + ws) * m;
+        double s = 0.0;
+        for (int i = j + tid; i < m; i += blockDim.x) {
+            const double xi = __ldcg(x + i);
+            v[i] = xi;
+            s += xi * xi;
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        __syncthreads();
+        if (lane == 0) red_d[warp] = s;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nwarp; ++w) t += red_d[w];
+            red_d[0] = t;
+        }
+        __syncthreads();
+        const double xn2 = red_d[0];
+        const double xn = sqrt(xn2);
+        const double x0 = v[j];
+        const double alpha = (x0 >= 0.0) ? -xn : xn;
+        const double v0 = x0 - alpha;
+        const double tau = 2.0 / (xn2 - x0 * x0 + v0 * v0);
+        __syncthreads();
+        if (tid == 0) v[j] = v0;
+        if (b == 0 && tid == 0) rdiag[j] = xn;
+        // ---- position bookkeeping (swap of positions j and pw) and the pivot column itself
+        for (int lc = tid; lc < nc; lc += blockDim.x) {
+            if (c0 + lc == cw) {
+                pos[lc] = j;
+                dn[lc] = 1;
+            } else if (!dn[lc] && pos[lc] == j) {
+                pos[lc] = pw;
+            }
+        }
+        __syncthreads();
+        // ---- trailing update of the remaining owned columns (warp per column)
+        for (int lc = warp; lc < nc; lc += nwarp) {
+            double* c = colp(lc);
+            if (c0 + lc == cw) {
+                for (int i = j + lane; i < m; i += 32) c[i] = (i == j) ? alpha : 0.0;
+                continue;
+            }
+            if (dn[lc]) continue;
+            double d = 0.0;
+            for (int i = j + lane; i < m; i += 32) d += v[i] * c[i];
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            const double f = tau * d;
+            double nn = 0.0;
+            for (int i = j + lane; i < m; i += 32) {
+                const double y = c[i] - f * v[i];
+                c[i] = y;
+                if (i > j) nn += y * y;
+            }
+            for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+            if (lane == 0) n2[lc] = nn;
+        }
+        __syncthreads();
+    }
+    if (SMEM)
+        for (int e = tid; e < nc * m; e += blockDim.x) Ag[(size_t)c0 * m + e] = cols[e];
+    for (int lc = tid; lc < nc; lc += blockDim.x) perm[pos[lc]] = c0 + lc;
+    if (b == 0 && tid == 0) *out_nmu = N;
 }
 
-__global__ void k_qr_advance(QrState* st) {
-    if (!st->stop) st->step += 1;
-}
-
-__global__ void k_iota(int* p, int n) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = i;
-}
-
-// T = R11^{-1} R12 (back substitution), one thread per trailing column; T stored row-major (mu, c').
-__global__ void k_trsm_cols(int m, int Ng, int N, const double* __restrict__ A, double* __restrict__ T) {
-    const int c = N + blockIdx.x * blockDim.x + threadIdx.x;
+// T = R11^{-1} R12 by column-oriented back substitution, one WARP per trailing column c:
+// lane l keeps b_nu for nu = l, l+32, ... in registers; for mu = N-1..0 the owner lane forms
+// x_mu = b_mu / R_mu,mu, broadcasts it, and every lane updates b_nu -= R_nu,mu x_mu (nu < mu)
+// reading column mu of R (contiguous, shared by all warps through L1/L2).  T row-major (mu, c').
+template <int SLOTS>
+__global__ void __launch_bounds__(256) k_trsm_warp(int m, int Ng, int N, const double* __restrict__ A,
+                                                   const int* __restrict__ perm, double* __restrict__ T) {
+    const int wglob = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int l = threadIdx.x & 31;
+    const int c = N + wglob;
     if (c >= Ng) return;
-    const int nc = Ng - N;
-    const int cc = c - N;
-    for (int mu = N - 1; mu >= 0; --mu) {
-        double s = A[(size_t)c * m + mu];
-        for (int nu = mu + 1; nu < N; ++nu) s -= A[(size_t)nu * m + mu] * T[(size_t)nu * nc + cc];
-        T[(size_t)mu * nc + cc] = s / A[(size_t)mu * m + mu];
+    const int nc = Ng - N, cc = c - N;
+    double b[SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+        const int nu = s * 32 + l;
+        b[s] = (nu < N) ? A[(size_t)perm[c] * m + nu] : 0.0;
     }
+    for (int mu = N - 1; mu >= 0; --mu) {
+        const int owner = mu & 31, slot = mu >> 5;
+        double bm = 0.0;
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s)
+            if (s == slot) bm = b[s];
+        const double* rcol = A + (size_t)perm[mu] * m;
+        double x = bm / rcol[mu];
+        x = __shfl_sync(0xffffffffu, x, owner);
+        if (l == owner) T[(size_t)mu * nc + cc] = x;
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s) {
+            const int nu = s * 32 + l;
+            if (nu < mu) b[s] -= rcol[nu] * x;
+        }
+    }
+}
+
+static void trsm_cols(acp_context* ctx, int m, int Ng, int N, const double* A, const int* perm, double* T) {
+    const int warps = Ng - N;
+    if (warps <= 0) return;
+    const int blocks = cdiv((long long)warps * 32, 256);
+    if (N <= 128) k_trsm_warp<4><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
+    else if (N <= 256) k_trsm_warp<8><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
+    else if (N <= 512) k_trsm_warp<16><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
+    else if (N <= 1024) k_trsm_warp<32><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
+    else throw Error(ACP_ERR_UNSUPPORTED, "N_mu > 1024 is not supported by the TRSM kernel");
+    launched(ctx);
 }
 
 // Xi[perm[c], mu] = T[mu, c - N] (c >= N) or delta_{c mu} (c < N);  S[mu] = perm[mu].
@@ -272,61 +357,43 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
         k_kron_rows<<<cdiv(Ng, 32), 256, smem, ctx->stream>>>(Ng, n_occ, r, Psi, Gt, A);
         launched(ctx);
     }
-    // QRCP
+    // QRCP: one persistent cooperative kernel
     int kmax = m < Ng ? m : Ng;
     if (n_fixed > 0 && n_fixed < kmax) kmax = n_fixed;
     if (n_mu_max < kmax && n_fixed > 0) ACP_REQUIRE(false, "n_mu_fixed exceeds n_mu_max");
-    double* norms2 = ctx->wsd("qr_norms", Ng);
     int* perm = ctx->wsi("qr_perm", Ng);
-    double* v = ctx->wsd("qr_v", m);
-    double* tau = ctx->wsd("qr_tau", 1);
-    double* rdiag = ctx->wsd("qr_rdiag", kmax);
-    QrState* st = static_cast<QrState*>(ctx->ws("qr_state", sizeof(QrState)));
-    QrState h0{0, 0, 0, kmax, 0.0};
-    ACP_CUDA(cudaMemcpyAsync(st, &h0, sizeof(QrState), cudaMemcpyHostToDevice, ctx->stream));
-    k_iota<<<cdiv(Ng, 256), 256, 0, ctx->stream>>>(perm, Ng);
+    double* rdiag = ctx->wsd("qr_rdiag", m < Ng ? m : Ng);
+    int* d_nmu = ctx->wsi("qr_nmu", 1);
+    int dev_sms = 148;
+    ACP_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    int G = dev_sms < Ng ? dev_sms : Ng;
+    int cpb = cdiv(Ng, G);
+    G = cdiv(Ng, cpb);
+    const size_t tail = (size_t)m * sizeof(double) + (size_t)cpb * (sizeof(double) + 2 * sizeof(int)) + 64;
+    const size_t smem_full = (size_t)cpb * m * sizeof(double) + tail;
+    const bool use_smem = smem_full <= 200 * 1024;
+    const size_t smem = use_smem ? smem_full : tail;
+    QrSlot* slots = static_cast<QrSlot*>(ctx->ws("qr_slots", 2 * (size_t)G * sizeof(QrSlot)));
+    double* cand = ctx->wsd("qr_cand", 2 * (size_t)G * m);
+    void* args[] = {(void*)&m, (void*)&Ng, (void*)&A, (void*)&kmax, (void*)&id_eps, (void*)&n_fixed, (void*)&slots,
+                    (void*)&cand, (void*)&perm, (void*)&rdiag, (void*)&d_nmu};
+    const void* fn = use_smem ? (const void*)k_qrcp_persistent<true> : (const void*)k_qrcp_persistent<false>;
+    ACP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    ACP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+    ACP_REQUIRE(occ >= 1 && G <= occ * dev_sms, "QRCP: cooperative grid does not fit");
+    ACP_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(256), args, smem, ctx->stream));
     launched(ctx);
-    k_qr_norms<<<cdiv((size_t)Ng * 32, 256), 256, 0, ctx->stream>>>(m, Ng, A, norms2);
-    launched(ctx);
-    const int upd_blocks = 148 * 4;
-    const int chunk = 16;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    long long before = ctx->launches;
-    ACP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    for (int s = 0; s < chunk; ++s) {
-        k_qr_pivot<<<1, 1024, 0, ctx->stream>>>(m, Ng, A, norms2, perm, v, tau, rdiag, st, id_eps, n_fixed);
-        launched(ctx);
-        k_qr_update<<<upd_blocks, 256, 0, ctx->stream>>>(m, Ng, A, norms2, v, tau, st);
-        launched(ctx);
-        k_qr_advance<<<1, 1, 0, ctx->stream>>>(st);
-        launched(ctx);
-    }
-    ACP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
-    const long long per = ctx->launches - before;
-    ctx->launches = before;
-    ACP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-    QrState hs{};
-    for (int done = 0; done <= kmax + chunk; done += chunk) {
-        ACP_CUDA(cudaGraphLaunch(exec, ctx->stream));
-        ctx->launches += per;
-        ACP_CUDA(cudaMemcpyAsync(&hs, st, sizeof(QrState), cudaMemcpyDeviceToHost, ctx->stream));
-        ACP_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (hs.stop) break;
-    }
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    ACP_REQUIRE(hs.stop, "QRCP did not terminate");
-    const int N = hs.n_mu;
+    int* hp = static_cast<int*>(ctx->pinned);
+    ACP_CUDA(cudaMemcpyAsync(hp, d_nmu, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int N = *hp;
     ACP_REQUIRE(N >= 1, "QRCP selected no rows (zero sketch)");
     if (N > n_mu_max)
         throw Error(ACP_ERR_INVALID, "N_mu = " + std::to_string(N) + " exceeds n_mu_max = " + std::to_string(n_mu_max));
     // Xi
     double* T = ctx->wsd("qr_T", (size_t)N * (Ng - N > 0 ? Ng - N : 1));
-    if (Ng > N) {
-        k_trsm_cols<<<cdiv(Ng - N, 64), 64, 0, ctx->stream>>>(m, Ng, N, A, T);
-        launched(ctx);
-    }
+    trsm_cols(ctx, m, Ng, N, A, perm, T);
     k_scatter_xi<<<dim3(cdiv(Ng, 256), N), 256, 0, ctx->stream>>>(Ng, N, perm, T, Xi, S);
     launched(ctx);
     return N;
