@@ -10,7 +10,8 @@
  * - All floating point is IEEE fp64.  Grid functions are real, sampled on a
  *   uniform periodic grid of N_g points, stored as column-major
  *   "batches": column j of an N_g x n batch starts at ptr + j*N_g (leading
- *   dimension = N_g, no padding).  In 2D the point index is i0*n1 + i1.
+ *   dimension = N_g, no padding).  In 2D (grid n0 x n1, N_g = n0*n1) the point index
+ *   is i0*n1 + i1 (C order; axis 0 pairs with position component 0).
  * - Orbitals are normalised as int psi_i psi_j dr = delta_ij, i.e.
  *   dV * Psi^T Psi = I with dV = cell volume / N_g.
  * - "d_" arguments are DEVICE pointers on the context's device; "h_" arguments
@@ -42,7 +43,7 @@ extern "C" {
 
 /* Physical system and discretisation (section 4.1 model). */
 typedef struct acp_system {
-    int dim;            /* spatial dimension d (1 supported; 2 -> ACP_ERR_UNSUPPORTED) */
+    int dim;            /* spatial dimension d = 1 or 2 (2D: square/rectangular periodic cell) */
     int grid[2];        /* grid points per dimension (grid[1] ignored for d = 1) */
     double cell[2];     /* periodic cell lengths (bohr) */
     int n_atoms;        /* N_A */
@@ -74,6 +75,8 @@ long long acp_kernel_launches(const acp_context* ctx);
 /* 1. Ground state (Eqs. Hamil/effV; solver PAPER.md:855).
  *    Self-consistent field for H = -1/2 Delta + K*(rho + m).
  *    h_R:      host, N_A*d atom positions (bohr), row-major (I, a).
+ *    Grids: every n_a must factor into 2, 3, 5; 1D n0 <= ~12000 (one CTA per column
+ *    pair), 2D slices n0*n1/cs <= ~6000 points per CTA of a <= 16-CTA cluster.
  *    d_Psi:    out, N_g x n_occ orbitals (dV Psi^T Psi = I), ascending energy.
  *    d_eps:    out, n_occ + n_extra eigenvalues (ascending).
  *    d_rho:    out, N_g density f sum |psi_i|^2.

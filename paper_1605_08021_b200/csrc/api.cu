@@ -37,17 +37,18 @@ int acp_create(const acp_system* sys, int device, acp_context** out) {
     if (!sys || !out) return ACP_ERR_INVALID;
     *out = nullptr;
     if (sys->dim != 1 && sys->dim != 2) return ACP_ERR_INVALID;
-    if (sys->dim == 2) return ACP_ERR_UNSUPPORTED;
     if (sys->grid[0] < 4 || sys->n_atoms < 1 || sys->n_occ < 1 || sys->cell[0] <= 0 || sys->kappa <= 0 ||
         sys->eps0 <= 0 || sys->sigma <= 0 || sys->occ <= 0)
         return ACP_ERR_INVALID;
-    if (sys->n_occ >= sys->grid[0]) return ACP_ERR_INVALID;
+    if (sys->dim == 2 && (sys->grid[1] < 4 || sys->cell[1] <= 0)) return ACP_ERR_INVALID;
+    const long long ng = (long long)sys->grid[0] * (sys->dim == 2 ? sys->grid[1] : 1);
+    if (sys->n_occ >= ng || ng > (1LL << 24)) return ACP_ERR_INVALID;
     acp_context* ctx = new acp_context();
     ctx->sys = *sys;
     ctx->device = device;
     ctx->dim = sys->dim;
-    ctx->Ng = sys->grid[0];
-    ctx->Omega = sys->cell[0];
+    ctx->Ng = (int)ng;
+    ctx->Omega = sys->cell[0] * (sys->dim == 2 ? sys->cell[1] : 1.0);
     ctx->dV = ctx->Omega / ctx->Ng;
     try {
         ACP_CUDA(cudaSetDevice(device));
@@ -59,6 +60,9 @@ int acp_create(const acp_system* sys, int device, acp_context** out) {
         int code = e.code;
         acp_destroy(ctx);
         return code;
+    } catch (const std::exception&) {
+        acp_destroy(ctx);
+        return ACP_ERR_CUDA;
     }
     *out = ctx;
     return ACP_OK;

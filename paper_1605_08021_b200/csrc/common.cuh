@@ -61,13 +61,24 @@ struct acp_context {
     std::string err;
     long long launches = 0;
 
-    acp::FftPlan plan;
-    double2* d_tw = nullptr;     // exp(-2 pi i m / N), m < N
-    double* d_k2 = nullptr;      // |k|^2 per FFT bin (numpy fft order)
-    double* d_kodd = nullptr;    // k_0 per bin with the Nyquist entry zeroed (odd multipliers)
-    double* d_kfull = nullptr;   // k_0 per bin (full)
-    double* d_khat = nullptr;    // Yukawa symbol 4 pi / (eps0 (|k|^2 + kappa^2))
-    double* d_mult = nullptr;    // scratch multiplier table (N)
+    // Grid / Fourier tables.  Axis a has n[a] points (n[1] = 1 in 1D); bins in numpy fft order,
+    // flattened C order (bin index k0 * n1 + k1).
+    int n[2] = {1, 1};
+    acp::FftPlan plan;           // axis 0 (1D: the whole grid)
+    acp::FftPlan plan1;          // axis 1 (2D only)
+    double2* d_tw = nullptr;     // exp(-2 pi i m / n0), m < n0
+    double2* d_tw1 = nullptr;    // exp(-2 pi i m / n1) (2D)
+    double* d_k2 = nullptr;      // |k|^2 per bin (N_g)
+    double* d_khat = nullptr;    // Yukawa symbol 4 pi / (eps0 (|k|^2 + kappa^2)) per bin (N_g)
+    double* d_kax[2] = {nullptr, nullptr};     // k_a per axis index (length n[a])
+    double* d_kaxodd[2] = {nullptr, nullptr};  // k_a with the Nyquist entry zeroed (odd multipliers)
+    double* d_kodd = nullptr;    // alias of d_kaxodd[0] (1D code)
+    double* d_kfull = nullptr;   // alias of d_kax[0]
+    double* d_mult = nullptr;    // scratch multiplier table (N_g)
+    // 2D operator geometry: a cluster of cs CTAs per column pair, r0 = n0/cs rows and
+    // c1 = n1/cs columns per CTA; threads per CTA and elements per thread of the FFT engine.
+    int cs = 1, r0 = 0, c1 = 0, fthreads = 0, fept = 0;
+    size_t fsmem = 0;
 
     std::map<std::string, acp::DevBuf> bufs;
     void* pinned = nullptr;  // 4 KiB pinned host scratch for small device->host reads
@@ -168,9 +179,9 @@ const double* multiplier(acp_context* ctx, MultKind kind, double tau);
 // Real grid functions from Hermitian spectra given as complex coefficients per bin:
 // out_j = (Ng/Omega) IFFT(spec_j)  (spec: Ng x n complex, bin-major per column).
 void ifft_hermitian(acp_context* ctx, const double2* spec, int n, double* out);
-// Spectrum out(k) = sum_a x(a) e^{-i k r_a} of one real column.
+// Spectrum out(k) = sum_a x(a) e^{-i k r_a} of one real column (bins in C order).
 void real_spectrum(acp_context* ctx, const double* x, double2* out);
-// Spectra of g_{I,a} (n = d*N_A columns) at positions R (device, N_A*d).
+// Spectra of g_{I,a} (n = d*N_A columns, j = I*d + a) at positions R (device, N_A x d row-major).
 void spectrum_G(acp_context* ctx, const double* d_R, double2* spec);
 // Spectrum of the total pseudocharge m.
 void spectrum_m(acp_context* ctx, const double* d_R, double2* spec);

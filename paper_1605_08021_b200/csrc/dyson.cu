@@ -124,20 +124,31 @@ void dyson(acp_context* ctx, const double* Psi, const double* eps, const double*
 }
 
 // ---- dynamical matrix ------------------------------------------------------
-// D_loc(I; a, b) = dV sum rho d2V_I = (1/N) sum_k Re( h^_I(k) conj(rho~(k)) ),
-// h^_I = (-i k_a)(-i k_b) Khat mhat e^{-i k R_I} (1D: a = b = 0).
-__global__ void k_dloc(int N, double L, const double* __restrict__ khat, const double* __restrict__ kodd,
-                       const double* __restrict__ k2, double Z, double sigma, const double* __restrict__ R,
+// Bin frequency integer (numpy fftfreq order) and the phase e^{-i k.R} of bin (i0, i1).
+__device__ __forceinline__ int dm_freq(int i, int N) { return (i < (N + 1) / 2) ? i : i - N; }
+
+// D_loc(I; a, b) = dV sum_r rho(r) d2V_I/dR_a dR_b (r) = (1/N) sum_k Re( h^_I^{ab}(k) conj(rho~(k)) ),
+// h^_I^{ab} = (-i k_a)(-i k_b) Khat mhat e^{-i k.R_I}  (Eq. SecDeriv second term).
+// One CTA per (I, a, b); dloc[(I d + a) d + b].
+__global__ void k_dloc(int n0, int n1, int dim, double L0, double L1, const double* __restrict__ khat,
+                       const double* __restrict__ k2, const double* __restrict__ kodd0,
+                       const double* __restrict__ kodd1, double Z, double sigma, const double* __restrict__ R,
                        const double2* __restrict__ rhot, double* __restrict__ dloc) {
     __shared__ double red[32];
-    const int I = blockIdx.x;
+    const int I = blockIdx.x, a = blockIdx.y / dim, b = blockIdx.y % dim;
+    const int N = n0 * n1;
     double s = 0.0;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const int m = (i < (N + 1) / 2) ? i : i - N;
+        const int i0 = i / n1, i1 = i - i0 * n1;
         const double mh = -Z * exp(-0.5 * sigma * sigma * k2[i]);
-        const double amp = -kodd[i] * kodd[i] * khat[i] * mh;
+        const double ka = a == 0 ? kodd0[i0] : kodd1[i1];
+        const double kb = b == 0 ? kodd0[i0] : kodd1[i1];
+        const double amp = -ka * kb * khat[i] * mh;
+        double t = (double)dm_freq(i0, n0) * R[I * dim] / L0;
+        if (dim == 2) t += (double)dm_freq(i1, n1) * R[I * dim + 1] / L1;
+        t -= rint(t);
         double sn, cs;
-        sincospi(-2.0 * (double)m * R[I] / L, &sn, &cs);
+        sincospi(-2.0 * t, &sn, &cs);
         // Re( amp (cs + i sn) * conj(rho) ) = amp (cs rho.x + sn rho.y)
         const double2 r = rhot[i];
         s += amp * (cs * r.x + sn * r.y);
@@ -148,70 +159,96 @@ __global__ void k_dloc(int N, double L, const double* __restrict__ khat, const d
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-        dloc[I] = t / (double)N;
+        dloc[((size_t)I * dim + a) * dim + b] = t / (double)N;
     }
 }
 
-// hpair[I + J NA] = phi''(R_I - R_J) = -(1/Omega) sum_k Khat mhat^2 k^2 cos(k d)   (1D)
-__global__ void k_eii_pairs(int N, double L, double Omega, const double* __restrict__ khat,
-                            const double* __restrict__ kfull, double Z, double sigma, const double* __restrict__ R,
-                            int NA, double* __restrict__ hpair) {
-    __shared__ double red[32];
+// Ion-ion pair Hessian (reading R4): for I != J,
+// hpair[((I NA + J) d + a) d + b] = phi''_ab(R_I - R_J) = -(1/Omega) sum_k Khat mhat^2 k_a k_b cos(k.d).
+__global__ void k_eii_pairs(int n0, int n1, int dim, double L0, double L1, double Omega,
+                            const double* __restrict__ khat, const double* __restrict__ kax0,
+                            const double* __restrict__ kax1, const double* __restrict__ k2, double Z,
+                            double sigma, const double* __restrict__ R, int NA, double* __restrict__ hpair) {
+    __shared__ double red[3][32];
     const int I = blockIdx.x, J = blockIdx.y;
+    const int nc = dim == 2 ? 3 : 1;
+    double* out = hpair + ((size_t)I * NA + J) * dim * dim;
     if (I == J) {
-        if (threadIdx.x == 0) hpair[I + J * NA] = 0.0;
+        if (threadIdx.x < dim * dim) out[threadIdx.x] = 0.0;
         return;
     }
-    const double d = R[I] - R[J];
-    double s = 0.0;
+    const int N = n0 * n1;
+    const double dx = R[I * dim] - R[J * dim];
+    const double dy = dim == 2 ? R[I * dim + 1] - R[J * dim + 1] : 0.0;
+    double s[3] = {0.0, 0.0, 0.0};
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const int m = (i < (N + 1) / 2) ? i : i - N;
-        const double k = kfull[i];
-        const double mh2 = Z * Z * exp(-sigma * sigma * k * k);
-        s += khat[i] * mh2 * k * k * cospi(2.0 * (double)m * d / L);
+        const int i0 = i / n1, i1 = i - i0 * n1;
+        const double mh2 = Z * Z * exp(-sigma * sigma * k2[i]);
+        double t = (double)dm_freq(i0, n0) * dx / L0;
+        if (dim == 2) t += (double)dm_freq(i1, n1) * dy / L1;
+        t -= rint(t);
+        const double w = khat[i] * mh2 * cospi(2.0 * t);
+        const double kx = kax0[i0];
+        if (dim == 1) {
+            s[0] += w * kx * kx;
+        } else {
+            const double ky = kax1[i1];
+            s[0] += w * kx * kx;
+            s[1] += w * kx * ky;
+            s[2] += w * ky * ky;
+        }
     }
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    for (int q = 0; q < nc; ++q) {
+        for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+        if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = s[q];
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < nc) {
         double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-        hpair[I + J * NA] = -t / Omega;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[threadIdx.x][w];
+        t = -t / Omega;
+        if (dim == 1) out[0] = t;
+        else if (threadIdx.x == 0) out[0] = t;
+        else if (threadIdx.x == 1) { out[1] = t; out[2] = t; }
+        else out[3] = t;
     }
 }
 
-// D = D_chi + D_loc + D_II, mass-scaled and symmetrised (1D: index I).
-__global__ void k_assemble_D(int NA, const double* __restrict__ Dchi, const double* __restrict__ dloc,
+// D = D_chi + D_loc + D_II (Eq. SecDeriv), mass-scaled and symmetrised; index (I, a) -> I d + a.
+// D_II[(I,a),(J,b)] = -phi''_ab(R_I - R_J) (I != J);  D_II[(I,a),(I,b)] = sum_{K != I} phi''_ab(R_I - R_K).
+__global__ void k_assemble_D(int NA, int dim, const double* __restrict__ Dchi, const double* __restrict__ dloc,
                              const double* __restrict__ hpair, const double* __restrict__ mass,
                              double* __restrict__ D) {
-    const int I = blockIdx.x * blockDim.x + threadIdx.x;
-    const int J = blockIdx.y;
-    if (I >= NA) return;
-    auto entry = [&](int a, int b) {
-        double v = Dchi[(size_t)b * NA + a];
-        if (a == b) {
-            v += dloc[a];
+    const int n = NA * dim;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;  // row (I, a)
+    const int q = blockIdx.y;                             // column (J, b)
+    if (p >= n) return;
+    auto entry = [&](int r, int c) {
+        const int I = r / dim, a = r % dim, J = c / dim, b = c % dim;
+        double v = Dchi[(size_t)c * n + r];
+        if (I == J) {
+            v += dloc[((size_t)I * dim + a) * dim + b];
             double s = 0.0;
-            for (int K = 0; K < NA; ++K) s += hpair[a + K * NA];
+            for (int K = 0; K < NA; ++K) s += hpair[(((size_t)I * NA + K) * dim + a) * dim + b];
             v += s;
         } else {
-            v -= hpair[a + b * NA];
+            v -= hpair[(((size_t)I * NA + J) * dim + a) * dim + b];
         }
         return v;
     };
-    const double v = 0.5 * (entry(I, J) + entry(J, I));
-    const double mm = mass ? sqrt(mass[I] * mass[J]) : 1.0;
-    D[(size_t)J * NA + I] = v / mm;
+    const double v = 0.5 * (entry(p, q) + entry(q, p));
+    const double mm = mass ? sqrt(mass[p / dim] * mass[q / dim]) : 1.0;
+    D[(size_t)q * n + p] = v / mm;
 }
 
 void dynamical_matrix(acp_context* ctx, const double* h_R, const double* rho, const double* G, const double* U,
                       const double* h_masses, double* h_D, double* h_lambda) {
-    ACP_REQUIRE(ctx->dim == 1, "2D dynamical matrix not built in this round");
     const int Ng = ctx->Ng;
     const int NA = ctx->sys.n_atoms;
-    const int n = NA;
-    double* dR = ctx->wsd("dm_R", NA);
-    ACP_CUDA(cudaMemcpyAsync(dR, h_R, NA * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    const int dim = ctx->dim;
+    const int n = dim * NA;
+    double* dR = ctx->wsd("dm_R", (size_t)NA * dim);
+    ACP_CUDA(cudaMemcpyAsync(dR, h_R, (size_t)NA * dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     double* dm = nullptr;
     if (h_masses) {
         dm = ctx->wsd("dm_mass", NA);
@@ -221,16 +258,21 @@ void dynamical_matrix(acp_context* ctx, const double* h_R, const double* rho, co
     gemm_tn(ctx, Ng, n, n, ctx->dV, G, Ng, U, Ng, Dchi);
     double2* rhot = static_cast<double2*>(ctx->ws("dm_rhot", (size_t)Ng * sizeof(double2)));
     real_spectrum(ctx, rho, rhot);
-    double* dloc = ctx->wsd("dm_dloc", NA);
-    k_dloc<<<NA, 256, 0, ctx->stream>>>(Ng, ctx->sys.cell[0], ctx->d_khat, ctx->d_kodd, ctx->d_k2, ctx->sys.Z,
-                                         ctx->sys.sigma, dR, rhot, dloc);
+    double* dloc = ctx->wsd("dm_dloc", (size_t)NA * dim * dim);
+    const double* kodd1 = dim == 2 ? ctx->d_kaxodd[1] : ctx->d_kaxodd[0];
+    const double* kax1 = dim == 2 ? ctx->d_kax[1] : ctx->d_kax[0];
+    k_dloc<<<dim3(NA, dim * dim), 256, 0, ctx->stream>>>(ctx->n[0], ctx->n[1], dim, ctx->sys.cell[0],
+                                                          ctx->sys.cell[1], ctx->d_khat, ctx->d_k2,
+                                                          ctx->d_kaxodd[0], kodd1, ctx->sys.Z, ctx->sys.sigma, dR,
+                                                          rhot, dloc);
     launched(ctx);
-    double* hpair = ctx->wsd("dm_hpair", (size_t)NA * NA);
-    k_eii_pairs<<<dim3(NA, NA), 256, 0, ctx->stream>>>(Ng, ctx->sys.cell[0], ctx->Omega, ctx->d_khat, ctx->d_kfull,
-                                                        ctx->sys.Z, ctx->sys.sigma, dR, NA, hpair);
+    double* hpair = ctx->wsd("dm_hpair", (size_t)NA * NA * dim * dim);
+    k_eii_pairs<<<dim3(NA, NA), 256, 0, ctx->stream>>>(ctx->n[0], ctx->n[1], dim, ctx->sys.cell[0],
+                                                        ctx->sys.cell[1], ctx->Omega, ctx->d_khat, ctx->d_kax[0],
+                                                        kax1, ctx->d_k2, ctx->sys.Z, ctx->sys.sigma, dR, NA, hpair);
     launched(ctx);
     double* D = ctx->wsd("dm_D", (size_t)n * n);
-    k_assemble_D<<<dim3(cdiv(NA, 128), NA), 128, 0, ctx->stream>>>(NA, Dchi, dloc, hpair, dm, D);
+    k_assemble_D<<<dim3(cdiv(n, 128), n), 128, 0, ctx->stream>>>(NA, dim, Dchi, dloc, hpair, dm, D);
     launched(ctx);
     ACP_CUDA(cudaMemcpyAsync(h_D, D, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     if (h_lambda) {
@@ -246,7 +288,7 @@ void dynamical_matrix(acp_context* ctx, const double* h_R, const double* rho, co
 void perturbations(acp_context* ctx, const double* h_R, double* G) {
     const int NA = ctx->sys.n_atoms;
     const int n = ctx->dim * NA;
-    double* dR = ctx->wsd("pt_R", (size_t)NA * ctx->dim);
+    double* dR = ctx->wsd("pt_R", (size_t)NA * ctx->dim);  // N_A x d row-major
     ACP_CUDA(cudaMemcpyAsync(dR, h_R, (size_t)NA * ctx->dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     double2* spec = static_cast<double2*>(ctx->ws("pt_spec", (size_t)ctx->Ng * n * sizeof(double2)));
     spectrum_G(ctx, dR, spec);

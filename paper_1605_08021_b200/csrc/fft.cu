@@ -1,18 +1,34 @@
-// fft.cu -- in-house fp64 FFT in shared memory and the Fourier-operator kernel (K1).
+// fft.cu -- in-house fp64 FFTs and the Fourier-operator kernel (K1), 1D and 2D.
 //
 // The Hamiltonian apply of PAPER.md:189 (Eq. Hamil), H psi = -1/2 Delta psi + V psi,
 // uses the Fourier symbol |k|^2/2 for -1/2 Delta on the periodic grid (PAPER.md:852
-// "plane wave basis set").  One CTA transforms one PAIR of real columns packed as
-// z = a + i b (Hermitian multipliers keep the two results separable), with a
-// Stockham autosort FFT (radices 8/4/2/5/3) ping-ponging between two shared-memory
-// buffers; the pointwise (V - shift) multiply, the multiplier and the per-column
-// dot products are fused into the same pass, so each column is read once and
+// "plane wave basis set"); the Yukawa operator v_hxc = K (Eq. yukawa)
+// and the CG preconditioner are Fourier multipliers of the same kind.
+//
+// K1 computes Y = IFFT(mult . FFT(X)) + (diag - shift_j) (.) X for a batch of real
+// columns.  Two real columns are packed as z = a + i b (real-even symbols keep the two
+// results separable exactly), the inverse transform is conj -> forward FFT (1/N folded
+// into the symbol), and the pointwise (V - shift) multiply, the activity mask and the
+// per-column CG dot products are fused into the write: each column is read once and
 // written once from HBM.
-#include "common.cuh"
+//   1D: one CTA per column pair, in-place Stockham FFT in shared memory (fft_engine.cuh).
+//   2D (n0 x n1 grid): one thread-block CLUSTER of cs CTAs per column pair.  CTA r owns
+//       rows [r n0/cs, (r+1) n0/cs): row FFTs in its shared memory, then a transpose
+//       through distributed shared memory (each CTA gathers its n1/cs columns from every
+//       peer), column FFTs, symbol multiply, column FFTs, transpose back, row FFTs.
+//       The column-phase layout is padded (ld = n0 + 1) so the DSMEM transposes are
+//       bank-conflict free.  Per-column dot products are reduced over the cluster in
+//       rank order (deterministic).
+#include <cooperative_groups.h>
+
+#include "fft_engine.cuh"
 
 #include <cmath>
+#include <cstdlib>
 
 namespace acp {
+
+namespace cg = cooperative_groups;
 
 FftPlan make_plan(int N) {
     FftPlan p;
@@ -31,198 +47,117 @@ FftPlan make_plan(int N) {
     return p;
 }
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-// multiply by -i
-__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }
+// Geometry handed to every FFT kernel.
+struct FftGeom {
+    FftPlan p0, p1;   // axis 0 / axis 1 plans (1D: p0 only)
+    int n0, n1;       // grid (1D: n1 = 1)
+    int cs, r0, c1;   // 2D cluster size, rows and columns per CTA
+    int sh0, sh1;     // twiddle table splits
+    int tw0n, tw1n;   // twiddle entries
+    int ldc;          // column-phase leading dimension (n0 + 1)
+};
 
-// Forward DFTs of small radix, in registers: y_s = sum_r x_r exp(-2 pi i r s / R).
-template <int R> __device__ __forceinline__ void dft(double2* x);
-
-template <> __device__ __forceinline__ void dft<2>(double2* x) {
-    double2 a = x[0], b = x[1];
-    x[0] = cadd(a, b);
-    x[1] = csub(a, b);
-}
-template <> __device__ __forceinline__ void dft<4>(double2* x) {
-    double2 t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]);
-    double2 t2 = cadd(x[1], x[3]), t3 = mul_mi(csub(x[1], x[3]));
-    x[0] = cadd(t0, t2);
-    x[2] = csub(t0, t2);
-    x[1] = cadd(t1, t3);
-    x[3] = csub(t1, t3);
-}
-template <> __device__ __forceinline__ void dft<8>(double2* x) {
-    double2 e[4] = {x[0], x[2], x[4], x[6]};
-    double2 o[4] = {x[1], x[3], x[5], x[7]};
-    dft<4>(e);
-    dft<4>(o);
-    const double h = 0.70710678118654752440;  // sqrt(1/2)
-    // w8^k = exp(-i pi k / 4)
-    double2 o1 = make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-    double2 o2 = mul_mi(o[2]);
-    double2 o3 = make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
-    x[0] = cadd(e[0], o[0]);
-    x[4] = csub(e[0], o[0]);
-    x[1] = cadd(e[1], o1);
-    x[5] = csub(e[1], o1);
-    x[2] = cadd(e[2], o2);
-    x[6] = csub(e[2], o2);
-    x[3] = cadd(e[3], o3);
-    x[7] = csub(e[3], o3);
-}
-template <> __device__ __forceinline__ void dft<3>(double2* x) {
-    const double s1 = 0.86602540378443864676;  // sin(2 pi / 3)
-    double2 a = cadd(x[1], x[2]);
-    double2 b = csub(x[1], x[2]);
-    double2 y0 = cadd(x[0], a);
-    double2 t = make_double2(x[0].x - 0.5 * a.x, x[0].y - 0.5 * a.y);
-    double2 u = make_double2(s1 * b.y, -s1 * b.x);  // -i s1 b
-    x[0] = y0;
-    x[1] = cadd(t, u);
-    x[2] = csub(t, u);
-}
-template <> __device__ __forceinline__ void dft<5>(double2* x) {
-    const double c1 = 0.30901699437494742410;   // cos(2 pi/5)
-    const double c2 = -0.80901699437494742410;  // cos(4 pi/5)
-    const double s1 = 0.95105651629515357212;   // sin(2 pi/5)
-    const double s2 = 0.58778525229247312917;   // sin(4 pi/5)
-    double2 a1 = cadd(x[1], x[4]), b1 = csub(x[1], x[4]);
-    double2 a2 = cadd(x[2], x[3]), b2 = csub(x[2], x[3]);
-    double2 y0 = make_double2(x[0].x + a1.x + a2.x, x[0].y + a1.y + a2.y);
-    double2 t1 = make_double2(x[0].x + c1 * a1.x + c2 * a2.x, x[0].y + c1 * a1.y + c2 * a2.y);
-    double2 t2 = make_double2(x[0].x + c2 * a1.x + c1 * a2.x, x[0].y + c2 * a1.y + c1 * a2.y);
-    double2 u1 = make_double2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y);
-    double2 u2 = make_double2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y);
-    x[0] = y0;
-    x[1] = cadd(t1, mul_mi(u1));
-    x[4] = csub(t1, mul_mi(u1));
-    x[2] = cadd(t2, mul_mi(u2));
-    x[3] = csub(t2, mul_mi(u2));
+static FftGeom geom(const acp_context* ctx) {
+    FftGeom g;
+    g.p0 = ctx->plan;
+    g.p1 = ctx->plan1;
+    g.n0 = ctx->n[0];
+    g.n1 = ctx->n[1];
+    g.cs = ctx->cs;
+    g.r0 = ctx->r0;
+    g.c1 = ctx->c1;
+    g.sh0 = tw_split(g.n0);
+    g.sh1 = ctx->dim == 2 ? tw_split(g.n1) : 0;
+    g.tw0n = tw_entries(g.n0);
+    g.tw1n = ctx->dim == 2 ? tw_entries(g.n1) : 0;
+    g.ldc = g.n0 + 1;
+    return g;
 }
 
-// One Stockham pass of radix R: sub-transforms of length Ns are combined into
-// length Ns*R; input read with stride N/R, output written in natural order.
-template <int R>
-__device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, double2* __restrict__ dst,
-                                              int N, int Ns, const double2* __restrict__ tw) {
-    const int nb = N / R;
-    const int stride = N / (Ns * R);
-    for (int j = threadIdx.x; j < nb; j += blockDim.x) {
-        const int k = j % Ns;
-        double2 x[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) x[r] = src[j + r * nb];
-        if (Ns > 1) {
-#pragma unroll
-            for (int r = 1; r < R; ++r) x[r] = cmul(x[r], __ldg(&tw[r * k * stride]));
-        }
-        dft<R>(x);
-        const int base = (j - k) * R + k;
-#pragma unroll
-        for (int r = 0; r < R; ++r) dst[base + r * Ns] = x[r];
-    }
-}
+// I/O modes of the FFT kernels.
+enum { IO_OP = 0, IO_HERM = 1, IO_SPEC = 2 };
 
-// Forward FFT of a (length N) using b as scratch; returns the buffer holding the result.
-__device__ double2* fft_forward(double2* a, double2* b, const FftPlan& pl, const double2* __restrict__ tw) {
-    double2* src = a;
-    double2* dst = b;
-    int Ns = 1;
-    for (int p = 0; p < pl.npass; ++p) {
-        const int R = pl.radix[p];
-        switch (R) {
-            case 8: stockham_pass<8>(src, dst, pl.N, Ns, tw); break;
-            case 4: stockham_pass<4>(src, dst, pl.N, Ns, tw); break;
-            case 2: stockham_pass<2>(src, dst, pl.N, Ns, tw); break;
-            case 5: stockham_pass<5>(src, dst, pl.N, Ns, tw); break;
-            default: stockham_pass<3>(src, dst, pl.N, Ns, tw); break;
-        }
-        __syncthreads();
-        double2* t = src;
-        src = dst;
-        dst = t;
-        Ns *= R;
-    }
-    return src;
-}
+struct IoArgs {
+    FopArgs f;                  // IO_OP
+    const double2* spec = nullptr;  // IO_HERM: n spectra (N_g complex each)
+    double* out = nullptr;      // IO_HERM: n real columns
+    double scale = 1.0;         // IO_HERM
+    const double* x = nullptr;  // IO_SPEC: one real column
+    double2* sout = nullptr;    // IO_SPEC: its spectrum
+    int n = 0;                  // number of columns (IO_OP: f.n)
+};
 
-// Deterministic block sum of up to 2 values (fixed reduction tree).
-__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
-    }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-    __syncthreads();
-    if (l == 0) {
-        red[2 * w] = a;
-        red[2 * w + 1] = b;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s0 = 0.0, s1 = 0.0;
-        for (int i = 0; i < nw; ++i) {
-            s0 += red[2 * i];
-            s1 += red[2 * i + 1];
-        }
-        red[0] = s0;
-        red[1] = s1;
-    }
-    __syncthreads();
-    a = red[0];
-    b = red[1];
-}
-
-// K1: Y = IFFT(mult . FFT(X)) + (diag - shift_j) X for the column pair (2 blockIdx.x, +1).
-__global__ void __launch_bounds__(256) k_fourier_op(FftPlan pl, const double2* __restrict__ tw, FopArgs a) {
-    extern __shared__ double2 smem[];
-    const int N = pl.N;
-    double2* b0 = smem;
-    double2* b1 = smem + N;
-    __shared__ double red[2 * 32 + 4];
-    const int c0 = 2 * blockIdx.x;
-    const int c1 = c0 + 1;
-    const bool has1 = c1 < a.n;
+// ============================================================================ 1D
+template <int EPT, int IO>
+__global__ void __launch_bounds__(512) k_fft1d(FftGeom G, const double2* __restrict__ twg, IoArgs io) {
+    extern __shared__ __align__(16) double2 sm1[];
+    __shared__ double red[132];
+    const int N = G.n0;
+    double2* buf = sm1;
+    const int c0 = 2 * blockIdx.x, c1 = c0 + 1;
+    const int ncol = IO == IO_OP ? io.f.n : io.n;
+    const bool has1 = c1 < ncol;
     bool act0 = true, act1 = has1;
-    if (a.active) {
-        act0 = a.active[c0] != 0;
-        act1 = has1 && a.active[c1] != 0;
+    if (IO == IO_OP && io.f.active) {
+        act0 = io.f.active[c0] != 0;
+        act1 = has1 && io.f.active[c1] != 0;
     }
     if (!act0 && !act1) return;
-    const double* x0 = a.X + (size_t)c0 * N;
-    const double* x1 = a.X + (size_t)c1 * N;
-    for (int i = threadIdx.x; i < N; i += blockDim.x)
-        b0[i] = make_double2(x0[i], has1 ? x1[i] : 0.0);
+    const TwTable tw = load_twiddles(sm1 + N, twg, N, G.sh0);
+    const double* x0 = nullptr;
+    const double* x1 = nullptr;
+    if (IO == IO_OP) {
+        x0 = io.f.X + (size_t)c0 * N;
+        x1 = io.f.X + (size_t)c1 * N;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) buf[i] = make_double2(x0[i], has1 ? x1[i] : 0.0);
+    } else if (IO == IO_HERM) {
+        const double2* s0 = io.spec + (size_t)c0 * N;
+        const double2* s1 = io.spec + (size_t)c1 * N;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            const double2 p = s0[i];
+            const double2 q = has1 ? s1[i] : make_double2(0.0, 0.0);
+            buf[i] = make_double2(p.x - q.y, -(p.y + q.x));  // conj(P + i Q)
+        }
+    } else {
+        for (int i = threadIdx.x; i < N; i += blockDim.x) buf[i] = make_double2(io.x[i], 0.0);
+    }
     __syncthreads();
-    double2* F = nullptr;
-    if (a.mult) {
-        F = fft_forward(b0, b1, pl, tw);
+    const bool do_fft = IO != IO_OP || io.f.mult != nullptr;
+    if (do_fft) fft_inplace<EPT>(buf, N, 1, G.p0, tw);
+    if (IO == IO_HERM) {
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            io.out[(size_t)c0 * N + i] = buf[i].x * io.scale;
+            if (has1) io.out[(size_t)c1 * N + i] = -buf[i].y * io.scale;
+        }
+        return;
+    }
+    if (IO == IO_SPEC) {
+        for (int i = threadIdx.x; i < N; i += blockDim.x) io.sout[i] = buf[i];
+        return;
+    }
+    const FopArgs& a = io.f;
+    if (do_fft) {
         // conj(mult * F) then forward FFT == N * conj(IFFT(mult * F)) (1/N folded into mult)
         for (int i = threadIdx.x; i < N; i += blockDim.x) {
             const double m = __ldg(&a.mult[i]);
-            double2 v = F[i];
-            F[i] = make_double2(m * v.x, -m * v.y);
+            const double2 v = buf[i];
+            buf[i] = make_double2(m * v.x, -m * v.y);
         }
         __syncthreads();
-        double2* other = (F == b0) ? b1 : b0;
-        F = fft_forward(F, other, pl, tw);
+        fft_inplace<EPT>(buf, N, 1, G.p0, tw);
     }
     const double s0 = a.shift ? a.shift[c0] : 0.0;
     const double s1 = (a.shift && has1) ? a.shift[c1] : 0.0;
-    double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
     double* y0 = a.Y + (size_t)c0 * N;
     double* y1 = a.Y + (size_t)c1 * N;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         const double u0 = x0[i];
         const double u1 = has1 ? x1[i] : 0.0;
         double v0 = 0.0, v1 = 0.0;
-        if (F) {
-            v0 = F[i].x;
-            v1 = -F[i].y;
+        if (do_fft) {
+            v0 = buf[i].x;
+            v1 = -buf[i].y;
         }
         if (a.diag) {
             const double dg = a.diag[i];
@@ -234,41 +169,267 @@ __global__ void __launch_bounds__(256) k_fourier_op(FftPlan pl, const double2* _
         }
         if (act0) y0[i] = v0;
         if (act1) y1[i] = v1;
-        d00 += u0 * v0;
-        d01 += u0 * u0;
-        d10 += u1 * v1;
-        d11 += u1 * u1;
+        d[0] += u0 * v0;
+        d[1] += u0 * u0;
+        d[2] += u1 * v1;
+        d[3] += u1 * u1;
     }
     if (a.dots) {
-        block_sum2(d00, d01, red);
-        block_sum2(d10, d11, red);
+        block_sum4(d, red);
         if (threadIdx.x == 0) {
             if (act0) {
-                a.dots[2 * c0] = d00;
-                a.dots[2 * c0 + 1] = d01;
+                a.dots[2 * c0] = d[0];
+                a.dots[2 * c0 + 1] = d[1];
             }
             if (act1) {
-                a.dots[2 * c1] = d10;
-                a.dots[2 * c1 + 1] = d11;
+                a.dots[2 * c1] = d[2];
+                a.dots[2 * c1 + 1] = d[3];
             }
         }
     }
 }
 
-static int fop_threads(int N) {
-    int t = N / 8;
-    if (t < 64) t = 64;
-    if (t > 256) t = 256;
-    return (t + 31) / 32 * 32;
+// ============================================================================ 2D
+// Transposes through distributed shared memory.  Row phase: buf[il * n1 + k1] (il < r0).
+// Column phase: buf[c * ldc + k0] (c < c1).  Two cluster barriers each: one before the
+// remote reads (peers finished writing), one after (peers may overwrite their buffer).
+template <int EPT>
+__device__ __forceinline__ void rows_to_cols(cg::cluster_group& cl, double2* buf, const FftGeom& G, int rank) {
+    double2 v[EPT];
+    const int E = G.n0 * G.c1;
+    cl.sync();
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+        const int e = threadIdx.x + q * blockDim.x;
+        if (e < E) {
+            const int i = e / G.c1, c = e - i * G.c1;
+            const int src = i / G.r0, il = i - src * G.r0;
+            const double2* rb = cl.map_shared_rank(buf, src);
+            v[q] = rb[il * G.n1 + rank * G.c1 + c];
+        }
+    }
+    cl.sync();
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+        const int e = threadIdx.x + q * blockDim.x;
+        if (e < E) {
+            const int i = e / G.c1, c = e - i * G.c1;
+            buf[c * G.ldc + i] = v[q];
+        }
+    }
+    __syncthreads();
+}
+
+template <int EPT>
+__device__ __forceinline__ void cols_to_rows(cg::cluster_group& cl, double2* buf, const FftGeom& G, int rank) {
+    double2 v[EPT];
+    const int E = G.r0 * G.n1;
+    cl.sync();
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+        const int e = threadIdx.x + q * blockDim.x;
+        if (e < E) {
+            const int il = e / G.n1, k1 = e - il * G.n1;
+            const int src = k1 / G.c1, c = k1 - src * G.c1;
+            const double2* rb = cl.map_shared_rank(buf, src);
+            v[q] = rb[c * G.ldc + rank * G.r0 + il];
+        }
+    }
+    cl.sync();
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+        const int e = threadIdx.x + q * blockDim.x;
+        if (e < E) buf[e] = v[q];
+    }
+    __syncthreads();
+}
+
+// One column pair (or spectrum pair / single column) per cluster; grid (cs, pairs).
+template <int EPT, int IO>
+__global__ void __launch_bounds__(512) k_fft2d(FftGeom G, const double2* __restrict__ tw0g,
+                                               const double2* __restrict__ tw1g, IoArgs io, int pair0) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double2 sm2[];
+    __shared__ double red[132];
+    __shared__ double part[4];
+    const int rank = (int)cl.block_rank();
+    const int N = G.n0 * G.n1;
+    const int bufn = G.c1 * G.ldc > G.r0 * G.n1 ? G.c1 * G.ldc : G.r0 * G.n1;
+    double2* buf = sm2;
+    const int pair = pair0 + blockIdx.y;
+    const int c0 = 2 * pair, c1 = c0 + 1;
+    const int ncol = IO == IO_OP ? io.f.n : io.n;
+    const bool has1 = c1 < ncol;
+    bool act0 = true, act1 = has1;
+    if (IO == IO_OP && io.f.active) {
+        act0 = io.f.active[c0] != 0;
+        act1 = has1 && io.f.active[c1] != 0;
+    }
+    if (!act0 && !act1) return;  // uniform over the cluster
+    const TwTable tw0 = load_twiddles(sm2 + bufn, tw0g, G.n0, G.sh0);
+    const TwTable tw1 = load_twiddles(sm2 + bufn + G.tw0n, tw1g, G.n1, G.sh1);
+    const int E = G.r0 * G.n1;            // elements owned in the row phase
+    const size_t rowbase = (size_t)rank * G.r0 * G.n1;
+    const double* x0 = nullptr;
+    const double* x1 = nullptr;
+    if (IO == IO_OP) {
+        x0 = io.f.X + (size_t)c0 * N + rowbase;
+        x1 = io.f.X + (size_t)c1 * N + rowbase;
+        for (int e = threadIdx.x; e < E; e += blockDim.x) buf[e] = make_double2(x0[e], has1 ? x1[e] : 0.0);
+    } else if (IO == IO_HERM) {
+        const double2* s0 = io.spec + (size_t)c0 * N + rowbase;
+        const double2* s1 = io.spec + (size_t)c1 * N + rowbase;
+        for (int e = threadIdx.x; e < E; e += blockDim.x) {
+            const double2 p = s0[e];
+            const double2 q = has1 ? s1[e] : make_double2(0.0, 0.0);
+            buf[e] = make_double2(p.x - q.y, -(p.y + q.x));
+        }
+    } else {
+        for (int e = threadIdx.x; e < E; e += blockDim.x) buf[e] = make_double2(io.x[rowbase + e], 0.0);
+    }
+    __syncthreads();
+    const bool do_fft = IO != IO_OP || io.f.mult != nullptr;
+    if (do_fft) {
+        fft_inplace<EPT>(buf, G.n1, G.r0, G.p1, tw1);       // rows (length n1)
+        rows_to_cols<EPT>(cl, buf, G, rank);
+        fft_inplace<EPT>(buf, G.ldc, G.c1, G.p0, tw0);      // columns (length n0)
+    }
+    if (IO == IO_HERM || IO == IO_SPEC) {
+        // write from the column phase: bin / point (k0, k1 = rank c1 + c) -> k0 n1 + k1
+        const int Ec = G.n0 * G.c1;
+        for (int e = threadIdx.x; e < Ec; e += blockDim.x) {
+            const int k0 = e / G.c1, c = e - k0 * G.c1;
+            const double2 v = buf[c * G.ldc + k0];
+            const size_t o = (size_t)k0 * G.n1 + rank * G.c1 + c;
+            if (IO == IO_SPEC) {
+                io.sout[o] = v;
+            } else {
+                io.out[(size_t)c0 * N + o] = v.x * io.scale;
+                if (has1) io.out[(size_t)c1 * N + o] = -v.y * io.scale;
+            }
+        }
+        return;  // the last remote read (rows_to_cols) is behind a cluster barrier
+    }
+    const FopArgs& a = io.f;
+    if (do_fft) {
+        const int Ec = G.n0 * G.c1;
+        for (int e = threadIdx.x; e < Ec; e += blockDim.x) {
+            const int k0 = e / G.c1, c = e - k0 * G.c1;
+            const double m = __ldg(&a.mult[(size_t)k0 * G.n1 + rank * G.c1 + c]);
+            const double2 v = buf[c * G.ldc + k0];
+            buf[c * G.ldc + k0] = make_double2(m * v.x, -m * v.y);
+        }
+        __syncthreads();
+        fft_inplace<EPT>(buf, G.ldc, G.c1, G.p0, tw0);      // columns
+        cols_to_rows<EPT>(cl, buf, G, rank);
+        fft_inplace<EPT>(buf, G.n1, G.r0, G.p1, tw1);       // rows
+    }
+    const double s0 = a.shift ? a.shift[c0] : 0.0;
+    const double s1 = (a.shift && has1) ? a.shift[c1] : 0.0;
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
+    double* y0 = a.Y + (size_t)c0 * N + rowbase;
+    double* y1 = a.Y + (size_t)c1 * N + rowbase;
+    const double* dg = a.diag ? a.diag + rowbase : nullptr;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const double u0 = x0[e];
+        const double u1 = has1 ? x1[e] : 0.0;
+        double v0 = 0.0, v1 = 0.0;
+        if (do_fft) {
+            v0 = buf[e].x;
+            v1 = -buf[e].y;
+        }
+        if (dg) {
+            const double w = dg[e];
+            v0 += (w - s0) * u0;
+            v1 += (w - s1) * u1;
+        } else if (a.shift) {
+            v0 -= s0 * u0;
+            v1 -= s1 * u1;
+        }
+        if (act0) y0[e] = v0;
+        if (act1) y1[e] = v1;
+        d[0] += u0 * v0;
+        d[1] += u0 * u0;
+        d[2] += u1 * v1;
+        d[3] += u1 * u1;
+    }
+    if (a.dots) {
+        block_sum4(d, red);
+        if (threadIdx.x < 4) part[threadIdx.x] = d[threadIdx.x];
+        cl.sync();
+        if (rank == 0 && threadIdx.x < 4) {
+            double s = 0.0;
+            for (int q = 0; q < G.cs; ++q) s += cl.map_shared_rank(part, q)[threadIdx.x];  // rank order
+            const int col = threadIdx.x < 2 ? c0 : c1;
+            const bool act = threadIdx.x < 2 ? act0 : act1;
+            if (act) a.dots[2 * col + (threadIdx.x & 1)] = s;
+        }
+        cl.sync();
+    }
+}
+
+// ============================================================================ launchers
+template <int IO>
+static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
+    if (ncols <= 0) return;
+    const FftGeom G = geom(ctx);
+    const int npair = (ncols + 1) / 2;
+    const int T = ctx->fthreads;
+    const size_t smem = ctx->fsmem;
+    if (ctx->dim == 1) {
+        auto kern = ctx->fept <= 4 ? k_fft1d<4, IO> : ctx->fept <= 8 ? k_fft1d<8, IO>
+                  : ctx->fept <= 12 ? k_fft1d<12, IO> : k_fft1d<16, IO>;
+        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<npair, T, smem, ctx->stream>>>(G, ctx->d_tw, io);
+        launched(ctx);
+        return;
+    }
+    auto kern = ctx->fept <= 4 ? k_fft2d<4, IO> : ctx->fept <= 8 ? k_fft2d<8, IO>
+              : ctx->fept <= 12 ? k_fft2d<12, IO> : k_fft2d<16, IO>;
+    ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (ctx->cs > 8) ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    for (int p0 = 0; p0 < npair; p0 += 32768) {
+        const int np = npair - p0 < 32768 ? npair - p0 : 32768;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ctx->cs, np, 1);
+        cfg.blockDim = dim3(T, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = ctx->cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, G, (const double2*)ctx->d_tw, (const double2*)ctx->d_tw1, io, p0));
+        launched(ctx);
+    }
 }
 
 void fourier_op(acp_context* ctx, const FopArgs& a) {
-    if (a.n <= 0) return;
-    const int N = ctx->plan.N;
-    const size_t smem = 2 * (size_t)N * sizeof(double2);
-    const int npair = (a.n + 1) / 2;
-    k_fourier_op<<<npair, fop_threads(N), smem, ctx->stream>>>(ctx->plan, ctx->d_tw, a);
-    launched(ctx);
+    IoArgs io;
+    io.f = a;
+    io.n = a.n;
+    launch_fft<IO_OP>(ctx, io, a.n);
+}
+
+void ifft_hermitian(acp_context* ctx, const double2* spec, int n, double* out) {
+    // (1/Omega) sum_k c_k e^{ikr} = (N/Omega) * (1/N) sum ...  -> scale = 1/Omega
+    IoArgs io;
+    io.spec = spec;
+    io.out = out;
+    io.n = n;
+    io.scale = 1.0 / ctx->Omega;
+    launch_fft<IO_HERM>(ctx, io, n);
+}
+
+void real_spectrum(acp_context* ctx, const double* x, double2* out) {
+    IoArgs io;
+    io.x = x;
+    io.sout = out;
+    io.n = 1;
+    launch_fft<IO_SPEC>(ctx, io, 1);
 }
 
 // ---- multipliers ----------------------------------------------------------
@@ -285,7 +446,7 @@ __global__ void k_make_mult(int N, const double* __restrict__ k2, const double* 
 
 const double* multiplier(acp_context* ctx, MultKind kind, double tau) {
     if (kind == MULT_NONE) return nullptr;
-    const int N = ctx->plan.N;
+    const int N = ctx->Ng;
     std::string name = "mult" + std::to_string((int)kind);
     double* m = ctx->wsd(name, N);
     k_make_mult<<<cdiv(N, 256), 256, 0, ctx->stream>>>(N, ctx->d_k2, ctx->d_khat, (int)kind, tau, m);
@@ -293,72 +454,51 @@ const double* multiplier(acp_context* ctx, MultKind kind, double tau) {
     return m;
 }
 
-// ---- Hermitian spectra -> real grid functions ------------------------------
-// out_j(r_alpha) = (1/Omega) sum_k spec_j(k) e^{i k r_alpha}, columns packed in pairs.
-__global__ void __launch_bounds__(256) k_ifft_hermitian(FftPlan pl, const double2* __restrict__ tw,
-                                                        const double2* __restrict__ spec, int n,
-                                                        double scale, double* __restrict__ out) {
-    extern __shared__ double2 smem[];
-    const int N = pl.N;
-    double2* b0 = smem;
-    double2* b1 = smem + N;
-    const int c0 = 2 * blockIdx.x, c1 = c0 + 1;
-    const bool has1 = c1 < n;
-    const double2* s0 = spec + (size_t)c0 * N;
-    const double2* s1 = spec + (size_t)c1 * N;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        double2 p = s0[i];
-        double2 q = has1 ? s1[i] : make_double2(0.0, 0.0);
-        // Z = P + i Q ; load conj(Z)
-        b0[i] = make_double2(p.x - q.y, -(p.y + q.x));
-    }
-    __syncthreads();
-    double2* F = fft_forward(b0, b1, pl, tw);
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        out[(size_t)c0 * N + i] = F[i].x * scale;
-        if (has1) out[(size_t)c1 * N + i] = -F[i].y * scale;
-    }
-}
-
-void ifft_hermitian(acp_context* ctx, const double2* spec, int n, double* out) {
-    const int N = ctx->plan.N;
-    const size_t smem = 2 * (size_t)N * sizeof(double2);
-    // (1/Omega) sum_k c_k e^{ikr} = (N/Omega) * (1/N) sum ...  -> scale = 1/Omega
-    k_ifft_hermitian<<<(n + 1) / 2, fop_threads(N), smem, ctx->stream>>>(ctx->plan, ctx->d_tw, spec, n,
-                                                                         1.0 / ctx->Omega, out);
-    launched(ctx);
-}
-
+// ---- model spectra ----------------------------------------------------------
 // Frequency integer m of FFT bin i (numpy fftfreq order).
 __device__ __forceinline__ int bin_freq(int i, int N) { return (i < (N + 1) / 2) ? i : i - N; }
 
-// spec_{I*d+a}(k) = -i k_a Khat(k) mhat(k) e^{-i k R_I},  mhat = -Z e^{-sigma^2 k^2 / 2}   (1D)
-__global__ void k_spectrum_G(int N, double L, const double* __restrict__ khat, const double* __restrict__ kodd,
-                             const double* __restrict__ k2, double Z, double sigma, const double* __restrict__ R,
-                             int NA, double2* __restrict__ spec) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int I = blockIdx.y;
-    if (i >= N || I >= NA) return;
-    const int m = bin_freq(i, N);
-    const double mh = -Z * exp(-0.5 * sigma * sigma * k2[i]);
-    double s, c;
-    sincospi(-2.0 * (double)m * R[I] / L, &s, &c);  // e^{-i k R}, k = 2 pi m / L
-    const double amp = khat[i] * mh;
-    // -i k a (c + i s) = k a (s - i c)
-    const double ka = kodd[i] * amp;
-    spec[(size_t)I * N + i] = make_double2(ka * s, -ka * c);
+// Phase e^{-i k.R} of bin (i0, i1) for position R (d components), as (cos, sin).
+__device__ __forceinline__ void bin_phase(int i0, int i1, int n0, int n1, double L0, double L1, int dim,
+                                          const double* R, double& c, double& s) {
+    double t = (double)bin_freq(i0, n0) * R[0] / L0;
+    if (dim == 2) t += (double)bin_freq(i1, n1) * R[1] / L1;
+    t -= rint(t);  // exact reduction of the turn count keeps sincospi accurate
+    sincospi(-2.0 * t, &s, &c);
 }
 
-__global__ void k_spectrum_m(int N, double L, const double* __restrict__ k2, double Z, double sigma,
+// spec_{I*d+a}(k) = -i k_a Khat(k) mhat(k) e^{-i k.R_I},  mhat = -Z e^{-sigma^2 |k|^2 / 2}
+__global__ void k_spectrum_G(int n0, int n1, int dim, double L0, double L1, const double* __restrict__ khat,
+                             const double* __restrict__ k2, const double* __restrict__ kodd0,
+                             const double* __restrict__ kodd1, double Z, double sigma,
                              const double* __restrict__ R, int NA, double2* __restrict__ spec) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int N = n0 * n1;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int I = blockIdx.y;
+    if (i >= N || I >= NA) return;
+    const int i0 = i / n1, i1 = i - i0 * n1;
+    const double mh = -Z * exp(-0.5 * sigma * sigma * k2[i]);
+    double s, c;
+    bin_phase(i0, i1, n0, n1, L0, L1, dim, R + (size_t)I * dim, c, s);
+    const double amp = khat[i] * mh;
+    for (int a = 0; a < dim; ++a) {
+        // -i k_a (c + i s) = k_a (s - i c)
+        const double ka = (a == 0 ? kodd0[i0] : kodd1[i1]) * amp;
+        spec[(size_t)(I * dim + a) * N + i] = make_double2(ka * s, -ka * c);
+    }
+}
+
+__global__ void k_spectrum_m(int n0, int n1, int dim, double L0, double L1, const double* __restrict__ k2, double Z,
+                             double sigma, const double* __restrict__ R, int NA, double2* __restrict__ spec) {
+    const int N = n0 * n1;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    const int m = bin_freq(i, N);
+    const int i0 = i / n1, i1 = i - i0 * n1;
     const double mh = -Z * exp(-0.5 * sigma * sigma * k2[i]);
     double re = 0.0, im = 0.0;
     for (int I = 0; I < NA; ++I) {
         double s, c;
-        sincospi(-2.0 * (double)m * R[I] / L, &s, &c);
+        bin_phase(i0, i1, n0, n1, L0, L1, dim, R + (size_t)I * dim, c, s);
         re += mh * c;
         im += mh * s;
     }
@@ -366,82 +506,135 @@ __global__ void k_spectrum_m(int N, double L, const double* __restrict__ k2, dou
 }
 
 void spectrum_G(acp_context* ctx, const double* d_R, double2* spec) {
-    ACP_REQUIRE(ctx->dim == 1, "2D perturbations not built in this round");
-    const int N = ctx->plan.N;
+    const int N = ctx->Ng;
     dim3 grid(cdiv(N, 256), ctx->sys.n_atoms);
-    k_spectrum_G<<<grid, 256, 0, ctx->stream>>>(N, ctx->sys.cell[0], ctx->d_khat, ctx->d_kodd, ctx->d_k2,
-                                                ctx->sys.Z, ctx->sys.sigma, d_R, ctx->sys.n_atoms, spec);
+    k_spectrum_G<<<grid, 256, 0, ctx->stream>>>(ctx->n[0], ctx->n[1], ctx->dim, ctx->sys.cell[0], ctx->sys.cell[1],
+                                                ctx->d_khat, ctx->d_k2, ctx->d_kaxodd[0],
+                                                ctx->dim == 2 ? ctx->d_kaxodd[1] : ctx->d_kaxodd[0], ctx->sys.Z,
+                                                ctx->sys.sigma, d_R, ctx->sys.n_atoms, spec);
     launched(ctx);
 }
 
 void spectrum_m(acp_context* ctx, const double* d_R, double2* spec) {
-    const int N = ctx->plan.N;
-    k_spectrum_m<<<cdiv(N, 256), 256, 0, ctx->stream>>>(N, ctx->sys.cell[0], ctx->d_k2, ctx->sys.Z,
-                                                        ctx->sys.sigma, d_R, ctx->sys.n_atoms, spec);
-    launched(ctx);
-}
-
-// Spectrum of one real column: out(k) = sum_a x(a) e^{-i k r_a}.
-__global__ void __launch_bounds__(256) k_real_spectrum(FftPlan pl, const double2* __restrict__ tw,
-                                                       const double* __restrict__ x, double2* __restrict__ out) {
-    extern __shared__ double2 smem[];
-    const int N = pl.N;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) smem[i] = make_double2(x[i], 0.0);
-    __syncthreads();
-    double2* F = fft_forward(smem, smem + N, pl, tw);
-    for (int i = threadIdx.x; i < N; i += blockDim.x) out[i] = F[i];
-}
-
-void real_spectrum(acp_context* ctx, const double* x, double2* out) {
-    const int N = ctx->plan.N;
-    k_real_spectrum<<<1, fop_threads(N), 2 * (size_t)N * sizeof(double2), ctx->stream>>>(ctx->plan, ctx->d_tw, x, out);
+    const int N = ctx->Ng;
+    k_spectrum_m<<<cdiv(N, 256), 256, 0, ctx->stream>>>(ctx->n[0], ctx->n[1], ctx->dim, ctx->sys.cell[0],
+                                                        ctx->sys.cell[1], ctx->d_k2, ctx->sys.Z, ctx->sys.sigma,
+                                                        d_R, ctx->sys.n_atoms, spec);
     launched(ctx);
 }
 
 // ---- plan / symbol setup ---------------------------------------------------
+static std::vector<double2> twiddle_table(int L) {
+    auto w = [L](long long m) {
+        long double ang = -2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)L;
+        return make_double2((double)cosl(ang), (double)sinl(ang));
+    };
+    const int sh = tw_split(L);
+    std::vector<double2> t;
+    if (sh == 0) {
+        for (int m = 0; m < L; ++m) t.push_back(w(m));
+    } else {
+        for (int m = 0; m < (1 << sh); ++m) t.push_back(w(m));              // lo
+        for (int m = 0; m <= (L >> sh); ++m) t.push_back(w((long long)m << sh));  // hi
+    }
+    return t;
+}
+
+template <class T>
+static T* upload(const std::vector<T>& v) {
+    T* d = nullptr;
+    ACP_CUDA(cudaMalloc(&d, v.size() * sizeof(T)));
+    ACP_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+}
+
+static int ept_for(int E, int T) {
+    const int need = (E + T - 1) / T;
+    return need <= 4 ? 4 : need <= 8 ? 8 : need <= 12 ? 12 : need <= 16 ? 16 : 0;
+}
+
 void fft_init(acp_context* ctx) {
-    ACP_REQUIRE(ctx->dim == 1, "only d = 1 grids are built in this round (2D is a later row)");
-    const int N = ctx->Ng;
-    ctx->plan = make_plan(N);
-    std::vector<double2> tw(N);
-    for (int m = 0; m < N; ++m) {
-        // exact argument reduction in long double, then round
-        long double ang = -2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)N;
-        tw[m] = make_double2((double)cosl(ang), (double)sinl(ang));
+    const int dim = ctx->dim;
+    ctx->n[0] = ctx->sys.grid[0];
+    ctx->n[1] = dim == 2 ? ctx->sys.grid[1] : 1;
+    const int n0 = ctx->n[0], n1 = ctx->n[1];
+    const int N = n0 * n1;
+    ctx->plan = make_plan(n0);
+    if (dim == 2) ctx->plan1 = make_plan(n1);
+    ctx->d_tw = upload(twiddle_table(n0));
+    if (dim == 2) ctx->d_tw1 = upload(twiddle_table(n1));
+    // per-axis frequencies and the N_g tables (bins in C order)
+    std::vector<double> kax[2], kodd[2];
+    for (int a = 0; a < dim; ++a) {
+        const int na = ctx->n[a];
+        const double L = ctx->sys.cell[a];
+        for (int i = 0; i < na; ++i) {
+            const int m = (i < (na + 1) / 2) ? i : i - na;
+            const double k = 2.0 * M_PI * (double)m / L;
+            kax[a].push_back(k);
+            kodd[a].push_back((na % 2 == 0 && i == na / 2) ? 0.0 : k);
+        }
+        ctx->d_kax[a] = upload(kax[a]);
+        ctx->d_kaxodd[a] = upload(kodd[a]);
     }
-    std::vector<double> k2(N), kodd(N), kfull(N), khat(N);
-    const double L = ctx->sys.cell[0];
-    for (int i = 0; i < N; ++i) {
-        int m = (i < (N + 1) / 2) ? i : i - N;
-        double k = 2.0 * M_PI * (double)m / L;
-        kfull[i] = k;
-        kodd[i] = (N % 2 == 0 && i == N / 2) ? 0.0 : k;
-        k2[i] = k * k;
-        khat[i] = 4.0 * M_PI / (ctx->sys.eps0 * (k * k + ctx->sys.kappa * ctx->sys.kappa));
+    ctx->d_kfull = ctx->d_kax[0];
+    ctx->d_kodd = ctx->d_kaxodd[0];
+    std::vector<double> k2(N), khat(N);
+    for (int i0 = 0; i0 < n0; ++i0)
+        for (int i1 = 0; i1 < n1; ++i1) {
+            double q = kax[0][i0] * kax[0][i0];
+            if (dim == 2) q += kax[1][i1] * kax[1][i1];
+            k2[(size_t)i0 * n1 + i1] = q;
+            khat[(size_t)i0 * n1 + i1] = 4.0 * M_PI / (ctx->sys.eps0 * (q + ctx->sys.kappa * ctx->sys.kappa));
+        }
+    ctx->d_k2 = upload(k2);
+    ctx->d_khat = upload(khat);
+    // launch geometry of the FFT kernels
+    if (dim == 1) {
+        int T = (N / 8 + 31) / 32 * 32;
+        T = T < 64 ? 64 : T > 512 ? 512 : T;
+        ctx->fthreads = T;
+        ctx->fept = ept_for(N, T);
+        ACP_REQUIRE(ctx->fept > 0, "1D grid too large for the shared-memory FFT");
+        ctx->fsmem = (size_t)(N + tw_entries(n0)) * sizeof(double2);
+        ACP_REQUIRE(ctx->fsmem <= 220 * 1024, "1D grid too large for the shared-memory FFT");
+    } else {
+        // smallest cluster whose per-CTA slice fits ~100 KB (2+ CTAs per SM), cs | n0 and cs | n1
+        int cs = 1;
+        auto bytes = [&](int c) {
+            const int rows = (n0 / c) * n1, cols = (n1 / c) * (n0 + 1);
+            return (size_t)((rows > cols ? rows : cols) + tw_entries(n0) + tw_entries(n1)) * sizeof(double2);
+        };
+        while (cs < 16 && (bytes(cs) > 100 * 1024) && n0 % (2 * cs) == 0 && n1 % (2 * cs) == 0) cs *= 2;
+        // test knob: ACP_FFT2D_CS forces a larger cluster (exercises the DSMEM transposes on small grids)
+        if (const char* e = getenv("ACP_FFT2D_CS")) {
+            const int f = atoi(e);
+            if (f >= 1 && f <= 16 && n0 % f == 0 && n1 % f == 0) cs = f;
+        }
+        ACP_REQUIRE(n0 % cs == 0 && n1 % cs == 0, "2D grid not divisible by the cluster size");
+        ACP_REQUIRE(bytes(cs) <= 220 * 1024, "2D grid too large for a 16-CTA cluster FFT");
+        ctx->cs = cs;
+        ctx->r0 = n0 / cs;
+        ctx->c1 = n1 / cs;
+        const int E = ctx->r0 * n1 > ctx->c1 * n0 ? ctx->r0 * n1 : ctx->c1 * n0;
+        int T = (E / 12 + 31) / 32 * 32;
+        T = T < 64 ? 64 : T > 512 ? 512 : T;
+        ctx->fthreads = T;
+        ctx->fept = ept_for(E, T);
+        ACP_REQUIRE(ctx->fept > 0, "2D slice too large for the FFT engine");
+        ctx->fsmem = bytes(cs);
     }
-    ACP_CUDA(cudaMalloc(&ctx->d_tw, N * sizeof(double2)));
-    ACP_CUDA(cudaMalloc(&ctx->d_k2, N * sizeof(double)));
-    ACP_CUDA(cudaMalloc(&ctx->d_kodd, N * sizeof(double)));
-    ACP_CUDA(cudaMalloc(&ctx->d_kfull, N * sizeof(double)));
-    ACP_CUDA(cudaMalloc(&ctx->d_khat, N * sizeof(double)));
-    ACP_CUDA(cudaMemcpy(ctx->d_tw, tw.data(), N * sizeof(double2), cudaMemcpyHostToDevice));
-    ACP_CUDA(cudaMemcpy(ctx->d_k2, k2.data(), N * sizeof(double), cudaMemcpyHostToDevice));
-    ACP_CUDA(cudaMemcpy(ctx->d_kodd, kodd.data(), N * sizeof(double), cudaMemcpyHostToDevice));
-    ACP_CUDA(cudaMemcpy(ctx->d_kfull, kfull.data(), N * sizeof(double), cudaMemcpyHostToDevice));
-    ACP_CUDA(cudaMemcpy(ctx->d_khat, khat.data(), N * sizeof(double), cudaMemcpyHostToDevice));
-    const size_t smem = 2 * (size_t)N * sizeof(double2);
-    ACP_REQUIRE(smem <= 227 * 1024, "grid too large for the shared-memory FFT");
-    ACP_CUDA(cudaFuncSetAttribute(k_fourier_op, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ACP_CUDA(cudaFuncSetAttribute(k_ifft_hermitian, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ACP_CUDA(cudaFuncSetAttribute(k_real_spectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
 
 void fft_free(acp_context* ctx) {
     cudaFree(ctx->d_tw);
+    cudaFree(ctx->d_tw1);
     cudaFree(ctx->d_k2);
-    cudaFree(ctx->d_kodd);
-    cudaFree(ctx->d_kfull);
     cudaFree(ctx->d_khat);
+    for (int a = 0; a < 2; ++a) {
+        cudaFree(ctx->d_kax[a]);
+        cudaFree(ctx->d_kaxodd[a]);
+    }
 }
 
 }  // namespace acp

@@ -1,0 +1,201 @@
+// fft_engine.cuh -- in-place, batched fp64 Stockham FFT in shared memory (sm_100a).
+//
+// Used by the 1D Fourier operator (one CTA per column pair) and the 2D operator (a
+// thread-block cluster per column pair, rows / columns exchanged through DSMEM).
+// A pass of radix R over `nb` independent transforms of length L stored back to back:
+// every thread first loads ALL of its butterflies into registers (at most EPT complex
+// values per thread), the block synchronises, then writes the results into the SAME
+// buffer -- the set of locations read equals the set written, so one buffer suffices
+// (half the shared memory of a ping-pong Stockham).  Twiddles exp(-2 pi i m / L) come
+// from a shared-memory table.
+#pragma once
+
+#include "common.cuh"
+
+namespace acp {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }  // * (-i)
+
+// Forward DFTs of small radix, in registers: y_s = sum_r x_r exp(-2 pi i r s / R).
+template <int R> __device__ __forceinline__ void dft(double2* x);
+
+template <> __device__ __forceinline__ void dft<2>(double2* x) {
+    double2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+}
+template <> __device__ __forceinline__ void dft<4>(double2* x) {
+    double2 t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]);
+    double2 t2 = cadd(x[1], x[3]), t3 = mul_mi(csub(x[1], x[3]));
+    x[0] = cadd(t0, t2);
+    x[2] = csub(t0, t2);
+    x[1] = cadd(t1, t3);
+    x[3] = csub(t1, t3);
+}
+template <> __device__ __forceinline__ void dft<8>(double2* x) {
+    double2 e[4] = {x[0], x[2], x[4], x[6]};
+    double2 o[4] = {x[1], x[3], x[5], x[7]};
+    dft<4>(e);
+    dft<4>(o);
+    const double h = 0.70710678118654752440;  // sqrt(1/2)
+    double2 o1 = make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+    double2 o2 = mul_mi(o[2]);
+    double2 o3 = make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+    x[0] = cadd(e[0], o[0]);
+    x[4] = csub(e[0], o[0]);
+    x[1] = cadd(e[1], o1);
+    x[5] = csub(e[1], o1);
+    x[2] = cadd(e[2], o2);
+    x[6] = csub(e[2], o2);
+    x[3] = cadd(e[3], o3);
+    x[7] = csub(e[3], o3);
+}
+template <> __device__ __forceinline__ void dft<3>(double2* x) {
+    const double s1 = 0.86602540378443864676;  // sin(2 pi / 3)
+    double2 a = cadd(x[1], x[2]);
+    double2 b = csub(x[1], x[2]);
+    double2 y0 = cadd(x[0], a);
+    double2 t = make_double2(x[0].x - 0.5 * a.x, x[0].y - 0.5 * a.y);
+    double2 u = make_double2(s1 * b.y, -s1 * b.x);  // -i s1 b
+    x[0] = y0;
+    x[1] = cadd(t, u);
+    x[2] = csub(t, u);
+}
+template <> __device__ __forceinline__ void dft<5>(double2* x) {
+    const double c1 = 0.30901699437494742410;   // cos(2 pi/5)
+    const double c2 = -0.80901699437494742410;  // cos(4 pi/5)
+    const double s1 = 0.95105651629515357212;   // sin(2 pi/5)
+    const double s2 = 0.58778525229247312917;   // sin(4 pi/5)
+    double2 a1 = cadd(x[1], x[4]), b1 = csub(x[1], x[4]);
+    double2 a2 = cadd(x[2], x[3]), b2 = csub(x[2], x[3]);
+    double2 y0 = make_double2(x[0].x + a1.x + a2.x, x[0].y + a1.y + a2.y);
+    double2 t1 = make_double2(x[0].x + c1 * a1.x + c2 * a2.x, x[0].y + c1 * a1.y + c2 * a2.y);
+    double2 t2 = make_double2(x[0].x + c2 * a1.x + c1 * a2.x, x[0].y + c2 * a1.y + c1 * a2.y);
+    double2 u1 = make_double2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y);
+    double2 u2 = make_double2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y);
+    x[0] = y0;
+    x[1] = cadd(t1, mul_mi(u1));
+    x[4] = csub(t1, mul_mi(u1));
+    x[2] = cadd(t2, mul_mi(u2));
+    x[3] = csub(t2, mul_mi(u2));
+}
+
+// Twiddle table exp(-2 pi i m / L), m < L, in shared memory.  Long transforms use a
+// two-level table w(m) = hi[m >> sh] * lo[m & (2^sh - 1)] (each entry correctly rounded on
+// the host; the product adds <= 2 ulp) so the table costs O(sqrt L) shared memory.
+struct TwTable {
+    const double2* lo;
+    const double2* hi;
+    int sh;  // 0: single-level table in lo
+    __device__ __forceinline__ double2 operator()(int m) const {
+        if (sh == 0) return lo[m];
+        return cmul(hi[m >> sh], lo[m & ((1 << sh) - 1)]);
+    }
+};
+
+// One in-place Stockham pass of radix R over nb transforms of length L (transform t at buf + t*ld):
+// sub-transforms of length Ns are combined into length Ns*R.  EPT = max complex values a
+// thread holds (EPT >= nb*L / blockDim.x).  Ends with a block barrier.
+template <int R, int EPT>
+__device__ __forceinline__ void pass_inplace(double2* buf, int L, int ld, int nb, int Ns, const TwTable& tw) {
+    constexpr int MB = (EPT + R - 1) / R;
+    const int per = L / R;              // butterflies per transform
+    const int total = nb * per;
+    const int stride = L / (Ns * R);    // twiddle stride for this pass
+    double2 x[MB][R];
+#pragma unroll
+    for (int b = 0; b < MB; ++b) {
+        const int g = threadIdx.x + b * blockDim.x;
+        if (g < total) {
+            const int t = g / per, j = g - t * per;
+            const int k = j % Ns;
+            const double2* src = buf + t * ld;
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[b][r] = src[j + r * per];
+            if (Ns > 1) {
+#pragma unroll
+                for (int r = 1; r < R; ++r) x[b][r] = cmul(x[b][r], tw(r * k * stride));
+            }
+            dft<R>(x[b]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < MB; ++b) {
+        const int g = threadIdx.x + b * blockDim.x;
+        if (g < total) {
+            const int t = g / per, j = g - t * per;
+            const int k = j % Ns;
+            double2* dst = buf + t * ld + (j - k) * R + k;
+#pragma unroll
+            for (int r = 0; r < R; ++r) dst[r * Ns] = x[b][r];
+        }
+    }
+    __syncthreads();
+}
+
+// Forward FFT (exp(-i ...)) of nb transforms of length pl.N in place (transform t at buf + t*ld).
+template <int EPT>
+__device__ __forceinline__ void fft_inplace(double2* buf, int ld, int nb, const FftPlan& pl, const TwTable& tw) {
+    // The plan lists its radices in the fixed order 8, 4, 2, 5, 3 (make_plan); one loop per
+    // radix keeps the register allocation of each pass independent (a switch inside a single
+    // loop made ptxas keep every variant's butterfly registers live at once).
+    int Ns = 1, p = 0;
+    for (; p < pl.npass && pl.radix[p] == 8; ++p, Ns *= 8) pass_inplace<8, EPT>(buf, pl.N, ld, nb, Ns, tw);
+    for (; p < pl.npass && pl.radix[p] == 4; ++p, Ns *= 4) pass_inplace<4, EPT>(buf, pl.N, ld, nb, Ns, tw);
+    for (; p < pl.npass && pl.radix[p] == 2; ++p, Ns *= 2) pass_inplace<2, EPT>(buf, pl.N, ld, nb, Ns, tw);
+    for (; p < pl.npass && pl.radix[p] == 5; ++p, Ns *= 5) pass_inplace<5, EPT>(buf, pl.N, ld, nb, Ns, tw);
+    for (; p < pl.npass && pl.radix[p] == 3; ++p, Ns *= 3) pass_inplace<3, EPT>(buf, pl.N, ld, nb, Ns, tw);
+}
+
+// Host-side layout of a twiddle table for length L: returns the level split sh (0 = single level)
+// and the number of double2 entries (lo followed by hi).
+inline int tw_split(int L) {
+    if (L <= 512) return 0;
+    int sh = 1;
+    while ((1 << (2 * sh)) < L) ++sh;   // lo has 2^sh ~ sqrt(L) entries
+    return sh;
+}
+inline int tw_entries(int L) {
+    const int sh = tw_split(L);
+    return sh == 0 ? L : (1 << sh) + (L >> sh) + 1;
+}
+
+// Copy a twiddle table (global layout from tw_entries) into shared memory `dst` (no barrier).
+__device__ __forceinline__ TwTable load_twiddles(double2* dst, const double2* __restrict__ src, int L, int sh) {
+    const int n = sh == 0 ? L : (1 << sh) + (L >> sh) + 1;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    TwTable t;
+    t.lo = dst;
+    t.hi = sh == 0 ? dst : dst + (1 << sh);
+    t.sh = sh;
+    return t;
+}
+
+// Deterministic block sum of 4 values (fixed reduction tree); red needs 132 doubles.
+__device__ __forceinline__ void block_sum4(double* v, double* red) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) red[4 * w + q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double s = 0.0;
+        for (int i = 0; i < nw; ++i) s += red[4 * i + threadIdx.x];
+        red[128 + threadIdx.x] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = red[128 + q];
+}
+
+}  // namespace acp

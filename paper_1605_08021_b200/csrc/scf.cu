@@ -95,19 +95,21 @@ __global__ void k_scale(size_t n, double s, double* __restrict__ x) {
     if (i < n) x[i] *= s;
 }
 
-// plane-wave start: column j -> 1, cos(k1 x), sin(k1 x), cos(k2 x), ... (normalised)
-__global__ void k_plane_waves(int Ng, int nb, double L, double* __restrict__ X) {
+// Plane-wave start: column j = cos / sin (k_j . r) for the host-sorted list of the lowest
+// wave vectors (mode[j] = (m0, m1, kind), kind 0 = constant, 1 = cos, 2 = sin); the first
+// Rayleigh-Ritz orthonormalises the block.
+__global__ void k_plane_waves(int n0, int n1, int nb, const int* __restrict__ mode, double* __restrict__ X) {
+    const size_t Ng = (size_t)n0 * n1;
     size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= (size_t)Ng * nb) return;
+    if (e >= Ng * nb) return;
     const int a = (int)(e % Ng), j = (int)(e / Ng);
-    const double x = (double)a / (double)Ng;  // r / L
-    const double nrm = sqrt(2.0 / L);
-    double v;
-    if (j == 0) v = sqrt(1.0 / L);
-    else {
-        const int m = (j + 1) / 2;
-        v = (j % 2) ? nrm * cospi(2.0 * m * x) : nrm * sinpi(2.0 * m * x);
-    }
+    const int i0 = a / n1, i1 = a % n1;
+    const int m0 = mode[3 * j], m1 = mode[3 * j + 1], kind = mode[3 * j + 2];
+    double t = (double)m0 * i0 / n0 + (double)m1 * i1 / n1;
+    t -= rint(t);
+    double v = 1.0;
+    if (kind == 1) v = cospi(2.0 * t);
+    else if (kind == 2) v = sinpi(2.0 * t);
     X[e] = v;
 }
 
@@ -262,7 +264,6 @@ struct Eig {
 
 void ground_state(acp_context* ctx, const double* h_R, const acp_scf_opts& o, double* Psi, double* eps, double* rho,
                   double* V, double* G, double* h_info) {
-    ACP_REQUIRE(ctx->dim == 1, "2D ground state not built in this round");
     const int Ng = ctx->Ng;
     const int NA = ctx->sys.n_atoms;
     const int n_occ = ctx->sys.n_occ;
@@ -271,8 +272,9 @@ void ground_state(acp_context* ctx, const double* h_R, const acp_scf_opts& o, do
     ACP_REQUIRE(nb <= 1024, "block too large");
     const double Ne = ctx->sys.Z * NA;
     const size_t tot = (size_t)Ng * nb;
-    double* dR = ctx->wsd("gs_R", NA);
-    ACP_CUDA(cudaMemcpyAsync(dR, h_R, NA * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    const int dim = ctx->dim;
+    double* dR = ctx->wsd("gs_R", (size_t)NA * dim);
+    ACP_CUDA(cudaMemcpyAsync(dR, h_R, (size_t)NA * dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     if (G) perturbations(ctx, h_R, G);
     // pseudocharge m
     double2* spec = static_cast<double2*>(ctx->ws("gs_spec", (size_t)Ng * sizeof(double2)));
@@ -328,8 +330,32 @@ void ground_state(acp_context* ctx, const double* h_R, const acp_scf_opts& o, do
     E.multH = multH;
     E.hw.resize(nb);
     E.hres.resize(nb);
-    k_plane_waves<<<cdiv(tot, 256), 256, 0, ctx->stream>>>(Ng, nb, ctx->sys.cell[0], E.X);
-    launched(ctx);
+    {
+        // lowest |k|^2 wave vectors on a half plane (m0 > 0, or m0 == 0 and m1 > 0), cos and sin each
+        const int n0 = ctx->n[0], n1 = ctx->n[1];
+        const double L0 = ctx->sys.cell[0], L1 = dim == 2 ? ctx->sys.cell[1] : 1.0;
+        std::vector<std::pair<double, std::pair<int, int>>> ks;
+        const int r0 = std::min(n0 / 2 - 1, 64), r1 = dim == 2 ? std::min(n1 / 2 - 1, 64) : 0;
+        for (int m0 = 0; m0 <= r0; ++m0)
+            for (int m1 = -r1; m1 <= r1; ++m1) {
+                if (m0 == 0 && m1 <= 0) continue;
+                const double k2v = (m0 / L0) * (m0 / L0) + (dim == 2 ? (m1 / L1) * (m1 / L1) : 0.0);
+                ks.push_back({k2v, {m0, m1}});
+            }
+        std::stable_sort(ks.begin(), ks.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        std::vector<int> mode(3 * (size_t)nb);
+        mode[0] = mode[1] = mode[2] = 0;
+        for (int j = 1; j < nb; ++j) {
+            const auto& kk = ks.at((size_t)(j - 1) / 2).second;
+            mode[3 * j] = kk.first;
+            mode[3 * j + 1] = kk.second;
+            mode[3 * j + 2] = (j % 2) ? 1 : 2;
+        }
+        int* dmode = ctx->wsi("gs_mode", 3 * (size_t)nb);
+        ACP_CUDA(cudaMemcpy(dmode, mode.data(), mode.size() * sizeof(int), cudaMemcpyHostToDevice));
+        k_plane_waves<<<cdiv(tot, 256), 256, 0, ctx->stream>>>(n0, n1, nb, dmode, E.X);
+        launched(ctx);
+    }
     // Anderson history
     const int hist = std::max(1, o.history);
     double* Xh = ctx->wsd("gs_Xh", (size_t)Ng * (hist + 1));

@@ -13,7 +13,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from workloads import atom_positions, get_config, sketch_draws  # noqa: E402
-from workloads.configs import small_config  # noqa: E402
+from workloads.configs import small_config, small_config_2d  # noqa: E402
 from oracle.model import Model  # noqa: E402
 from oracle.scf import scf  # noqa: E402
 from oracle import acp as oacp, phonon as ophonon, response as ors  # noqa: E402
@@ -56,12 +56,12 @@ _cache = {}
 
 def system(name):
     if name not in _cache:
-        cfg = small_config() if name == "tiny4" else get_config(name)
+        cfg = {"tiny4": small_config, "tiny2d": small_config_2d}.get(name, lambda: get_config(name))()
         _cache[name] = Sys(cfg)
     return _cache[name]
 
 
-@pytest.fixture(scope="module", params=["tiny4", "c0_1d_tiny"])
+@pytest.fixture(scope="module", params=["tiny4", "c0_1d_tiny", "tiny2d"])
 def sysx(request):
     return system(request.param)
 
@@ -82,6 +82,44 @@ def test_fourier_operators(sysx):
         ref = s.m.kinetic(X) + (s.gs.V[:, None] - shifts[None, :]) * X
         assert rel(Y, ref) < 1e-12
         assert rel(Y, (s.H @ X) - shifts[None, :] * X) < 1e-11
+
+
+@pytest.mark.parametrize("cs", [1, 2, 4, 8])
+def test_fourier_operator_2d_cluster_sizes(cs, monkeypatch):
+    """2D K1 with the DSMEM transposes of a cs-CTA cluster (forced via ACP_FFT2D_CS) vs the oracle."""
+    from paper_1605_08021_b200 import Context
+    s = system("tiny2d")
+    monkeypatch.setenv("ACP_FFT2D_CS", str(cs))
+    ctx = Context.from_config(s.cfg)
+    rng = np.random.default_rng(20 + cs)
+    for ncol in (1, 4, 7):
+        X = rng.standard_normal((s.m.Ng, ncol))
+        Xt = T(X.T)
+        assert rel(ctx.fourier_apply(Xt, 0).cpu().numpy().T, s.m.kinetic(X)) < 1e-12
+        assert rel(ctx.fourier_apply(Xt, 1).cpu().numpy().T, s.m.yukawa(X)) < 1e-12
+        shifts = rng.uniform(-0.1, 0.1, ncol)
+        Y = ctx.fourier_apply(Xt, 0, diag=s.V_t, shift=T(shifts)).cpu().numpy().T
+        assert rel(Y, (s.H @ X) - shifts[None, :] * X) < 1e-11
+    assert rel(ctx.perturbations(s.R).cpu().numpy().T, s.G) < 1e-12
+    ctx.close()
+
+
+@pytest.mark.parametrize("cs", [1, 8])
+def test_fourier_operator_rectangular_grid(cs, monkeypatch):
+    """Non-square 2D grid and cell (axis bookkeeping): kinetic symbol vs numpy's FFT."""
+    from paper_1605_08021_b200 import Context
+    monkeypatch.setenv("ACP_FFT2D_CS", str(cs))
+    n0, n1, L0, L1 = 24, 40, 10.0, 16.0
+    ctx = Context(2, (n0, n1), (L0, L1), 2, 2, 2.0, 2.0, 1.0, 0.01, 1.0)
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((3, n0, n1))
+    k0 = 2 * np.pi * np.fft.fftfreq(n0, d=L0 / n0)
+    k1 = 2 * np.pi * np.fft.fftfreq(n1, d=L1 / n1)
+    k2 = k0[:, None] ** 2 + k1[None, :] ** 2
+    ref = np.real(np.fft.ifft2(np.fft.fft2(X) * (0.5 * k2)[None]))
+    Y = ctx.fourier_apply(T(X.reshape(3, -1)), 0).cpu().numpy().reshape(3, n0, n1)
+    assert rel(Y, ref) < 1e-12
+    ctx.close()
 
 
 def test_gemms(sysx):

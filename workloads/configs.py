@@ -114,6 +114,17 @@ def get_config(name_or_index) -> SystemConfig:
     return CONFIGS[name_or_index]
 
 
+def small_config_2d(name: str = "tiny2d", **overrides) -> SystemConfig:
+    """A cheap GAPPED 2D test system (configs[3]'s shape: square lattice, Z=2, f=2, x and y
+    perturbations).  eps0 = 0.3 instead of the configs' 10: at eps0 = 10 the 2x2 lattice is
+    (nearly) metallic -- HOMO-LUMO gap ~5e-4, the SCF oscillates between degenerate
+    occupations -- while here the gap is 0.083."""
+    base = dict(name=name, dim=2, n_side=2, spacing=6.0, Z=2.0, sigma=1.2, kappa=0.01, eps0=0.3,
+                grid=(32, 32), n_occ=4, occ=2.0, n_cheb=4, jitter=0.15, seed=9, sketch_r=16, n_outer=2)
+    base.update(overrides)
+    return SystemConfig(**base)
+
+
 def small_config(name: str = "tiny4", **overrides) -> SystemConfig:
     """A cheap test system (shape of configs[0], fewer atoms/points)."""
     base = dict(name=name, dim=1, n_side=4, spacing=6.0, Z=2.0, sigma=1.2,
