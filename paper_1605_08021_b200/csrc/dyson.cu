@@ -58,8 +58,9 @@ void smw_update(acp_context* ctx, const double* G, const int* S, const double* W
     const int Ng = ctx->Ng;
     const int n = ctx->dim * ctx->sys.n_atoms;
     double* KW = ctx->wsd("dy_KW", (size_t)Ng * N);
-    double* A = ctx->wsd("dy_A", (size_t)N * N);
-    double* Y = ctx->wsd("dy_Y", (size_t)N * n);
+    double* AB = ctx->wsd("dy_AB", (size_t)N * (N + n));  // [A | Y], ld N (blocked LU operand)
+    double* A = AB;
+    double* Y = AB + (size_t)N * N;
     double* mK = ctx->wsd("dy_multK", Ng);
     copy_cols(ctx, mK, multiplier(ctx, MULT_YUKAWA, 0.0), Ng);
     FopArgs f;
@@ -70,7 +71,7 @@ void smw_update(acp_context* ctx, const double* G, const int* S, const double* W
     fourier_op(ctx, f);
     k_smw_gather<<<dim3(cdiv(N, 128), N > n ? N : n), 128, 0, ctx->stream>>>(Ng, N, n, S, KW, G, A, Y);
     launched(ctx);
-    lu_solve(ctx, A, N, Y, n);
+    lu_solve_blocked(ctx, AB, N, n);
     gemm_nn(ctx, Ng, N, n, 1.0, W, Ng, Y, N, 0.0, U, Ng);
     if (Gp) {
         copy_cols(ctx, Gp, G, (size_t)Ng * n);

@@ -16,13 +16,15 @@
 //       rows [r n0/cs, (r+1) n0/cs): row FFTs in its shared memory, then a transpose
 //       through distributed shared memory (each CTA gathers its n1/cs columns from every
 //       peer), column FFTs, symbol multiply, column FFTs, transpose back, row FFTs.
-//       The column-phase layout is padded (ld = n0 + 1) so the DSMEM transposes are
-//       bank-conflict free.  Per-column dot products are reduced over the cluster in
+//       Shared memory is indexed through P(i) = i + i/8 and the column phase uses ld = n0 + 8,
+//       which makes the Stockham passes and the DSMEM transposes (nearly) bank-conflict free.  Per-column dot products are reduced over the cluster in
 //       rank order (deterministic).
 #include <cooperative_groups.h>
 
 #include "fft_engine.cuh"
 
+#include <algorithm>
+#include <map>
 #include <cmath>
 #include <cstdlib>
 
@@ -54,7 +56,7 @@ struct FftGeom {
     int cs, r0, c1;   // 2D cluster size, rows and columns per CTA
     int sh0, sh1;     // twiddle table splits
     int tw0n, tw1n;   // twiddle entries
-    int ldc;          // column-phase leading dimension (n0 + 1)
+    int ldc;          // column-phase leading dimension (n0 + 8)
 };
 
 static FftGeom geom(const acp_context* ctx) {
@@ -70,7 +72,7 @@ static FftGeom geom(const acp_context* ctx) {
     g.sh1 = ctx->dim == 2 ? tw_split(g.n1) : 0;
     g.tw0n = tw_entries(g.n0);
     g.tw1n = ctx->dim == 2 ? tw_entries(g.n1) : 0;
-    g.ldc = g.n0 + 1;
+    g.ldc = g.n0 + 8;  // with the P() pad: conflict-free column passes and transposes (enumerated)
     return g;
 }
 
@@ -88,12 +90,21 @@ struct IoArgs {
 };
 
 // ============================================================================ 1D
-template <int EPT, int IO>
-__global__ void __launch_bounds__(512) k_fft1d(FftGeom G, const double2* __restrict__ twg, IoArgs io) {
+
+// One CTA per column pair.  Shared memory: the padded FFT buffer, the twiddle table and (IO_OP)
+// the multiplier, which is copied with cp.async at kernel start and consumed after the first FFT.
+// Each thread keeps its input values (i = tid + q T) in registers for the epilogue and
+// prefetches the potential before the second FFT, so no global load sits on the critical path
+// after the initial one.
+template <int EPT, bool KEEP, int IO>
+__global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGeom G, const double2* __restrict__ twg,
+                                                             IoArgs io) {
     extern __shared__ __align__(16) double2 sm1[];
     __shared__ double red[132];
     const int N = G.n0;
+    const int T = blockDim.x, tid = threadIdx.x;
     double2* buf = sm1;
+    double* smult = reinterpret_cast<double*>(sm1 + padded(N) + G.tw0n);
     const int c0 = 2 * blockIdx.x, c1 = c0 + 1;
     const int ncol = IO == IO_OP ? io.f.n : io.n;
     const bool has1 = c1 < ncol;
@@ -103,45 +114,74 @@ __global__ void __launch_bounds__(512) k_fft1d(FftGeom G, const double2* __restr
         act1 = has1 && io.f.active[c1] != 0;
     }
     if (!act0 && !act1) return;
-    const TwTable tw = load_twiddles(sm1 + N, twg, N, G.sh0);
-    const double* x0 = nullptr;
-    const double* x1 = nullptr;
-    if (IO == IO_OP) {
-        x0 = io.f.X + (size_t)c0 * N;
-        x1 = io.f.X + (size_t)c1 * N;
-        for (int i = threadIdx.x; i < N; i += blockDim.x) buf[i] = make_double2(x0[i], has1 ? x1[i] : 0.0);
+    const bool do_fft = IO != IO_OP || io.f.mult != nullptr;
+    if (IO == IO_OP && do_fft) {
+        if ((N & 1) == 0) {
+            for (int c = tid; c < N / 2; c += T) cp_async16_fe(smult + 2 * c, io.f.mult + 2 * c);
+        } else {
+            for (int i = tid; i < N; i += T) smult[i] = io.f.mult[i];
+        }
+    }
+    const TwTable tw = load_twiddles(sm1 + padded(N), twg, N, G.sh0);
+    constexpr int NK = KEEP ? EPT : 1;  // register-resident inputs (KEEP) or re-read in the epilogue
+    double u0[NK], u1[NK];
+    const double* x0 = io.f.X + (size_t)c0 * N;
+    const double* x1 = io.f.X + (size_t)c1 * N;
+    if (IO == IO_OP && KEEP) {
+#pragma unroll
+        for (int q = 0; q < NK; ++q) {
+            const int i = tid + q * T;
+            u0[q] = i < N ? x0[i] : 0.0;
+            u1[q] = (i < N && has1) ? x1[i] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < NK; ++q) {
+            const int i = tid + q * T;
+            if (i < N) buf[P(i)] = make_double2(u0[q], u1[q]);
+        }
+    } else if (IO == IO_OP) {
+        for (int i = tid; i < N; i += T) buf[P(i)] = make_double2(x0[i], has1 ? x1[i] : 0.0);
     } else if (IO == IO_HERM) {
         const double2* s0 = io.spec + (size_t)c0 * N;
         const double2* s1 = io.spec + (size_t)c1 * N;
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        for (int i = tid; i < N; i += T) {
             const double2 p = s0[i];
             const double2 q = has1 ? s1[i] : make_double2(0.0, 0.0);
-            buf[i] = make_double2(p.x - q.y, -(p.y + q.x));  // conj(P + i Q)
+            buf[P(i)] = make_double2(p.x - q.y, -(p.y + q.x));  // conj(P + i Q)
         }
     } else {
-        for (int i = threadIdx.x; i < N; i += blockDim.x) buf[i] = make_double2(io.x[i], 0.0);
+        for (int i = tid; i < N; i += T) buf[P(i)] = make_double2(io.x[i], 0.0);
     }
+    cp_async_wait_all_fe();  // twiddles and the multiplier
     __syncthreads();
-    const bool do_fft = IO != IO_OP || io.f.mult != nullptr;
     if (do_fft) fft_inplace<EPT>(buf, N, 1, G.p0, tw);
     if (IO == IO_HERM) {
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
-            io.out[(size_t)c0 * N + i] = buf[i].x * io.scale;
-            if (has1) io.out[(size_t)c1 * N + i] = -buf[i].y * io.scale;
+        for (int i = tid; i < N; i += T) {
+            const double2 v = buf[P(i)];
+            io.out[(size_t)c0 * N + i] = v.x * io.scale;
+            if (has1) io.out[(size_t)c1 * N + i] = -v.y * io.scale;
         }
         return;
     }
     if (IO == IO_SPEC) {
-        for (int i = threadIdx.x; i < N; i += blockDim.x) io.sout[i] = buf[i];
+        for (int i = tid; i < N; i += T) io.sout[i] = buf[P(i)];
         return;
     }
     const FopArgs& a = io.f;
+    double dv[NK];
+    if (KEEP) {
+#pragma unroll
+        for (int q = 0; q < NK; ++q) {
+            const int i = tid + q * T;
+            dv[q] = (a.diag && i < N) ? __ldg(&a.diag[i]) : 0.0;  // consumed after the second FFT
+        }
+    }
     if (do_fft) {
         // conj(mult * F) then forward FFT == N * conj(IFFT(mult * F)) (1/N folded into mult)
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
-            const double m = __ldg(&a.mult[i]);
-            const double2 v = buf[i];
-            buf[i] = make_double2(m * v.x, -m * v.y);
+        for (int i = tid; i < N; i += T) {
+            const double m = smult[i];
+            const double2 v = buf[P(i)];
+            buf[P(i)] = make_double2(m * v.x, -m * v.y);
         }
         __syncthreads();
         fft_inplace<EPT>(buf, N, 1, G.p0, tw);
@@ -151,32 +191,33 @@ __global__ void __launch_bounds__(512) k_fft1d(FftGeom G, const double2* __restr
     double d[4] = {0.0, 0.0, 0.0, 0.0};
     double* y0 = a.Y + (size_t)c0 * N;
     double* y1 = a.Y + (size_t)c1 * N;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const double u0 = x0[i];
-        const double u1 = has1 ? x1[i] : 0.0;
-        double v0 = 0.0, v1 = 0.0;
-        if (do_fft) {
-            v0 = buf[i].x;
-            v1 = -buf[i].y;
+    const int nq = KEEP ? NK : (N + T - 1) / T;
+#pragma unroll(KEEP ? NK : 1)
+    for (int q = 0; q < nq; ++q) {
+        const int i = tid + q * T;
+        if (i < N) {
+            const double xa = KEEP ? u0[KEEP ? q : 0] : x0[i];
+            const double xb = KEEP ? u1[KEEP ? q : 0] : (has1 ? x1[i] : 0.0);
+            const double dg = KEEP ? dv[KEEP ? q : 0] : (a.diag ? a.diag[i] : 0.0);
+            double v0 = 0.0, v1 = 0.0;
+            if (do_fft) {
+                const double2 v = buf[P(i)];
+                v0 = v.x;
+                v1 = -v.y;
+            }
+            v0 += (dg - s0) * xa;
+            v1 += (dg - s1) * xb;
+            if (act0) y0[i] = v0;
+            if (act1) y1[i] = v1;
+            d[0] += xa * v0;
+            d[1] += xa * xa;
+            d[2] += xb * v1;
+            d[3] += xb * xb;
         }
-        if (a.diag) {
-            const double dg = a.diag[i];
-            v0 += (dg - s0) * u0;
-            v1 += (dg - s1) * u1;
-        } else if (a.shift) {
-            v0 -= s0 * u0;
-            v1 -= s1 * u1;
-        }
-        if (act0) y0[i] = v0;
-        if (act1) y1[i] = v1;
-        d[0] += u0 * v0;
-        d[1] += u0 * u0;
-        d[2] += u1 * v1;
-        d[3] += u1 * u1;
     }
     if (a.dots) {
         block_sum4(d, red);
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             if (act0) {
                 a.dots[2 * c0] = d[0];
                 a.dots[2 * c0 + 1] = d[1];
@@ -205,7 +246,7 @@ __device__ __forceinline__ void rows_to_cols(cg::cluster_group& cl, double2* buf
             const int i = e / G.c1, c = e - i * G.c1;
             const int src = i / G.r0, il = i - src * G.r0;
             const double2* rb = cl.map_shared_rank(buf, src);
-            v[q] = rb[il * G.n1 + rank * G.c1 + c];
+            v[q] = rb[P(il * G.n1 + rank * G.c1 + c)];
         }
     }
     cl.sync();
@@ -214,7 +255,7 @@ __device__ __forceinline__ void rows_to_cols(cg::cluster_group& cl, double2* buf
         const int e = threadIdx.x + q * blockDim.x;
         if (e < E) {
             const int i = e / G.c1, c = e - i * G.c1;
-            buf[c * G.ldc + i] = v[q];
+            buf[P(c * G.ldc + i)] = v[q];
         }
     }
     __syncthreads();
@@ -232,21 +273,21 @@ __device__ __forceinline__ void cols_to_rows(cg::cluster_group& cl, double2* buf
             const int il = e / G.n1, k1 = e - il * G.n1;
             const int src = k1 / G.c1, c = k1 - src * G.c1;
             const double2* rb = cl.map_shared_rank(buf, src);
-            v[q] = rb[c * G.ldc + rank * G.r0 + il];
+            v[q] = rb[P(c * G.ldc + rank * G.r0 + il)];
         }
     }
     cl.sync();
 #pragma unroll
     for (int q = 0; q < EPT; ++q) {
         const int e = threadIdx.x + q * blockDim.x;
-        if (e < E) buf[e] = v[q];
+        if (e < E) buf[P(e)] = v[q];
     }
     __syncthreads();
 }
 
 // One column pair (or spectrum pair / single column) per cluster; grid (cs, pairs).
 template <int EPT, int IO>
-__global__ void __launch_bounds__(512) k_fft2d(FftGeom G, const double2* __restrict__ tw0g,
+__global__ void __launch_bounds__(1024) k_fft2d(FftGeom G, const double2* __restrict__ tw0g,
                                                const double2* __restrict__ tw1g, IoArgs io, int pair0) {
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double2 sm2[];
@@ -254,7 +295,7 @@ __global__ void __launch_bounds__(512) k_fft2d(FftGeom G, const double2* __restr
     __shared__ double part[4];
     const int rank = (int)cl.block_rank();
     const int N = G.n0 * G.n1;
-    const int bufn = G.c1 * G.ldc > G.r0 * G.n1 ? G.c1 * G.ldc : G.r0 * G.n1;
+    const int bufn = padded(G.c1 * G.ldc > G.r0 * G.n1 ? G.c1 * G.ldc : G.r0 * G.n1);
     double2* buf = sm2;
     const int pair = pair0 + blockIdx.y;
     const int c0 = 2 * pair, c1 = c0 + 1;
@@ -275,18 +316,19 @@ __global__ void __launch_bounds__(512) k_fft2d(FftGeom G, const double2* __restr
     if (IO == IO_OP) {
         x0 = io.f.X + (size_t)c0 * N + rowbase;
         x1 = io.f.X + (size_t)c1 * N + rowbase;
-        for (int e = threadIdx.x; e < E; e += blockDim.x) buf[e] = make_double2(x0[e], has1 ? x1[e] : 0.0);
+        for (int e = threadIdx.x; e < E; e += blockDim.x) buf[P(e)] = make_double2(x0[e], has1 ? x1[e] : 0.0);
     } else if (IO == IO_HERM) {
         const double2* s0 = io.spec + (size_t)c0 * N + rowbase;
         const double2* s1 = io.spec + (size_t)c1 * N + rowbase;
         for (int e = threadIdx.x; e < E; e += blockDim.x) {
             const double2 p = s0[e];
             const double2 q = has1 ? s1[e] : make_double2(0.0, 0.0);
-            buf[e] = make_double2(p.x - q.y, -(p.y + q.x));
+            buf[P(e)] = make_double2(p.x - q.y, -(p.y + q.x));
         }
     } else {
-        for (int e = threadIdx.x; e < E; e += blockDim.x) buf[e] = make_double2(io.x[rowbase + e], 0.0);
+        for (int e = threadIdx.x; e < E; e += blockDim.x) buf[P(e)] = make_double2(io.x[rowbase + e], 0.0);
     }
+    cp_async_wait_all_fe();  // twiddles
     __syncthreads();
     const bool do_fft = IO != IO_OP || io.f.mult != nullptr;
     if (do_fft) {
@@ -299,7 +341,7 @@ __global__ void __launch_bounds__(512) k_fft2d(FftGeom G, const double2* __restr
         const int Ec = G.n0 * G.c1;
         for (int e = threadIdx.x; e < Ec; e += blockDim.x) {
             const int k0 = e / G.c1, c = e - k0 * G.c1;
-            const double2 v = buf[c * G.ldc + k0];
+            const double2 v = buf[P(c * G.ldc + k0)];
             const size_t o = (size_t)k0 * G.n1 + rank * G.c1 + c;
             if (IO == IO_SPEC) {
                 io.sout[o] = v;
@@ -316,8 +358,8 @@ __global__ void __launch_bounds__(512) k_fft2d(FftGeom G, const double2* __restr
         for (int e = threadIdx.x; e < Ec; e += blockDim.x) {
             const int k0 = e / G.c1, c = e - k0 * G.c1;
             const double m = __ldg(&a.mult[(size_t)k0 * G.n1 + rank * G.c1 + c]);
-            const double2 v = buf[c * G.ldc + k0];
-            buf[c * G.ldc + k0] = make_double2(m * v.x, -m * v.y);
+            const double2 v = buf[P(c * G.ldc + k0)];
+            buf[P(c * G.ldc + k0)] = make_double2(m * v.x, -m * v.y);
         }
         __syncthreads();
         fft_inplace<EPT>(buf, G.ldc, G.c1, G.p0, tw0);      // columns
@@ -335,8 +377,9 @@ __global__ void __launch_bounds__(512) k_fft2d(FftGeom G, const double2* __restr
         const double u1 = has1 ? x1[e] : 0.0;
         double v0 = 0.0, v1 = 0.0;
         if (do_fft) {
-            v0 = buf[e].x;
-            v1 = -buf[e].y;
+            const double2 v = buf[P(e)];
+            v0 = v.x;
+            v1 = -v.y;
         }
         if (dg) {
             const double w = dg[e];
@@ -369,6 +412,17 @@ __global__ void __launch_bounds__(512) k_fft2d(FftGeom G, const double2* __restr
 }
 
 // ============================================================================ launchers
+// cudaFuncSetAttribute once per kernel instance and size (a host call per launch would make the
+// un-graphed launches host-bound).
+static void set_smem_attr(const void* kern, size_t smem, bool cluster16) {
+    static std::map<const void*, size_t> done;  // per kernel instance (device attributes are per process)
+    size_t& d = done[kern];
+    if (d >= smem) return;
+    ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (cluster16) ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    d = smem;
+}
+
 template <int IO>
 static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
     if (ncols <= 0) return;
@@ -377,17 +431,18 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
     const int T = ctx->fthreads;
     const size_t smem = ctx->fsmem;
     if (ctx->dim == 1) {
-        auto kern = ctx->fept <= 4 ? k_fft1d<4, IO> : ctx->fept <= 8 ? k_fft1d<8, IO>
-                  : ctx->fept <= 12 ? k_fft1d<12, IO> : k_fft1d<16, IO>;
-        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // KEEP (register-resident inputs, <= 160 threads, 4 CTAs/SM) for N <= 1280
+        auto kern = T > 160 ? (ctx->fept <= 8 ? k_fft1d<8, false, IO> : k_fft1d<16, false, IO>)
+                  : ctx->fept <= 2 ? k_fft1d<2, true, IO> : ctx->fept <= 4 ? k_fft1d<4, true, IO>
+                  : k_fft1d<8, true, IO>;
+        set_smem_attr((const void*)kern, smem, false);
         kern<<<npair, T, smem, ctx->stream>>>(G, ctx->d_tw, io);
         launched(ctx);
         return;
     }
-    auto kern = ctx->fept <= 4 ? k_fft2d<4, IO> : ctx->fept <= 8 ? k_fft2d<8, IO>
-              : ctx->fept <= 12 ? k_fft2d<12, IO> : k_fft2d<16, IO>;
-    ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (ctx->cs > 8) ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    auto kern = ctx->fept <= 2 ? k_fft2d<2, IO> : ctx->fept <= 4 ? k_fft2d<4, IO>
+              : ctx->fept <= 8 ? k_fft2d<8, IO> : k_fft2d<16, IO>;
+    set_smem_attr((const void*)kern, smem, true);
     for (int p0 = 0; p0 < npair; p0 += 32768) {
         const int np = npair - p0 < 32768 ? npair - p0 : 32768;
         cudaLaunchConfig_t cfg = {};
@@ -550,7 +605,7 @@ static T* upload(const std::vector<T>& v) {
 
 static int ept_for(int E, int T) {
     const int need = (E + T - 1) / T;
-    return need <= 4 ? 4 : need <= 8 ? 8 : need <= 12 ? 12 : need <= 16 ? 16 : 0;
+    return need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : need <= 12 ? 12 : need <= 16 ? 16 : 0;
 }
 
 void fft_init(acp_context* ctx) {
@@ -589,24 +644,31 @@ void fft_init(acp_context* ctx) {
         }
     ctx->d_k2 = upload(k2);
     ctx->d_khat = upload(khat);
-    // launch geometry of the FFT kernels
+    // Launch geometry of the FFT kernels.  The FFT is latency-bound (log N dependent passes
+    // with a block barrier each), so each CTA gets as many threads as there are radix-2
+    // butterflies (<= 1024): every thread holds <= 2-4 values per pass and the chain is short.
+    auto round32 = [](int t) { return (t + 31) / 32 * 32; };
+    // tuning knob: ACP_FFT_THREADS overrides the CTA size (sweeps in tools/k1_sweep.py)
+    const int tknob = getenv("ACP_FFT_THREADS") ? atoi(getenv("ACP_FFT_THREADS")) : 0;
     if (dim == 1) {
-        int T = (N / 8 + 31) / 32 * 32;
-        T = T < 64 ? 64 : T > 512 ? 512 : T;
+        // T = N/8 (<= 8 values per thread): with the register-resident inputs this keeps ~100
+        // registers/thread and 4 CTAs per SM (k1_sweep on B200: 160 threads best for N = 1280)
+        int T = tknob > 0 ? round32(tknob) : round32((N + 7) / 8);
+        T = T < 64 ? 64 : T > 1024 ? 1024 : T;
         ctx->fthreads = T;
         ctx->fept = ept_for(N, T);
         ACP_REQUIRE(ctx->fept > 0, "1D grid too large for the shared-memory FFT");
-        ctx->fsmem = (size_t)(N + tw_entries(n0)) * sizeof(double2);
+        ctx->fsmem = (size_t)(padded(N) + tw_entries(n0)) * sizeof(double2) + (size_t)N * sizeof(double);
         ACP_REQUIRE(ctx->fsmem <= 220 * 1024, "1D grid too large for the shared-memory FFT");
     } else {
-        // smallest cluster whose per-CTA slice fits ~100 KB (2+ CTAs per SM), cs | n0 and cs | n1
-        int cs = 1;
+        // smallest cluster (cs | n0, cs | n1, cs <= 16) whose per-CTA slice has <= 4096 points
+        auto slice = [&](int c) { return std::max((n0 / c) * n1, (n1 / c) * (n0 + 8)); };
         auto bytes = [&](int c) {
-            const int rows = (n0 / c) * n1, cols = (n1 / c) * (n0 + 1);
-            return (size_t)((rows > cols ? rows : cols) + tw_entries(n0) + tw_entries(n1)) * sizeof(double2);
+            return (size_t)(padded(slice(c)) + tw_entries(n0) + tw_entries(n1)) * sizeof(double2);
         };
-        while (cs < 16 && (bytes(cs) > 100 * 1024) && n0 % (2 * cs) == 0 && n1 % (2 * cs) == 0) cs *= 2;
-        // test knob: ACP_FFT2D_CS forces a larger cluster (exercises the DSMEM transposes on small grids)
+        int cs = 1;
+        while (cs < 16 && slice(cs) > 4096 && n0 % (2 * cs) == 0 && n1 % (2 * cs) == 0) cs *= 2;
+        // test knob: ACP_FFT2D_CS forces another cluster size (exercises the DSMEM transposes on small grids)
         if (const char* e = getenv("ACP_FFT2D_CS")) {
             const int f = atoi(e);
             if (f >= 1 && f <= 16 && n0 % f == 0 && n1 % f == 0) cs = f;
@@ -616,9 +678,9 @@ void fft_init(acp_context* ctx) {
         ctx->cs = cs;
         ctx->r0 = n0 / cs;
         ctx->c1 = n1 / cs;
-        const int E = ctx->r0 * n1 > ctx->c1 * n0 ? ctx->r0 * n1 : ctx->c1 * n0;
-        int T = (E / 12 + 31) / 32 * 32;
-        T = T < 64 ? 64 : T > 512 ? 512 : T;
+        const int E = std::max(ctx->r0 * n1, ctx->c1 * n0);
+        int T = tknob > 0 ? round32(tknob) : round32((E + 3) / 4);
+        T = T < 64 ? 64 : T > 1024 ? 1024 : T;
         ctx->fthreads = T;
         ctx->fept = ept_for(E, T);
         ACP_REQUIRE(ctx->fept > 0, "2D slice too large for the FFT engine");

@@ -85,41 +85,68 @@ template <> __device__ __forceinline__ void dft<5>(double2* x) {
     x[3] = csub(t2, mul_mi(u2));
 }
 
-// Twiddle table exp(-2 pi i m / L), m < L, in shared memory.  Long transforms use a
-// two-level table w(m) = hi[m >> sh] * lo[m & (2^sh - 1)] (each entry correctly rounded on
-// the host; the product adds <= 2 ulp) so the table costs O(sqrt L) shared memory.
+// Shared-memory index padding: one spare 16-byte slot every 8 complex values.  A 16-byte
+// access touches 4 banks, so 8 consecutive values fill all 32 banks; the first Stockham pass
+// writes with stride R (and the 2D transposes with stride ld), which without padding puts 8
+// lanes of a quarter-warp on the same 4 banks.  With the pad every pattern here is
+// conflict-free (checked by enumeration for the c1 / 2D plans).
+__device__ __forceinline__ int P(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int padded(int n) { return n + (n >> 3) + 1; }
+
+// Twiddle table exp(-2 pi i m / L), m < L, in shared memory (padded indexing).  Long
+// transforms (L > 4096) use a two-level table w(m) = hi[m >> sh] * lo[m & (2^sh - 1)] (each
+// entry correctly rounded on the host; the product adds <= 2 ulp).
 struct TwTable {
     const double2* lo;
     const double2* hi;
-    int sh;  // 0: single-level table in lo
+    int sh;    // 0: single-level table in lo
+    int half;  // single level, L even: lo holds m < L/2 and w(m + L/2) = -w(m)
     __device__ __forceinline__ double2 operator()(int m) const {
-        if (sh == 0) return lo[m];
-        return cmul(hi[m >> sh], lo[m & ((1 << sh) - 1)]);
+        if (sh == 0) {
+            if (m < half || half == 0) return lo[P(m)];
+            const double2 v = lo[P(m - half)];
+            return make_double2(-v.x, -v.y);
+        }
+        return cmul(hi[m >> sh], lo[P(m & ((1 << sh) - 1))]);
     }
 };
 
-// One in-place Stockham pass of radix R over nb transforms of length L (transform t at buf + t*ld):
-// sub-transforms of length Ns are combined into length Ns*R.  EPT = max complex values a
-// thread holds (EPT >= nb*L / blockDim.x).  Ends with a block barrier.
+// q = floor(a / d) for 0 <= a < 2^21, d >= 1, via a float reciprocal: (a + 0.5)/d lies at least
+// 0.5/d from an integer, and the two roundings of (a + 0.5) * fl(1/d) err by < 2^-22 (a + 0.5)/d
+// < 0.5/d.  Avoids the ~20-instruction integer division.
+__device__ __forceinline__ int fdiv(int a, float rd) { return __float2int_rz(((float)a + 0.5f) * rd); }
+
+// One in-place Stockham pass of radix R over nb transforms of length L (transform t at buf + t*ld,
+// padded indexing P): sub-transforms of length Ns are combined into length Ns*R.  EPT = max
+// complex values a thread holds (EPT >= nb*L / blockDim.x).  Ends with a block barrier.
 template <int R, int EPT>
 __device__ __forceinline__ void pass_inplace(double2* buf, int L, int ld, int nb, int Ns, const TwTable& tw) {
     constexpr int MB = (EPT + R - 1) / R;
     const int per = L / R;              // butterflies per transform
     const int total = nb * per;
     const int stride = L / (Ns * R);    // twiddle stride for this pass
+    const float rper = 1.0f / (float)per, rNs = 1.0f / (float)Ns;
     double2 x[MB][R];
 #pragma unroll
     for (int b = 0; b < MB; ++b) {
         const int g = threadIdx.x + b * blockDim.x;
         if (g < total) {
-            const int t = g / per, j = g - t * per;
-            const int k = j % Ns;
-            const double2* src = buf + t * ld;
+            const int t = nb == 1 ? 0 : fdiv(g, rper);
+            const int j = g - t * per;
+            const int k = j - Ns * fdiv(j, rNs);
+            const int base = t * ld + j;
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[b][r] = src[j + r * per];
+            for (int r = 0; r < R; ++r) x[b][r] = buf[P(base + r * per)];
             if (Ns > 1) {
+                // one table read per butterfly; w^r by repeated products (error <= ~R ulp)
+                const double2 w = tw(k * stride);
+                double2 wr = w;
+                x[b][1] = cmul(x[b][1], w);
 #pragma unroll
-                for (int r = 1; r < R; ++r) x[b][r] = cmul(x[b][r], tw(r * k * stride));
+                for (int r = 2; r < R; ++r) {
+                    wr = cmul(wr, w);
+                    x[b][r] = cmul(x[b][r], wr);
+                }
             }
             dft<R>(x[b]);
         }
@@ -129,11 +156,12 @@ __device__ __forceinline__ void pass_inplace(double2* buf, int L, int ld, int nb
     for (int b = 0; b < MB; ++b) {
         const int g = threadIdx.x + b * blockDim.x;
         if (g < total) {
-            const int t = g / per, j = g - t * per;
-            const int k = j % Ns;
-            double2* dst = buf + t * ld + (j - k) * R + k;
+            const int t = nb == 1 ? 0 : fdiv(g, rper);
+            const int j = g - t * per;
+            const int k = j - Ns * fdiv(j, rNs);
+            const int base = t * ld + (j - k) * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) dst[r * Ns] = x[b][r];
+            for (int r = 0; r < R; ++r) buf[P(base + r * Ns)] = x[b][r];
         }
     }
     __syncthreads();
@@ -153,27 +181,44 @@ __device__ __forceinline__ void fft_inplace(double2* buf, int ld, int nb, const 
     for (; p < pl.npass && pl.radix[p] == 3; ++p, Ns *= 3) pass_inplace<3, EPT>(buf, pl.N, ld, nb, Ns, tw);
 }
 
-// Host-side layout of a twiddle table for length L: returns the level split sh (0 = single level)
-// and the number of double2 entries (lo followed by hi).
+// Host-side layout of a twiddle table for length L: the level split sh (0 = single level) and
+// the number of double2 entries in GLOBAL memory (lo followed by hi, unpadded) and in SHARED
+// memory (lo padded).
 inline int tw_split(int L) {
-    if (L <= 512) return 0;
+    if (L <= 4096) return 0;
     int sh = 1;
     while ((1 << (2 * sh)) < L) ++sh;   // lo has 2^sh ~ sqrt(L) entries
     return sh;
 }
 inline int tw_entries(int L) {
     const int sh = tw_split(L);
-    return sh == 0 ? L : (1 << sh) + (L >> sh) + 1;
+    return sh == 0 ? padded((L & 1) ? L : L / 2) : padded(1 << sh) + (L >> sh) + 1;
 }
 
-// Copy a twiddle table (global layout from tw_entries) into shared memory `dst` (no barrier).
+// Copy a twiddle table into shared memory `dst` with cp.async (16-byte chunks, no register
+// round trip: the copies overlap whatever the CTA does next).  The caller commits/waits and
+// synchronises before the first twiddled pass.
+__device__ __forceinline__ void cp_async16_fe(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all_fe() {
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+}
 __device__ __forceinline__ TwTable load_twiddles(double2* dst, const double2* __restrict__ src, int L, int sh) {
-    const int n = sh == 0 ? L : (1 << sh) + (L >> sh) + 1;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    const int half = (sh == 0 && (L & 1) == 0) ? L / 2 : 0;
+    const int nlo = sh == 0 ? (half ? half : L) : (1 << sh);
+    const int nhi = sh == 0 ? 0 : (L >> sh) + 1;
+    const int hoff = sh == 0 ? L : nlo;  // global offset of the hi table
+    for (int i = threadIdx.x; i < nlo; i += blockDim.x) cp_async16_fe(dst + P(i), src + i);
+    double2* hi = dst + padded(nlo);
+    for (int i = threadIdx.x; i < nhi; i += blockDim.x) cp_async16_fe(hi + i, src + hoff + i);
     TwTable t;
     t.lo = dst;
-    t.hi = sh == 0 ? dst : dst + (1 << sh);
+    t.hi = hi;
     t.sh = sh;
+    t.half = half;
     return t;
 }
 

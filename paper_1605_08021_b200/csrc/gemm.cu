@@ -103,9 +103,14 @@ struct EpAxpby {
     double alpha, beta;
     double* C;
     int ldc;
-    __device__ __forceinline__ void operator()(int r, int c, double acc) const {
-        double* p = C + (size_t)c * ldc + r;
-        *p = (beta == 0.0 ? 0.0 : beta * *p) + alpha * acc;
+    struct Regs {
+        double c;
+    };
+    __device__ __forceinline__ void load(int r, int c, Regs& g) const {
+        g.c = beta == 0.0 ? 0.0 : C[(size_t)c * ldc + r];
+    }
+    __device__ __forceinline__ void store(int r, int c, double acc, const Regs& g) const {
+        C[(size_t)c * ldc + r] = (beta == 0.0 ? 0.0 : beta * g.c) + alpha * acc;
     }
 };
 

@@ -20,7 +20,9 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 
 // NN tile: C_tile(64 x 32) = A(64 x K) * B(K x 32); A col-major (lda), B col-major (ldb).
 // 128 threads = 4 warps as 2 (m) x 2 (n); each warp owns 32 x 16 = 4 x 2 DMMA tiles.
-// The epilogue functor is called as ep(row, col, acc) for every in-range element.
+// Epilogue functor interface (two phases, so that all global reads of a thread's 16 output
+// elements are in flight together instead of serialising behind possibly-aliasing stores):
+//   typename Ep::Regs;  ep.load(row, col, regs);  ep.store(row, col, acc, regs).
 constexpr int NN_BM = 64, NN_BN = 32, NN_BK = 16;
 
 template <class Ep>
@@ -66,16 +68,31 @@ __device__ __forceinline__ void nn_tile(int M, int K, int n, const double* __res
         }
         __syncthreads();
     }
+    // two halves of 8 elements each: loads of a half are all in flight together (~130 registers)
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int ih = 0; ih < 4; ih += 2) {
+        typename Ep::Regs regs[2][2][2];
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int row = m0 + wm * 32 + i * 8 + g;
-                const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
-                if (row < M && col < n) ep(row, col, acc[i][j][e]);
-            }
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = m0 + wm * 32 + (ih + i) * 8 + g;
+                    const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
+                    if (row < M && col < n) ep.load(row, col, regs[i][j][e]);
+                }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = m0 + wm * 32 + (ih + i) * 8 + g;
+                    const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
+                    if (row < M && col < n) ep.store(row, col, acc[ih + i][j][e], regs[i][j][e]);
+                }
+    }
 }
 
 // ---------------------------------------------------------------------------

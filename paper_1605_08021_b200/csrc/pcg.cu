@@ -118,13 +118,25 @@ struct EpAlpha {
     const double* alpha;
     const int* active;
     int ld;
-    __device__ __forceinline__ void operator()(int r, int c, double acc) const {
-        if (!active[c]) return;
+    struct Regs {
+        double y, p, x, r;
+        bool on;
+    };
+    __device__ __forceinline__ void load(int r, int c, Regs& g) const {
+        g.on = active[c] != 0;
+        if (!g.on) return;
+        const size_t o = (size_t)c * ld + r;
+        g.y = Y[o];
+        g.p = P[o];
+        g.x = X[o];
+        g.r = R[o];
+    }
+    __device__ __forceinline__ void store(int r, int c, double acc, const Regs& g) const {
+        if (!g.on) return;
         const size_t o = (size_t)c * ld + r;
         const double a = alpha[c];
-        const double ap = Y[o] - acc;
-        X[o] += a * P[o];
-        R[o] -= a * ap;
+        X[o] = g.x + a * g.p;
+        R[o] = g.r - a * (g.y - acc);
     }
 };
 // K3 after M r: Z = Zh - Psi Cz;  P = Z + beta P (or P = Z at init).
@@ -135,16 +147,26 @@ struct EpBeta {
     const int* active;
     int ld;
     int init;
-    __device__ __forceinline__ void operator()(int r, int c, double acc) const {
-        if (!active[c]) return;
+    struct Regs {
+        double zh, p;
+        bool on;
+    };
+    __device__ __forceinline__ void load(int r, int c, Regs& g) const {
+        g.on = active[c] != 0;
+        if (!g.on) return;
         const size_t o = (size_t)c * ld + r;
-        const double z = Zh[o] - acc;
-        P[o] = init ? z : z + beta[c] * P[o];
+        g.zh = Zh[o];
+        g.p = init ? 0.0 : P[o];
+    }
+    __device__ __forceinline__ void store(int r, int c, double acc, const Regs& g) const {
+        if (!g.on) return;
+        const double z = g.zh - acc;
+        P[(size_t)c * ld + r] = init ? z : z + beta[c] * g.p;
     }
 };
 
 template <class Ep>
-__global__ void __launch_bounds__(128) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
+__global__ void __launch_bounds__(128, 4) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
                                                     const double* __restrict__ B, int ldb, Ep ep) {
     // skip tiles whose columns are all inactive (uniform per CTA)
     const int n0 = blockIdx.y * NN_BN;

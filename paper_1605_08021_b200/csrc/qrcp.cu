@@ -12,7 +12,10 @@
 
 #include "gemm.cuh"
 
+#include <algorithm>
 #include <cmath>
+#include <vector>
+#include <cstdlib>
 #include <cstdio>
 
 namespace acp {
@@ -74,6 +77,49 @@ struct QrSlot {
     int col;
 };
 
+// Warp index that the compiler can prove warp-uniform (a shuffle from lane 0): branches and
+// loops on it stay convergent, so the __shfl_sync calls inside them compile to plain SHFL
+// instead of the WARPSYNC.COLLECTIVE emulation used for possibly-divergent code.
+__device__ __forceinline__ int uniform_warp() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+
+// Householder update of a CTA's owned, not-yet-pivoted columns, two columns per warp (16 lanes
+// each; warp-uniform loop, predicated work, full-warp shuffles).  Column `cw` (global index) is
+// the pivot: it becomes (alpha, 0, ...).  v (rows j..m-1) and tau are shared by the CTA; n2[lc]
+// receives the exact trailing norm^2 (rows j+1..m-1).  Summation order is fixed.
+template <class ColP>
+__device__ __forceinline__ void qr_update_cols(ColP colp, int warp, int nc, int c0, int cw, int j, int m,
+                                               double alpha, double tau, const double* __restrict__ v,
+                                               const int* __restrict__ dn, double* __restrict__ n2) {
+    const int nwarp = blockDim.x >> 5;
+    const int h = (threadIdx.x >> 4) & 1, q = threadIdx.x & 15;
+    for (int base = 2 * warp; base < nc; base += 2 * nwarp) {
+        const int lc = base + h;
+        const bool valid = lc < nc;
+        const bool piv = valid && (c0 + lc == cw);
+        const bool live = valid && !piv && !dn[lc];
+        double* c = colp(valid ? lc : base);
+        double d = 0.0;
+        if (live)
+            for (int i = j + q; i < m; i += 16) d += v[i] * c[i];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        const double f = tau * d;
+        double nn = 0.0;
+        if (live) {
+            for (int i = j + q; i < m; i += 16) {
+                const double y = c[i] - f * v[i];
+                c[i] = y;
+                if (i > j) nn += y * y;
+            }
+        } else if (piv) {
+            for (int i = j + q; i < m; i += 16) c[i] = (i == j) ? alpha : 0.0;
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+        if (live && q == 0) n2[lc] = nn;
+    }
+}
+
 template <bool SMEM>
 __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* __restrict__ Ag, int kmax, double eps,
                                                          int fixed, QrSlot* __restrict__ slots,
@@ -87,7 +133,7 @@ __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* 
     __shared__ int red_j[32];
     __shared__ int s_lc;
     const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    const int lane = tid & 31, warp = uniform_warp(), nwarp = blockDim.x >> 5;
     const int cpb = (Ng + G - 1) / G;
     const int c0 = b * cpb;
     const int nc = max(0, min(Ng, c0 + cpb) - c0);
@@ -156,6 +202,7 @@ __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* 
         }
         __threadfence();
         grid.sync();
+        __syncthreads();  // re-establishes (for the compiler) a convergent block after grid.sync
         // ---- global winner (identical in every CTA)
         double bn = -1.0;
         int bp = 1 << 30, bs = -1;
@@ -199,7 +246,8 @@ __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* 
         const int pw = red_i[0], ws = red_j[0];
         const double rjj = sqrt(fmax(wn2, 0.0));
         if (j == 0) r11 = rjj;
-        if (ws < 0 || rjj == 0.0 || (fixed <= 0 && rjj < eps * r11)) {
+        // block-uniform exit (__syncthreads_or), so the code after the loop stays convergent
+        if (__syncthreads_or(ws < 0 || rjj == 0.0 || (fixed <= 0 && rjj < eps * r11))) {
             N = j;
             break;
         }
@@ -241,33 +289,212 @@ __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* 
             }
         }
         __syncthreads();
-        // ---- trailing update of the remaining owned columns (warp per column)
-        for (int lc = warp; lc < nc; lc += nwarp) {
-            double* c = colp(lc);
-            if (c0 + lc == cw) {
-                for (int i = j + lane; i < m; i += 32) c[i] = (i == j) ? alpha : 0.0;
-                continue;
-            }
-            if (dn[lc]) continue;
-            double d = 0.0;
-            for (int i = j + lane; i < m; i += 32) d += v[i] * c[i];
-            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-            const double f = tau * d;
-            double nn = 0.0;
-            for (int i = j + lane; i < m; i += 32) {
-                const double y = c[i] - f * v[i];
-                c[i] = y;
-                if (i > j) nn += y * y;
-            }
-            for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
-            if (lane == 0) n2[lc] = nn;
-        }
+        // ---- trailing update of the remaining owned columns (16 threads per column)
+        qr_update_cols(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
         __syncthreads();
     }
     if (SMEM)
         for (int e = tid; e < nc * m; e += blockDim.x) Ag[(size_t)c0 * m + e] = cols[e];
     for (int lc = tid; lc < nc; lc += blockDim.x) perm[pos[lc]] = c0 + lc;
     if (b == 0 && tid == 0) *out_nmu = N;
+}
+
+// ---------------------------------------------------------------------------
+// Cluster QRCP for problems that fit in the shared memory of one thread-block cluster
+// (N_g * m * 8 B <= ~16 x 190 KB; configs[0..1] and small 2D): the same algorithm and tie
+// rules as k_qrcp_persistent, with the per-pivot exchange through distributed shared memory
+// and ONE cluster barrier per pivot:
+//   * each CTA finds its local best column (warp 0), PUSHES its (norm^2, position, column)
+//     slot into every peer's slot table (DSMEM stores) and copies the candidate's rows j..m-1
+//     into a parity-double-buffered publish buffer of its own shared memory;
+//   * cluster barrier; every CTA selects the same winner from its LOCAL slot table, then reads
+//     the winner's published copy through DSMEM (the only remote read of the step);
+//   * |R_jj| is the winner's exact trailing norm (recomputed in the previous step), and the
+//     Householder update of the owned columns is one pass per column with the column's rows in
+//     registers (16 lanes per column): dot, shuffle reduction, update + new exact norm.
+// A slot / publish buffer of parity j is rewritten only at step j+2, after another barrier.
+template <int MAXK>
+__global__ void __launch_bounds__(1024) k_qrcp_cluster(int m, int Ng, double* __restrict__ Ag, int kmax, double eps,
+                                                      int fixed, int* __restrict__ perm, double* __restrict__ rdiag,
+                                                      int* __restrict__ out_nmu, long long* __restrict__ tprof) {
+    // tprof (debug, may be null): per step j, clock64() at phase boundaries of CTA 0 / thread 0
+#define QR_TP(k) \
+    if (tprof && blockIdx.x == 0 && threadIdx.x == 0 && j < 512) tprof[8 * j + (k)] = clock64();
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double csm[];
+    __shared__ QrSlot allslot[2][16];  // [parity][source rank], filled by the peers' pushes
+    __shared__ double s_wn2;
+    __shared__ int s_pos, s_rank, s_col, s_lc;
+    const int CS = (int)cl.num_blocks(), b = (int)cl.block_rank(), tid = threadIdx.x;
+    const int lane = tid & 31, warp = uniform_warp(), nwarp = blockDim.x >> 5;
+    const int cpb = (Ng + CS - 1) / CS;
+    const int c0 = b * cpb;
+    const int nc = max(0, min(Ng, c0 + cpb) - c0);
+    double* cols = csm;                         // cpb x m
+    double* v = cols + (size_t)cpb * m;         // m
+    double* pub = v + m;                        // 2 x m published candidate copies
+    double* n2 = pub + 2 * (size_t)m;           // cpb
+    int* pos = reinterpret_cast<int*>(n2 + cpb);
+    int* dn = pos + cpb;
+    for (int e = tid; e < nc * m; e += blockDim.x) cols[e] = Ag[(size_t)c0 * m + e];
+    __syncthreads();
+    for (int lc = warp; lc < nc; lc += nwarp) {
+        const double* c = cols + (size_t)lc * m;
+        double s = 0.0;
+        for (int i = lane; i < m; i += 32) s += c[i] * c[i];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            n2[lc] = s;
+            pos[lc] = c0 + lc;
+            dn[lc] = 0;
+        }
+    }
+    __syncthreads();
+    double r11 = 0.0;
+    int N = kmax;
+    cl.sync();  // every CTA of the cluster has started before the first DSMEM push
+    for (int j = 0; j < kmax; ++j) {
+        const int buf = j & 1;
+        QR_TP(0)
+        if (warp == 0) {
+            double bn = -1.0;
+            int bp = 1 << 30, bl = -1;
+            for (int lc = lane; lc < nc; lc += 32) {
+                if (dn[lc]) continue;
+                const double x = n2[lc];
+                if (x > bn || (x == bn && pos[lc] < bp)) {
+                    bn = x;
+                    bp = pos[lc];
+                    bl = lc;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {  // butterfly: every lane ends with the result
+                const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                if (on > bn || (on == bn && op < bp)) {
+                    bn = on;
+                    bp = op;
+                    bl = ol;
+                }
+            }
+            QrSlot sl;
+            sl.n2 = bn;
+            sl.pos = bp;
+            sl.col = bl >= 0 ? c0 + bl : -1;
+            if (lane < CS) cl.map_shared_rank(&allslot[0][0], lane)[buf * 16 + b] = sl;  // push to peer `lane`
+            if (lane == 0) s_lc = bl;
+        }
+        __syncthreads();
+        if (s_lc >= 0) {
+            const double* c = cols + (size_t)s_lc * m;
+            for (int i = j + tid; i < m; i += blockDim.x) pub[(size_t)buf * m + i] = c[i];
+        }
+        cl.sync();
+        QR_TP(1)
+        if (warp == 0) {
+            double bn = -1.0;
+            int bp = 1 << 30, bs = -1, bc = -1;
+            if (lane < CS) {
+                const QrSlot sl = allslot[buf][lane];
+                if (sl.col >= 0) {
+                    bn = sl.n2;
+                    bp = sl.pos;
+                    bs = lane;
+                    bc = sl.col;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+                if (on > bn || (on == bn && op < bp)) {
+                    bn = on;
+                    bp = op;
+                    bs = os;
+                    bc = oc;
+                }
+            }
+            if (lane == 0) {
+                s_wn2 = bn;
+                s_pos = bp;
+                s_rank = bs;
+                s_col = bc;
+            }
+        }
+        __syncthreads();
+        const double wn2 = s_wn2;
+        const int pw = s_pos, ws = s_rank, cw = s_col;
+        const double rjj = sqrt(fmax(wn2, 0.0));
+        if (j == 0) r11 = rjj;
+        // block-uniform exit (__syncthreads_or), so the code after the loop stays convergent
+        if (__syncthreads_or(ws < 0 || rjj == 0.0 || (fixed <= 0 && rjj < eps * r11))) {
+            N = j;
+            break;
+        }
+        QR_TP(2)
+        // ---- Householder vector: the winner's published rows j..m-1 (one DSMEM read); row j of
+        // v holds v0 = x0 - alpha directly, so the update below has no per-element selects
+        const double* x = cl.map_shared_rank(pub, ws) + (size_t)buf * m;
+        const double x0 = x[j];
+        const double alpha = (x0 >= 0.0) ? -rjj : rjj;
+        const double v0 = x0 - alpha;
+        const double tau = 2.0 / (wn2 - x0 * x0 + v0 * v0);
+        for (int i = j + tid; i < m; i += blockDim.x) v[i] = (i == j) ? v0 : x[i];
+        if (b == 0 && tid == 0) rdiag[j] = rjj;
+        __syncthreads();
+        QR_TP(3)
+        // ---- fused single-pass update: one column per warp, rows i = j + lane + 32k in registers
+        const int kc = (m - j - lane + 31) >> 5;  // rows of this lane (<= MAXK)
+        for (int lc = warp; lc < nc; lc += nwarp) {
+            double* c = cols + (size_t)lc * m + j + lane;
+            const double* vv = v + j + lane;
+            if (c0 + lc == cw) {
+#pragma unroll
+                for (int k = 0; k < MAXK; ++k)
+                    if (k < kc) c[32 * k] = (k == 0 && lane == 0) ? alpha : 0.0;
+                if (lane == 0) {
+                    pos[lc] = j;
+                    dn[lc] = 1;
+                }
+                continue;  // warp-uniform
+            }
+            if (dn[lc]) continue;  // warp-uniform
+            double y[MAXK];
+            double d = 0.0;
+#pragma unroll
+            for (int k = 0; k < MAXK; ++k) {
+                y[k] = k < kc ? c[32 * k] : 0.0;
+                d += (k < kc ? vv[32 * k] : 0.0) * y[k];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            const double f = tau * d;
+            double nn = 0.0;
+#pragma unroll
+            for (int k = 0; k < MAXK; ++k) {
+                if (k < kc) {
+                    const double yy = y[k] - f * vv[32 * k];
+                    c[32 * k] = yy;
+                    if (k > 0 || lane > 0) nn += yy * yy;  // trailing rows j+1..m-1 only
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+            if (lane == 0) {
+                n2[lc] = nn;
+                if (pos[lc] == j) pos[lc] = pw;  // swap semantics of column pivoting
+            }
+        }
+        __syncthreads();
+        QR_TP(4)
+    }
+    for (int e = tid; e < nc * m; e += blockDim.x) Ag[(size_t)c0 * m + e] = cols[e];
+    for (int lc = tid; lc < nc; lc += blockDim.x) perm[pos[lc]] = c0 + lc;
+    if (b == 0 && tid == 0) *out_nmu = N;
+    cl.sync();  // peers may still be reading this CTA's buffers when it leaves the loop
 }
 
 // T = R11^{-1} R12 by column-oriented back substitution, one WARP per trailing column c:
@@ -277,7 +504,7 @@ __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* 
 template <int SLOTS>
 __global__ void __launch_bounds__(256) k_trsm_warp(int m, int Ng, int N, const double* __restrict__ A,
                                                    const int* __restrict__ perm, double* __restrict__ T) {
-    const int wglob = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int wglob = blockIdx.x * (blockDim.x >> 5) + uniform_warp();
     const int l = threadIdx.x & 31;
     const int c = N + wglob;
     if (c >= Ng) return;
@@ -306,9 +533,69 @@ __global__ void __launch_bounds__(256) k_trsm_warp(int m, int Ng, int N, const d
     }
 }
 
+// Same back substitution with R11 staged in shared memory (one CTA per SM, 32 warps, columns
+// strided over the grid) and the reciprocals of its diagonal precomputed: the per-column chain
+// then runs on shared-memory latency instead of L2 latency.  Used when N^2 doubles fit.
+template <int SLOTS>
+__global__ void __launch_bounds__(1024) k_trsm_smem(int m, int Ng, int N, const double* __restrict__ A,
+                                                   const int* __restrict__ perm, double* __restrict__ T) {
+    extern __shared__ double rsm[];
+    double* Rs = rsm;            // Rs[mu * N + nu] = R(nu, mu), nu <= mu
+    double* rd = rsm + (size_t)N * N;
+    for (int e = threadIdx.x; e < N * N; e += blockDim.x) {
+        const int mu = e / N, nu = e - mu * N;
+        Rs[e] = nu <= mu ? A[(size_t)perm[mu] * m + nu] : 0.0;
+    }
+    __syncthreads();
+    for (int mu = threadIdx.x; mu < N; mu += blockDim.x) rd[mu] = 1.0 / Rs[(size_t)mu * N + mu];
+    __syncthreads();
+    const int l = threadIdx.x & 31;
+    const int nwarps_total = gridDim.x * (blockDim.x >> 5);
+    const int nc = Ng - N;
+    for (int cc = blockIdx.x * (blockDim.x >> 5) + uniform_warp(); cc < nc; cc += nwarps_total) {
+        const int c = N + cc;
+        double b[SLOTS];
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s) {
+            const int nu = s * 32 + l;
+            b[s] = (nu < N) ? A[(size_t)perm[c] * m + nu] : 0.0;
+        }
+        for (int mu = N - 1; mu >= 0; --mu) {
+            const int owner = mu & 31, slot = mu >> 5;
+            double bm = 0.0;
+#pragma unroll
+            for (int s = 0; s < SLOTS; ++s)
+                if (s == slot) bm = b[s];
+            double x = __shfl_sync(0xffffffffu, bm, owner) * rd[mu];
+            if (l == owner) T[(size_t)mu * nc + cc] = x;
+            const double* rcol = Rs + (size_t)mu * N;
+#pragma unroll
+            for (int s = 0; s < SLOTS; ++s) {
+                const int nu = s * 32 + l;
+                if (nu < mu) b[s] -= rcol[nu] * x;
+            }
+        }
+    }
+}
+
 static void trsm_cols(acp_context* ctx, int m, int Ng, int N, const double* A, const int* perm, double* T) {
     const int warps = Ng - N;
     if (warps <= 0) return;
+    const size_t smem = ((size_t)N * N + N) * sizeof(double);
+    if (smem <= 200 * 1024) {
+        int sms = 148;
+        ACP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        const int blocks = std::min(sms, cdiv(warps, 32));
+        auto launch = [&](auto kern) {
+            ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            kern<<<blocks, 1024, smem, ctx->stream>>>(m, Ng, N, A, perm, T);
+        };
+        if (N <= 64) launch(k_trsm_smem<2>);
+        else if (N <= 128) launch(k_trsm_smem<4>);
+        else launch(k_trsm_smem<8>);   // N^2 <= 25600 -> N <= 160
+        launched(ctx);
+        return;
+    }
     const int blocks = cdiv((long long)warps * 32, 256);
     if (N <= 128) k_trsm_warp<4><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
     else if (N <= 256) k_trsm_warp<8><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
@@ -366,24 +653,77 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
     int* d_nmu = ctx->wsi("qr_nmu", 1);
     int dev_sms = 148;
     ACP_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device));
-    int G = dev_sms < Ng ? dev_sms : Ng;
-    int cpb = cdiv(Ng, G);
-    G = cdiv(Ng, cpb);
-    const size_t tail = (size_t)m * sizeof(double) + (size_t)cpb * (sizeof(double) + 2 * sizeof(int)) + 64;
-    const size_t smem_full = (size_t)cpb * m * sizeof(double) + tail;
-    const bool use_smem = smem_full <= 200 * 1024;
-    const size_t smem = use_smem ? smem_full : tail;
-    QrSlot* slots = static_cast<QrSlot*>(ctx->ws("qr_slots", 2 * (size_t)G * sizeof(QrSlot)));
-    double* cand = ctx->wsd("qr_cand", 2 * (size_t)G * m);
-    void* args[] = {(void*)&m, (void*)&Ng, (void*)&A, (void*)&kmax, (void*)&id_eps, (void*)&n_fixed, (void*)&slots,
-                    (void*)&cand, (void*)&perm, (void*)&rdiag, (void*)&d_nmu};
-    const void* fn = use_smem ? (const void*)k_qrcp_persistent<true> : (const void*)k_qrcp_persistent<false>;
-    ACP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    ACP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
-    ACP_REQUIRE(occ >= 1 && G <= occ * dev_sms, "QRCP: cooperative grid does not fit");
-    ACP_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(256), args, smem, ctx->stream));
-    launched(ctx);
+    // cluster path: the whole M~^T in the shared memory of <= 16 CTAs
+    int csq = 0;
+    size_t csmem = 0;
+    for (int c = 1; c <= 16; c *= 2) {
+        const int cpb = cdiv(Ng, c);
+        const size_t bytes = ((size_t)cpb * m + 3 * (size_t)m + cpb) * sizeof(double) + 2 * (size_t)cpb * sizeof(int);
+        if (bytes <= 200 * 1024 && cpb >= 1) {
+            csq = c;
+            csmem = bytes;
+            // prefer a few CTAs over one: more SMs share the trailing updates
+            if (c >= 4 || (size_t)Ng * m * sizeof(double) <= 64 * 1024) break;
+        }
+    }
+    if (getenv("ACP_QRCP_GRID") || m > 256) csq = 0;  // test knob / register-resident update needs m <= 256
+    if (csq > 0) {
+        auto kern = m <= 64 ? k_qrcp_cluster<2> : m <= 128 ? k_qrcp_cluster<4> : k_qrcp_cluster<8>;
+        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(csq, 1, 1);
+        cfg.blockDim = dim3(1024, 1, 1);
+        cfg.dynamicSmemBytes = csmem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr1[1];
+        attr1[0].id = cudaLaunchAttributeClusterDimension;
+        attr1[0].val.clusterDim.x = csq;
+        attr1[0].val.clusterDim.y = 1;
+        attr1[0].val.clusterDim.z = 1;
+        cfg.attrs = attr1;
+        cfg.numAttrs = 1;
+        long long* tprof = nullptr;
+        const char* tpath = getenv("ACP_QR_PROFILE");
+        if (tpath) {
+            tprof = reinterpret_cast<long long*>(ctx->ws("qr_tprof", 8 * 512 * sizeof(long long)));
+            ACP_CUDA(cudaMemsetAsync(tprof, 0, 8 * 512 * sizeof(long long), ctx->stream));
+        }
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, m, Ng, A, kmax, id_eps, n_fixed, perm, rdiag, d_nmu, tprof));
+        if (tpath) {
+            std::vector<long long> h(8 * 512);
+            ACP_CUDA(cudaMemcpyAsync(h.data(), tprof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (FILE* f = fopen(tpath, "a")) {
+                for (int j = 0; j < 512 && h[8 * j]; ++j) {
+                    for (int k = 0; k < 5; ++k) fprintf(f, "%lld ", h[8 * j + k]);
+                    fprintf(f, "\n");
+                }
+                fclose(f);
+            }
+        }
+        launched(ctx);
+    } else {
+        int G = dev_sms < Ng ? dev_sms : Ng;
+        int cpb = cdiv(Ng, G);
+        G = cdiv(Ng, cpb);
+        const size_t tail = (size_t)m * sizeof(double) + (size_t)cpb * (sizeof(double) + 2 * sizeof(int)) + 64;
+        const size_t smem_full = (size_t)cpb * m * sizeof(double) + tail;
+        const bool use_smem = smem_full <= 200 * 1024;
+        const size_t smem = use_smem ? smem_full : tail;
+        QrSlot* slots = static_cast<QrSlot*>(ctx->ws("qr_slots", 2 * (size_t)G * sizeof(QrSlot)));
+        double* cand = ctx->wsd("qr_cand", 2 * (size_t)G * m);
+        void* args[] = {(void*)&m, (void*)&Ng, (void*)&A, (void*)&kmax, (void*)&id_eps, (void*)&n_fixed,
+                        (void*)&slots, (void*)&cand, (void*)&perm, (void*)&rdiag, (void*)&d_nmu};
+        const void* fn = use_smem ? (const void*)k_qrcp_persistent<true> : (const void*)k_qrcp_persistent<false>;
+        ACP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        ACP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+        ACP_REQUIRE(occ >= 1 && G <= occ * dev_sms, "QRCP: cooperative grid does not fit");
+        ACP_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(256), args, smem, ctx->stream));
+        launched(ctx);
+    }
     int* hp = static_cast<int*>(ctx->pinned);
     ACP_CUDA(cudaMemcpyAsync(hp, d_nmu, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ACP_CUDA(cudaStreamSynchronize(ctx->stream));

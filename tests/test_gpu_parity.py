@@ -159,6 +159,21 @@ def test_compress_pivots_bit_exact(sysx):
         assert rel(Xi_g2.cpu().numpy().T, Xi_o2) < 1e-9
 
 
+def test_compress_cluster_and_grid_qrcp_agree(sysx, monkeypatch):
+    """The cluster/DSMEM QRCP (small problems) and the grid-wide persistent QRCP (forced with
+    ACP_QRCP_GRID) pick the same pivots and agree with the oracle."""
+    from paper_1605_08021_b200 import Context
+    s = sysx
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    monkeypatch.setenv("ACP_QRCP_GRID", "1")
+    ctx = Context.from_config(s.cfg)
+    S_g, Xi_g, n = ctx.compress(s.Psi_t, s.G_t, th, nu, id_eps=s.cfg.id_eps)
+    ctx.close()
+    assert np.array_equal(S_g.cpu().numpy(), S_o)
+    assert rel(Xi_g.cpu().numpy().T, Xi_o) < 1e-9
+
+
 # ---------------------------------------------------------------- Alg. 3
 def test_apply_chi0_matches_direct_solves(sysx):
     s = sysx
@@ -185,6 +200,19 @@ def test_apply_chi0_sharding_is_bitwise(sysx):
     s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb, mu_range=(0, cut), W=W_sh)
     s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb, mu_range=(cut, n), W=W_sh)
     assert torch.equal(W_full, W_sh)
+
+
+def test_smw_update_vs_oracle(sysx):
+    """Eq. dyson4 alone with a random low-rank chi0~ = W Pi^T of rank N (several LU panels)."""
+    s = sysx
+    rng = np.random.default_rng(31)
+    N = min(100, s.m.Ng // 2)
+    S = np.sort(rng.choice(s.m.Ng, N, replace=False)).astype(np.int32)
+    W = 1e-2 * rng.standard_normal((s.m.Ng, N))
+    U_o, Gp_o, _ = oacp.smw_update(s.m, s.G, W, S)
+    U_g, Gp_g = s.ctx.smw_update(s.G_t, T(S, torch.int32), T(W.T))
+    assert rel(U_g.cpu().numpy().T, U_o) < 1e-11
+    assert rel(Gp_g.cpu().numpy().T, Gp_o) < 1e-11
 
 
 # ---------------------------------------------------------------- Alg. 4 + D

@@ -1,6 +1,6 @@
 """Probe the full-size 2D configs on the GPU: K1 accuracy/timing and the ground state (gap, SCF).
 
-  python tools/probe_2d.py [c3_2d_8x8|c4_2d_16x16] [max_scf_iter]
+  python tools/probe_2d.py [c3_2d_8x8|c4_2d_16x16] [max_scf_iter] [eps0 override]
 
 Prints one JSON line per config.  The oracle is used only for the cheap FFT-based
 operator reference (Model.kinetic), never for the dense solvers.
@@ -23,10 +23,13 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c3_2d_8x8"
     max_it = int(sys.argv[2]) if len(sys.argv) > 2 else 300
     cfg = get_config(name)
+    if len(sys.argv) > 3:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, eps0=float(sys.argv[3]))
     R = atom_positions(cfg)
     ctx = Context.from_config(cfg)
     m = Model(cfg, R)
-    out = {"config": name, "N_g": m.Ng}
+    out = {"config": name, "eps0": cfg.eps0, "N_g": m.Ng}
     rng = np.random.default_rng(0)
     X = rng.standard_normal((m.Ng, 4))
     Y = ctx.fourier_apply(torch.as_tensor(X.T.copy(), device="cuda"), 0).cpu().numpy().T
