@@ -40,6 +40,7 @@ struct FftPlan {
     int N = 0;
     int npass = 0;
     int radix[24] = {0};
+    int twoff[25] = {0};  // per-pass twiddle table offsets (entries), twoff[npass] = total
 };
 
 // Grow-only device buffer.
@@ -171,6 +172,12 @@ struct FopArgs {
     const double* shift = nullptr; // per-column shift or null
     const int* active = nullptr;   // per-column activity flags or null
     double* dots = nullptr;        // per column: [0] x.y [1] x.x  (stride 2) or null
+    long long* tprof = nullptr;    // debug: clock64() at phase boundaries of CTA 0 / thread 0, or null
+    // Analytic symbol computed in-kernel from the bin index instead of a table read (saves the
+    // per-CTA table traffic): -1 = use `mult`, MULT_KINETIC = |k|^2/2, MULT_PRECOND =
+    // 1/(|k|^2/2 + tau) (preconditioner: reciprocal by rcp.approx + 2 Newton steps).
+    int sym = -1;
+    double tau = 0.0;
 };
 // Y = IFFT(mult * FFT(X)) + (diag - shift_j) (.) X, two real columns per complex FFT.
 void fourier_op(acp_context* ctx, const FopArgs& a);

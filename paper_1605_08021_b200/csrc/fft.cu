@@ -46,6 +46,11 @@ FftPlan make_plan(int N) {
         }
     }
     ACP_REQUIRE(n == 1, "grid size must factor into 2, 3 and 5");
+    int Ns = 1;
+    for (int q = 0; q < p.npass; ++q) {
+        p.twoff[q + 1] = p.twoff[q] + Ns * (p.radix[q] - 1);
+        Ns *= p.radix[q];
+    }
     return p;
 }
 
@@ -54,8 +59,9 @@ struct FftGeom {
     FftPlan p0, p1;   // axis 0 / axis 1 plans (1D: p0 only)
     int n0, n1;       // grid (1D: n1 = 1)
     int cs, r0, c1;   // 2D cluster size, rows and columns per CTA
-    int sh0, sh1;     // twiddle table splits
-    int tw0n, tw1n;   // twiddle entries
+    int tw0n, tw1n;   // twiddle table entries (axis 0 / axis 1)
+    double dk0, dk1;  // 2 pi / L per axis
+    double invN;      // 1 / N_g
     int ldc;          // column-phase leading dimension (n0 + 8)
 };
 
@@ -68,10 +74,11 @@ static FftGeom geom(const acp_context* ctx) {
     g.cs = ctx->cs;
     g.r0 = ctx->r0;
     g.c1 = ctx->c1;
-    g.sh0 = tw_split(g.n0);
-    g.sh1 = ctx->dim == 2 ? tw_split(g.n1) : 0;
-    g.tw0n = tw_entries(g.n0);
-    g.tw1n = ctx->dim == 2 ? tw_entries(g.n1) : 0;
+    g.dk0 = 2.0 * M_PI / ctx->sys.cell[0];
+    g.dk1 = ctx->dim == 2 ? 2.0 * M_PI / ctx->sys.cell[1] : 0.0;
+    g.invN = 1.0 / (double)ctx->Ng;
+    g.tw0n = g.p0.twoff[g.p0.npass];
+    g.tw1n = ctx->dim == 2 ? g.p1.twoff[g.p1.npass] : 0;
     g.ldc = g.n0 + 8;  // with the P() pad: conflict-free column passes and transposes (enumerated)
     return g;
 }
@@ -88,6 +95,22 @@ struct IoArgs {
     double2* sout = nullptr;    // IO_SPEC: its spectrum
     int n = 0;                  // number of columns (IO_OP: f.n)
 };
+
+// In-kernel symbol of bin (i0, i1) (already divided by N, like the tables).
+__device__ __forceinline__ double sym_value(const FftGeom& G, int sym, double tau, int i0, int i1) {
+    const int m0 = i0 < (G.n0 + 1) / 2 ? i0 : i0 - G.n0;
+    const int m1 = i1 < (G.n1 + 1) / 2 ? i1 : i1 - G.n1;
+    const double ka = m0 * G.dk0, kb = m1 * G.dk1;
+    const double h = 0.5 * (ka * ka + kb * kb);
+    if (sym == MULT_KINETIC) return h * G.invN;
+    // MULT_PRECOND: 1/(h + tau) by the hardware reciprocal estimate refined by two Newton steps
+    const double d = h + tau;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    r = r * (2.0 - d * r);
+    r = r * (2.0 - d * r);
+    return r * G.invN;
+}
 
 // ============================================================================ 1D
 
@@ -114,15 +137,18 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
         act1 = has1 && io.f.active[c1] != 0;
     }
     if (!act0 && !act1) return;
-    const bool do_fft = IO != IO_OP || io.f.mult != nullptr;
-    if (IO == IO_OP && do_fft) {
+#define K1_TP(q) \
+    if (IO == IO_OP && io.f.tprof && blockIdx.x == 0 && threadIdx.x == 0) io.f.tprof[q] = clock64();
+    K1_TP(0)
+    const bool do_fft = IO != IO_OP || io.f.mult != nullptr || io.f.sym >= 0;
+    if (IO == IO_OP && io.f.mult && io.f.sym < 0) {
         if ((N & 1) == 0) {
             for (int c = tid; c < N / 2; c += T) cp_async16_fe(smult + 2 * c, io.f.mult + 2 * c);
         } else {
             for (int i = tid; i < N; i += T) smult[i] = io.f.mult[i];
         }
     }
-    const TwTable tw = load_twiddles(sm1 + padded(N), twg, N, G.sh0);
+    const double2* tw = load_twiddles(sm1 + padded(N), twg, G.p0);
     constexpr int NK = KEEP ? EPT : 1;  // register-resident inputs (KEEP) or re-read in the epilogue
     double u0[NK], u1[NK];
     const double* x0 = io.f.X + (size_t)c0 * N;
@@ -154,7 +180,9 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
     }
     cp_async_wait_all_fe();  // twiddles and the multiplier
     __syncthreads();
+    K1_TP(1)
     if (do_fft) fft_inplace<EPT>(buf, N, 1, G.p0, tw);
+    K1_TP(2)
     if (IO == IO_HERM) {
         for (int i = tid; i < N; i += T) {
             const double2 v = buf[P(i)];
@@ -179,13 +207,15 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
     if (do_fft) {
         // conj(mult * F) then forward FFT == N * conj(IFFT(mult * F)) (1/N folded into mult)
         for (int i = tid; i < N; i += T) {
-            const double m = smult[i];
+            const double m = a.sym >= 0 ? sym_value(G, a.sym, a.tau, i, 0) : smult[i];
             const double2 v = buf[P(i)];
             buf[P(i)] = make_double2(m * v.x, -m * v.y);
         }
         __syncthreads();
+        K1_TP(3)
         fft_inplace<EPT>(buf, N, 1, G.p0, tw);
     }
+    K1_TP(4)
     const double s0 = a.shift ? a.shift[c0] : 0.0;
     const double s1 = (a.shift && has1) ? a.shift[c1] : 0.0;
     double d[4] = {0.0, 0.0, 0.0, 0.0};
@@ -215,6 +245,7 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
             d[3] += xb * xb;
         }
     }
+    K1_TP(5)
     if (a.dots) {
         block_sum4(d, red);
         if (tid == 0) {
@@ -228,6 +259,7 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
             }
         }
     }
+    K1_TP(6)
 }
 
 // ============================================================================ 2D
@@ -307,8 +339,8 @@ __global__ void __launch_bounds__(1024) k_fft2d(FftGeom G, const double2* __rest
         act1 = has1 && io.f.active[c1] != 0;
     }
     if (!act0 && !act1) return;  // uniform over the cluster
-    const TwTable tw0 = load_twiddles(sm2 + bufn, tw0g, G.n0, G.sh0);
-    const TwTable tw1 = load_twiddles(sm2 + bufn + G.tw0n, tw1g, G.n1, G.sh1);
+    const double2* tw0 = load_twiddles(sm2 + bufn, tw0g, G.p0);
+    const double2* tw1 = load_twiddles(sm2 + bufn + G.tw0n, tw1g, G.p1);
     const int E = G.r0 * G.n1;            // elements owned in the row phase
     const size_t rowbase = (size_t)rank * G.r0 * G.n1;
     const double* x0 = nullptr;
@@ -330,7 +362,7 @@ __global__ void __launch_bounds__(1024) k_fft2d(FftGeom G, const double2* __rest
     }
     cp_async_wait_all_fe();  // twiddles
     __syncthreads();
-    const bool do_fft = IO != IO_OP || io.f.mult != nullptr;
+    const bool do_fft = IO != IO_OP || io.f.mult != nullptr || io.f.sym >= 0;
     if (do_fft) {
         fft_inplace<EPT>(buf, G.n1, G.r0, G.p1, tw1);       // rows (length n1)
         rows_to_cols<EPT>(cl, buf, G, rank);
@@ -357,7 +389,8 @@ __global__ void __launch_bounds__(1024) k_fft2d(FftGeom G, const double2* __rest
         const int Ec = G.n0 * G.c1;
         for (int e = threadIdx.x; e < Ec; e += blockDim.x) {
             const int k0 = e / G.c1, c = e - k0 * G.c1;
-            const double m = __ldg(&a.mult[(size_t)k0 * G.n1 + rank * G.c1 + c]);
+            const double m = a.sym >= 0 ? sym_value(G, a.sym, a.tau, k0, rank * G.c1 + c)
+                                        : __ldg(&a.mult[(size_t)k0 * G.n1 + rank * G.c1 + c]);
             const double2 v = buf[P(c * G.ldc + k0)];
             buf[P(c * G.ldc + k0)] = make_double2(m * v.x, -m * v.y);
         }
@@ -579,18 +612,21 @@ void spectrum_m(acp_context* ctx, const double* d_R, double2* spec) {
 }
 
 // ---- plan / symbol setup ---------------------------------------------------
-static std::vector<double2> twiddle_table(int L) {
-    auto w = [L](long long m) {
-        long double ang = -2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)L;
-        return make_double2((double)cosl(ang), (double)sinl(ang));
-    };
-    const int sh = tw_split(L);
-    std::vector<double2> t;
-    if (sh == 0) {
-        for (int m = 0; m < L; ++m) t.push_back(w(m));
-    } else {
-        for (int m = 0; m < (1 << sh); ++m) t.push_back(w(m));              // lo
-        for (int m = 0; m <= (L >> sh); ++m) t.push_back(w((long long)m << sh));  // hi
+// Per-pass twiddle tables of a plan: pass q (radix R, Ns) stores w = exp(-2 pi i r k / (Ns R))
+// at twoff[q] + k (R - 1) + r - 1 (k < Ns, 1 <= r < R), argument reduced exactly in long double.
+static std::vector<double2> twiddle_table(const FftPlan& pl) {
+    std::vector<double2> t(pl.twoff[pl.npass] > 0 ? pl.twoff[pl.npass] : 1);
+    int Ns = 1;
+    for (int q = 0; q < pl.npass; ++q) {
+        const int R = pl.radix[q];
+        for (int k = 0; k < Ns; ++k)
+            for (int r = 1; r < R; ++r) {
+                const long long num = (long long)r * k, den = (long long)Ns * R;
+                const long double ang = -2.0L * 3.14159265358979323846264338327950288L * (long double)(num % den) /
+                                        (long double)den;
+                t[pl.twoff[q] + k * (R - 1) + r - 1] = make_double2((double)cosl(ang), (double)sinl(ang));
+            }
+        Ns *= R;
     }
     return t;
 }
@@ -616,8 +652,8 @@ void fft_init(acp_context* ctx) {
     const int N = n0 * n1;
     ctx->plan = make_plan(n0);
     if (dim == 2) ctx->plan1 = make_plan(n1);
-    ctx->d_tw = upload(twiddle_table(n0));
-    if (dim == 2) ctx->d_tw1 = upload(twiddle_table(n1));
+    ctx->d_tw = upload(twiddle_table(ctx->plan));
+    if (dim == 2) ctx->d_tw1 = upload(twiddle_table(ctx->plan1));
     // per-axis frequencies and the N_g tables (bins in C order)
     std::vector<double> kax[2], kodd[2];
     for (int a = 0; a < dim; ++a) {
@@ -658,13 +694,14 @@ void fft_init(acp_context* ctx) {
         ctx->fthreads = T;
         ctx->fept = ept_for(N, T);
         ACP_REQUIRE(ctx->fept > 0, "1D grid too large for the shared-memory FFT");
-        ctx->fsmem = (size_t)(padded(N) + tw_entries(n0)) * sizeof(double2) + (size_t)N * sizeof(double);
+        ctx->fsmem = (size_t)(padded(N) + ctx->plan.twoff[ctx->plan.npass]) * sizeof(double2) + (size_t)N * sizeof(double);
         ACP_REQUIRE(ctx->fsmem <= 220 * 1024, "1D grid too large for the shared-memory FFT");
     } else {
         // smallest cluster (cs | n0, cs | n1, cs <= 16) whose per-CTA slice has <= 4096 points
         auto slice = [&](int c) { return std::max((n0 / c) * n1, (n1 / c) * (n0 + 8)); };
         auto bytes = [&](int c) {
-            return (size_t)(padded(slice(c)) + tw_entries(n0) + tw_entries(n1)) * sizeof(double2);
+            return (size_t)(padded(slice(c)) + ctx->plan.twoff[ctx->plan.npass] + ctx->plan1.twoff[ctx->plan1.npass]) *
+                   sizeof(double2);
         };
         int cs = 1;
         while (cs < 16 && slice(cs) > 4096 && n0 % (2 * cs) == 0 && n1 % (2 * cs) == 0) cs *= 2;
@@ -679,7 +716,7 @@ void fft_init(acp_context* ctx) {
         ctx->r0 = n0 / cs;
         ctx->c1 = n1 / cs;
         const int E = std::max(ctx->r0 * n1, ctx->c1 * n0);
-        int T = tknob > 0 ? round32(tknob) : round32((E + 3) / 4);
+        int T = tknob > 0 ? round32(tknob) : round32((E + 7) / 8);  // k1_sweep: E/8 beats E/4 (c3 512 vs 297 GB/s)
         T = T < 64 ? 64 : T > 1024 ? 1024 : T;
         ctx->fthreads = T;
         ctx->fept = ept_for(E, T);

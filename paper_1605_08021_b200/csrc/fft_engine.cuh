@@ -93,23 +93,11 @@ template <> __device__ __forceinline__ void dft<5>(double2* x) {
 __device__ __forceinline__ int P(int i) { return i + (i >> 3); }
 __host__ __device__ constexpr int padded(int n) { return n + (n >> 3) + 1; }
 
-// Twiddle table exp(-2 pi i m / L), m < L, in shared memory (padded indexing).  Long
-// transforms (L > 4096) use a two-level table w(m) = hi[m >> sh] * lo[m & (2^sh - 1)] (each
-// entry correctly rounded on the host; the product adds <= 2 ulp).
-struct TwTable {
-    const double2* lo;
-    const double2* hi;
-    int sh;    // 0: single-level table in lo
-    int half;  // single level, L even: lo holds m < L/2 and w(m + L/2) = -w(m)
-    __device__ __forceinline__ double2 operator()(int m) const {
-        if (sh == 0) {
-            if (m < half || half == 0) return lo[P(m)];
-            const double2 v = lo[P(m - half)];
-            return make_double2(-v.x, -v.y);
-        }
-        return cmul(hi[m >> sh], lo[P(m & ((1 << sh) - 1))]);
-    }
-};
+// Twiddles: one table per Stockham pass, laid out [k][r-1] for the pass's Ns sub-transform
+// offsets k and radix digits r = 1..R-1: w = exp(-2 pi i r k / (Ns R)), each entry correctly
+// rounded on the host.  A butterfly reads its R-1 twiddles contiguously (stride R-1 across
+// threads, odd for R = 8, 4, 2: conflict-free) -- no power recurrences, no 2-level products.
+// FftPlan::twoff[p] is pass p's offset; FftPlan::twoff[npass] the table length.
 
 // q = floor(a / d) for 0 <= a < 2^21, d >= 1, via a float reciprocal: (a + 0.5)/d lies at least
 // 0.5/d from an integer, and the two roundings of (a + 0.5) * fl(1/d) err by < 2^-22 (a + 0.5)/d
@@ -120,11 +108,10 @@ __device__ __forceinline__ int fdiv(int a, float rd) { return __float2int_rz(((f
 // padded indexing P): sub-transforms of length Ns are combined into length Ns*R.  EPT = max
 // complex values a thread holds (EPT >= nb*L / blockDim.x).  Ends with a block barrier.
 template <int R, int EPT>
-__device__ __forceinline__ void pass_inplace(double2* buf, int L, int ld, int nb, int Ns, const TwTable& tw) {
+__device__ __forceinline__ void pass_inplace(double2* buf, int L, int ld, int nb, int Ns, const double2* __restrict__ tw) {
     constexpr int MB = (EPT + R - 1) / R;
     const int per = L / R;              // butterflies per transform
     const int total = nb * per;
-    const int stride = L / (Ns * R);    // twiddle stride for this pass
     const float rper = 1.0f / (float)per, rNs = 1.0f / (float)Ns;
     double2 x[MB][R];
 #pragma unroll
@@ -138,15 +125,9 @@ __device__ __forceinline__ void pass_inplace(double2* buf, int L, int ld, int nb
 #pragma unroll
             for (int r = 0; r < R; ++r) x[b][r] = buf[P(base + r * per)];
             if (Ns > 1) {
-                // one table read per butterfly; w^r by repeated products (error <= ~R ulp)
-                const double2 w = tw(k * stride);
-                double2 wr = w;
-                x[b][1] = cmul(x[b][1], w);
+                const double2* tk = tw + k * (R - 1);
 #pragma unroll
-                for (int r = 2; r < R; ++r) {
-                    wr = cmul(wr, w);
-                    x[b][r] = cmul(x[b][r], wr);
-                }
+                for (int r = 1; r < R; ++r) x[b][r] = cmul(x[b][r], tk[r - 1]);
             }
             dft<R>(x[b]);
         }
@@ -169,35 +150,22 @@ __device__ __forceinline__ void pass_inplace(double2* buf, int L, int ld, int nb
 
 // Forward FFT (exp(-i ...)) of nb transforms of length pl.N in place (transform t at buf + t*ld).
 template <int EPT>
-__device__ __forceinline__ void fft_inplace(double2* buf, int ld, int nb, const FftPlan& pl, const TwTable& tw) {
+__device__ __forceinline__ void fft_inplace(double2* buf, int ld, int nb, const FftPlan& pl,
+                                            const double2* __restrict__ tw) {
     // The plan lists its radices in the fixed order 8, 4, 2, 5, 3 (make_plan); one loop per
     // radix keeps the register allocation of each pass independent (a switch inside a single
     // loop made ptxas keep every variant's butterfly registers live at once).
     int Ns = 1, p = 0;
-    for (; p < pl.npass && pl.radix[p] == 8; ++p, Ns *= 8) pass_inplace<8, EPT>(buf, pl.N, ld, nb, Ns, tw);
-    for (; p < pl.npass && pl.radix[p] == 4; ++p, Ns *= 4) pass_inplace<4, EPT>(buf, pl.N, ld, nb, Ns, tw);
-    for (; p < pl.npass && pl.radix[p] == 2; ++p, Ns *= 2) pass_inplace<2, EPT>(buf, pl.N, ld, nb, Ns, tw);
-    for (; p < pl.npass && pl.radix[p] == 5; ++p, Ns *= 5) pass_inplace<5, EPT>(buf, pl.N, ld, nb, Ns, tw);
-    for (; p < pl.npass && pl.radix[p] == 3; ++p, Ns *= 3) pass_inplace<3, EPT>(buf, pl.N, ld, nb, Ns, tw);
+    for (; p < pl.npass && pl.radix[p] == 8; ++p, Ns *= 8) pass_inplace<8, EPT>(buf, pl.N, ld, nb, Ns, tw + pl.twoff[p]);
+    for (; p < pl.npass && pl.radix[p] == 4; ++p, Ns *= 4) pass_inplace<4, EPT>(buf, pl.N, ld, nb, Ns, tw + pl.twoff[p]);
+    for (; p < pl.npass && pl.radix[p] == 2; ++p, Ns *= 2) pass_inplace<2, EPT>(buf, pl.N, ld, nb, Ns, tw + pl.twoff[p]);
+    for (; p < pl.npass && pl.radix[p] == 5; ++p, Ns *= 5) pass_inplace<5, EPT>(buf, pl.N, ld, nb, Ns, tw + pl.twoff[p]);
+    for (; p < pl.npass && pl.radix[p] == 3; ++p, Ns *= 3) pass_inplace<3, EPT>(buf, pl.N, ld, nb, Ns, tw + pl.twoff[p]);
 }
 
-// Host-side layout of a twiddle table for length L: the level split sh (0 = single level) and
-// the number of double2 entries in GLOBAL memory (lo followed by hi, unpadded) and in SHARED
-// memory (lo padded).
-inline int tw_split(int L) {
-    if (L <= 4096) return 0;
-    int sh = 1;
-    while ((1 << (2 * sh)) < L) ++sh;   // lo has 2^sh ~ sqrt(L) entries
-    return sh;
-}
-inline int tw_entries(int L) {
-    const int sh = tw_split(L);
-    return sh == 0 ? padded((L & 1) ? L : L / 2) : padded(1 << sh) + (L >> sh) + 1;
-}
-
-// Copy a twiddle table into shared memory `dst` with cp.async (16-byte chunks, no register
-// round trip: the copies overlap whatever the CTA does next).  The caller commits/waits and
-// synchronises before the first twiddled pass.
+// Copy a plan's twiddle table (pl.twoff[pl.npass] entries) into shared memory with cp.async
+// (16-byte chunks, no register round trip: the copies overlap whatever the CTA does next).
+// The caller commits/waits and synchronises before the first twiddled pass.
 __device__ __forceinline__ void cp_async16_fe(void* smem, const void* gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
@@ -206,20 +174,11 @@ __device__ __forceinline__ void cp_async_wait_all_fe() {
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 0;\n" ::);
 }
-__device__ __forceinline__ TwTable load_twiddles(double2* dst, const double2* __restrict__ src, int L, int sh) {
-    const int half = (sh == 0 && (L & 1) == 0) ? L / 2 : 0;
-    const int nlo = sh == 0 ? (half ? half : L) : (1 << sh);
-    const int nhi = sh == 0 ? 0 : (L >> sh) + 1;
-    const int hoff = sh == 0 ? L : nlo;  // global offset of the hi table
-    for (int i = threadIdx.x; i < nlo; i += blockDim.x) cp_async16_fe(dst + P(i), src + i);
-    double2* hi = dst + padded(nlo);
-    for (int i = threadIdx.x; i < nhi; i += blockDim.x) cp_async16_fe(hi + i, src + hoff + i);
-    TwTable t;
-    t.lo = dst;
-    t.hi = hi;
-    t.sh = sh;
-    t.half = half;
-    return t;
+__device__ __forceinline__ const double2* load_twiddles(double2* dst, const double2* __restrict__ src,
+                                                        const FftPlan& pl) {
+    const int n = pl.twoff[pl.npass];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) cp_async16_fe(dst + i, src + i);
+    return dst;
 }
 
 // Deterministic block sum of 4 values (fixed reduction tree); red needs 132 doubles.

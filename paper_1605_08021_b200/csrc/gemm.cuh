@@ -210,8 +210,13 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     // rank r finalises elements e = r, r + CS, ... (column-major walk for coalesced stores)
     for (int e = rank * 128 + tid; e < BM * TC_BN; e += CS * 128) {
         const int row = e % BM, col = e / BM;
+        // all CS remote loads in flight together (one DSMEM latency), then summed in rank order
+        double part[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) part[q] = q < CS ? cluster.map_shared_rank(Cs, q)[row * LDC + col] : 0.0;
         double s = 0.0;
-        for (int q = 0; q < CS; ++q) s += cluster.map_shared_rank(Cs, q)[row * LDC + col];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += part[q];
         const int gm = m0 + row, gn = n0 + col;
         if (gm < m && gn < n) C[(size_t)gn * ldc + gm] = alpha * s;
     }
