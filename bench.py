@@ -273,6 +273,11 @@ def run_acp(args, cfg):
             byts = 16.0 * Ng * ncols
             kern[name] = dict(bound="hbm", us=us, bytes=byts, achieved=byts / us / 1e3, unit="GB/s",
                               peak=peaks["hbm_gbs"])
+            # the same launch seen as FP64 ALU work: two length-N_g FFTs per packed column pair,
+            # 5 N log2 N flops each (complex radix-2 count), i.e. 5 N_g log2 N_g per real column
+            fl = 5.0 * Ng * np.log2(Ng) * ncols
+            kern[name]["alu"] = dict(flops=fl, achieved=fl / us / 1e6, unit="TFLOP/s", peak=peaks["fp64_tflops"],
+                                     frac=fl / us / 1e6 / peaks["fp64_tflops"])
         elif which == 1:
             fl = 2.0 * Ng * No * ncols
             kern[name] = dict(bound="tensor", us=us, flops=fl, achieved=fl / us / 1e6, unit="TFLOP/s",

@@ -214,3 +214,19 @@ def acp_dyson(model: Model, H: np.ndarray, Psi: np.ndarray, eps_occ: np.ndarray,
         U_prev = U
     res.U = U_prev
     return res
+
+
+def compressed_W_free_electron(model: Model, Psi: np.ndarray, eps_occ: np.ndarray, occ_mask: np.ndarray,
+                               S: np.ndarray, Xi: np.ndarray, Nc: int) -> np.ndarray:
+    """Eq. eqnW with the compressed Sternheimer solutions of Eq. eqncompressU
+    taken from the V = 0 closed form (response.sternheimer_free_electron); everything else as in
+    compressed_W.  Valid only for a free-electron ground state with complete occupied shells."""
+    from .response import sternheimer_free_electron
+    nodes = chebyshev_nodes(eps_occ[0], eps_occ[-1], Nc)
+    Lw = lagrange_weights(nodes, eps_occ)
+    W = np.zeros_like(Xi)
+    for c in range(Nc):
+        Z = sternheimer_free_electron(model, occ_mask, nodes[c], Xi)
+        Phi_c = Psi @ (Lw[:, c:c + 1] * Psi[S, :].T)
+        W += 2.0 * model.f * Z * Phi_c
+    return W

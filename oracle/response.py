@@ -94,3 +94,14 @@ def dyson_dfpt(model: Model, H: np.ndarray, Psi: np.ndarray, eps: np.ndarray,
     """
     C0 = chi0_apply(model, H, Psi, eps, np.eye(model.Ng))
     return dyson_dense(model, C0, G)
+
+
+def sternheimer_free_electron(model: Model, occ_mask: np.ndarray, shift: float, rhs: np.ndarray) -> np.ndarray:
+    """Closed form of Q(shift - H)Q zeta = Q rhs for the free-electron case V = 0
+    with the occupied orbitals = the plane waves of a complete shell set (occ_mask over the FFT
+    bins, True = occupied).  H = -1/2 Laplacian is diagonal in Fourier space and Q removes the
+    occupied bins, so zeta^(k) = rhs^(k) / (shift - |k|^2/2) on unoccupied bins and 0 on
+    occupied ones (the solution in range(Q)).  Used as a full-grid pin (no dense matrices)."""
+    with np.errstate(divide="ignore"):
+        mult = np.where(occ_mask, 0.0, 1.0 / (shift - 0.5 * model.k2))
+    return model.fourier_multiply(rhs, mult)
