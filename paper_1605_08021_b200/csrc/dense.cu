@@ -282,10 +282,13 @@ __global__ void __launch_bounds__(1024) k_lu_panel(double* __restrict__ AB, int 
         __syncthreads();
         const double akk = ck[kk];
         const double rp = akk == 0.0 ? 0.0 : 1.0 / akk;
-        for (int i = kk + 1 + tid; i < R; i += nt) {
-            const double l = ck[i] * rp;
-            ck[i] = l;
-            for (int jj = kk + 1; jj < pw; ++jj) P[(size_t)jj * ld + i] -= l * P[(size_t)jj * ld + kk];
+        for (int i = kk + 1 + tid; i < R; i += nt) ck[i] *= rp;
+        __syncthreads();
+        // rank-1 update of the panel's remaining columns: warps over columns, lanes over rows
+        for (int jj = kk + 1 + warp; jj < pw; jj += nwarp) {
+            double* cj = P + (size_t)jj * ld;
+            const double akj = cj[kk];
+            for (int i = kk + 1 + lane; i < R; i += 32) cj[i] -= ck[i] * akj;
         }
         __syncthreads();
     }
@@ -310,8 +313,15 @@ __global__ void k_lu_swap(double* __restrict__ AB, int n, int ntot, int p0, int 
     }
 }
 
-// U12 = L11^{-1} A12 for columns j >= p0 + pw: one warp per column, lane i holds row p0 + i.
-__global__ void k_lu_trsm12(double* __restrict__ AB, int n, int ntot, int p0, int pw) {
+// U12 = L11^{-1} A12 for columns j >= p0 + pw: one warp per column, lane i holds row p0 + i;
+// the unit lower triangle L11 (pw x pw) is staged in shared memory once per CTA.
+__global__ void __launch_bounds__(256) k_lu_trsm12(double* __restrict__ AB, int n, int ntot, int p0, int pw) {
+    __shared__ double Ls[32][33];
+    for (int e = threadIdx.x; e < pw * pw; e += blockDim.x) {
+        const int k = e / pw, i = e - k * pw;
+        Ls[k][i] = AB[(size_t)(p0 + k) * n + p0 + i];
+    }
+    __syncthreads();
     const int w = blockIdx.x * (blockDim.x >> 5) + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     const int j = p0 + pw + w;
@@ -320,22 +330,32 @@ __global__ void k_lu_trsm12(double* __restrict__ AB, int n, int ntot, int p0, in
     double x = lane < pw ? cj[lane] : 0.0;
     for (int k = 0; k < pw; ++k) {
         const double xk = __shfl_sync(0xffffffffu, x, k);
-        if (lane > k && lane < pw) x -= AB[(size_t)(p0 + k) * n + p0 + lane] * xk;
+        if (lane > k && lane < pw) x -= Ls[k][lane] * xk;
     }
     if (lane < pw) cj[lane] = x;
 }
 
-// X_b = U_bb^{-1} B_b for the rows [q0, q0 + qb) (qb <= 32): one warp per right-hand side.
-__global__ void k_lu_bsub(double* __restrict__ AB, int n, int nrhs, int q0, int qb) {
+// X_b = U_bb^{-1} B_b for the rows [q0, q0 + qb) (qb <= 32): one warp per right-hand side, the
+// diagonal block of U staged in shared memory with reciprocal diagonal.
+__global__ void __launch_bounds__(256) k_lu_bsub(double* __restrict__ AB, int n, int nrhs, int q0, int qb) {
+    __shared__ double Us[32][33];
+    __shared__ double rd[32];
+    for (int e = threadIdx.x; e < qb * qb; e += blockDim.x) {
+        const int k = e / qb, i = e - k * qb;
+        Us[k][i] = AB[(size_t)(q0 + k) * n + q0 + i];
+    }
+    __syncthreads();
+    if (threadIdx.x < qb) rd[threadIdx.x] = 1.0 / Us[threadIdx.x][threadIdx.x];
+    __syncthreads();
     const int w = blockIdx.x * (blockDim.x >> 5) + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     if (w >= nrhs) return;
     double* bj = AB + (size_t)(n + w) * n + q0;
     double x = lane < qb ? bj[lane] : 0.0;
     for (int k = qb - 1; k >= 0; --k) {
-        const double xk = __shfl_sync(0xffffffffu, x, k) / AB[(size_t)(q0 + k) * n + q0 + k];
+        const double xk = __shfl_sync(0xffffffffu, x, k) * rd[k];
         if (lane == k) x = xk;
-        if (lane < k) x -= AB[(size_t)(q0 + k) * n + q0 + lane] * xk;
+        if (lane < k) x -= Us[k][lane] * xk;
     }
     if (lane < qb) bj[lane] = x;
 }
@@ -356,7 +376,7 @@ void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
         const int R = n - p0;
         const size_t pbytes = (size_t)R * pw * sizeof(double);
         const int use_smem = pbytes <= 200 * 1024;
-        const int T = std::min(1024, std::max(128, (R + 31) / 32 * 32));
+        const int T = 1024;
         k_lu_panel<<<1, T, use_smem ? pbytes : 0, ctx->stream>>>(AB, n, p0, pw, use_smem, piv, st);
         launched(ctx);
         k_lu_swap<<<cdiv(ntot, 128), 128, 0, ctx->stream>>>(AB, n, ntot, p0, pw, piv);
@@ -550,7 +570,9 @@ void sym_eig(acp_context* ctx, double* A, int n, double* w, double* V) {
         ACP_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    k_jacobi<<<1, 1024, use_smem ? bytes : 0, ctx->stream>>>(A, n, Vt, w, order, rot, 40, use_smem);
+    // one warp per rotation pair (n/2 pairs) is enough; fewer threads make each barrier cheaper
+    const int jt = std::min(1024, std::max(64, ((n + 1) / 2) * 32));
+    k_jacobi<<<1, jt, use_smem ? bytes : 0, ctx->stream>>>(A, n, Vt, w, order, rot, 40, use_smem);
     launched(ctx);
     if (V) {
         k_permute_cols<<<cdiv((long long)n * n, 256), 256, 0, ctx->stream>>>(n, Vt, order, V);

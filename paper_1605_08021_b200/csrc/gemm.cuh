@@ -95,6 +95,75 @@ __device__ __forceinline__ void nn_tile(int M, int K, int n, const double* __res
     }
 }
 
+// 32 x 32 NN tile with the epilogue operands PREFETCHED: every thread issues the global loads
+// of its 8 output elements' epilogue operands before the K loop, so their latency overlaps the
+// tile loads and the DMMA work (the PCG updates are bound by exactly those loads).  128 threads =
+// 4 warps as 2 (m) x 2 (n), warp tile 16 x 16 = 2 x 2 DMMA tiles.
+constexpr int NP_BM = 32, NP_BN = 32, NP_BK = 16;
+
+template <class Ep>
+__device__ __forceinline__ void nn_tile_pf(int M, int K, int n, const double* __restrict__ A, int lda,
+                                           const double* __restrict__ B, int ldb, int m0, int n0, const Ep& ep) {
+    __shared__ double As[NP_BK][NP_BM + 4];
+    __shared__ double Bs[NP_BN][NP_BK + 4];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp & 1, wn = warp >> 1;
+    typename Ep::Regs regs[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = m0 + wm * 16 + i * 8 + g;
+                const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
+                if (row < M && col < n) ep.load(row, col, regs[i][j][e]);
+            }
+    double acc[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int k0 = 0; k0 < K; k0 += NP_BK) {
+        for (int idx = tid; idx < NP_BK * NP_BM; idx += 128) {
+            const int kk = idx / NP_BM, mm = idx % NP_BM;
+            const int gm = m0 + mm, gk = k0 + kk;
+            As[kk][mm] = (gm < M && gk < K) ? A[(size_t)gk * lda + gm] : 0.0;
+        }
+        for (int idx = tid; idx < NP_BN * NP_BK; idx += 128) {
+            const int nn = idx / NP_BK, kk = idx % NP_BK;
+            const int gn = n0 + nn, gk = k0 + kk;
+            Bs[nn][kk] = (gn < n && gk < K) ? B[(size_t)gn * ldb + gk] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < NP_BK; ks += 4) {
+            double af[2], bf[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) af[i] = As[ks + t][wm * 16 + i * 8 + g];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) bf[j] = Bs[wn * 16 + j * 8 + g][ks + t];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = m0 + wm * 16 + i * 8 + g;
+                const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
+                if (row < M && col < n) ep.store(row, col, acc[i][j][e], regs[i][j][e]);
+            }
+}
+
 // ---------------------------------------------------------------------------
 // Split-K TN GEMM with the K-split reduced through distributed shared memory.
 //   C(m x n, ld ldc) = alpha * A(:, m)^T B(:, n),  A: K x m (lda), B: K x n (ldb).
@@ -104,7 +173,7 @@ __device__ __forceinline__ void nn_tile(int M, int K, int n, const double* __res
 // barrier each rank sums a slice of the tile over all CS ranks IN RANK ORDER through
 // DSMEM.  No global partials, no atomics: the result depends only on (K, CS), not on n.
 // `hook(col)` runs once per output column (rank 0, m-tile 0) after the tile is final.
-constexpr int TC_BN = 32, TC_BK = 32, TC_PAD = 4;
+constexpr int TC_BN = 32, TC_BK = 32, TC_PAD = 4, TC_ST = 4;  // TC_ST-stage cp.async ring
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -123,7 +192,7 @@ struct NoHook {
 
 template <int BM>
 constexpr size_t tn_cluster_smem() {
-    return (size_t)2 * (BM + TC_BN) * (TC_BK + TC_PAD) * sizeof(double);
+    return (size_t)TC_ST * (BM + TC_BN) * (TC_BK + TC_PAD) * sizeof(double);
 }
 
 template <int BM, class Hook>
@@ -134,8 +203,8 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) double tsm[];
     constexpr int LD = TC_BK + TC_PAD;
-    double* As = tsm;                         // [2][BM][LD]
-    double* Bs = tsm + 2 * BM * LD;           // [2][BN][LD]
+    double* As = tsm;                         // [TC_ST][BM][LD]
+    double* Bs = tsm + TC_ST * BM * LD;       // [TC_ST][BN][LD]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp & 1, wn = warp >> 1;
@@ -171,15 +240,21 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
 #pragma unroll
         for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    if (nk > 0) load_stage(0, kb);
-    cp_async_commit();
-    for (int it = 0; it < nk; ++it) {
-        if (it + 1 < nk) load_stage((it + 1) & 1, kb + (it + 1) * TC_BK);
+    // TC_ST-stage ring: TC_ST - 1 stages in flight ahead of the one being multiplied (for the
+    // 1D configs the whole K chunk, <= 160 rows, is requested at once: one memory latency)
+#pragma unroll
+    for (int st = 0; st < TC_ST - 1; ++st) {
+        if (st < nk) load_stage(st, kb + st * TC_BK);
         cp_async_commit();
-        cp_async_wait<1>();
+    }
+    for (int it = 0; it < nk; ++it) {
+        const int nxt = it + TC_ST - 1;
+        if (nxt < nk) load_stage(nxt % TC_ST, kb + nxt * TC_BK);
+        cp_async_commit();
+        cp_async_wait<TC_ST - 1>();
         __syncthreads();
-        const double* as = As + (it & 1) * BM * LD;
-        const double* bs = Bs + (it & 1) * TC_BN * LD;
+        const double* as = As + (it % TC_ST) * BM * LD;
+        const double* bs = Bs + (it % TC_ST) * TC_BN * LD;
 #pragma unroll
         for (int ks = 0; ks < TC_BK; ks += 4) {
             double af[TI], bf[2];
@@ -247,6 +322,12 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
     if (m <= 32) {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
         cfg.dynamicSmemBytes = tn_cluster_smem<32>();
+        static bool attr32 = false;
+        if (!attr32) {
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)tn_cluster_smem<32>()));
+            attr32 = true;
+        }
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
     } else {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 64));

@@ -168,18 +168,18 @@ struct EpBeta {
 
 template <class Ep>
 __global__ void __launch_bounds__(128, 4) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
-                                                    const double* __restrict__ B, int ldb, Ep ep) {
+                                                       const double* __restrict__ B, int ldb, Ep ep) {
     // skip tiles whose columns are all inactive (uniform per CTA)
-    const int n0 = blockIdx.y * NN_BN;
+    const int n0 = blockIdx.y * NP_BN;
     __shared__ int any;
     if (threadIdx.x == 0) {
         int a = 0;
-        for (int c = n0; c < min(n, n0 + NN_BN); ++c) a |= ep.active[c];
+        for (int c = n0; c < min(n, n0 + NP_BN); ++c) a |= ep.active[c];
         any = a;
     }
     __syncthreads();
     if (!any) return;
-    nn_tile(M, K, n, A, lda, B, ldb, blockIdx.x * NN_BM, n0, ep);
+    nn_tile_pf(M, K, n, A, lda, B, ldb, blockIdx.x * NP_BM, n0, ep);
 }
 
 __global__ void k_count_active(const int* __restrict__ active, int n, int* __restrict__ out) {
@@ -264,7 +264,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         launched(ctx);
     }
     const double tol2 = tol * tol;
-    dim3 ugrid(cdiv(Ng, NN_BM), cdiv(n, NN_BN));
+    dim3 ugrid(cdiv(Ng, NP_BM), cdiv(n, NP_BN));
 
     auto precond_half = [&](int mode) {
         FopArgs f;
@@ -416,7 +416,7 @@ void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* 
                 launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, X, Ng, C, n_occ, NoHook{});
             } else {
                 EpBeta ep{X, Y, beta, active, Ng, 0};
-                dim3 ugrid(cdiv(Ng, NN_BM), cdiv(n, NN_BN));
+                dim3 ugrid(cdiv(Ng, NP_BM), cdiv(n, NP_BN));
                 k_pcg_update<EpBeta><<<ugrid, 128, 0, ctx->stream>>>(Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
                 launched(ctx);
             }

@@ -497,6 +497,248 @@ __global__ void __launch_bounds__(1024) k_qrcp_cluster(int m, int Ng, double* __
     cl.sync();  // peers may still be reading this CTA's buffers when it leaves the loop
 }
 
+// ---------------------------------------------------------------------------
+// Cluster QRCP with REGISTER-RESIDENT columns (problems with N_g/CS <= 16*CPW columns per CTA
+// and m <= 32*KR rows): the same algorithm, exchange and tie rules as k_qrcp_cluster, but each
+// CTA's columns never leave registers -- warp w owns local columns w, w+16, ..., lane l rows
+// l, l+32, ... -- so a pivot step moves no column data through shared memory: each lane reads
+// its KR entries of the Householder vector once per step and updates CPW columns in registers
+// (v is zero above row j, so rows < j are untouched without any masking).  512 threads.
+template <int CPW, int KR>
+__global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __restrict__ Ag, int kmax, double eps,
+                                                    int fixed, int* __restrict__ perm, double* __restrict__ rdiag,
+                                                    int* __restrict__ out_nmu, long long* __restrict__ tprof) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double rsm2[];
+    __shared__ QrSlot allslot[2][16];
+    __shared__ double allx0[2][16];   // row j of each peer's candidate (pushed with the slot)
+    __shared__ double s_wn2, s_x0;
+    __shared__ int s_pos, s_rank, s_col, s_lc;
+    const int CS = (int)cl.num_blocks(), b = (int)cl.block_rank(), tid = threadIdx.x;
+    const int lane = tid & 31, warp = uniform_warp();
+    constexpr int NW = 16;
+    const int cpb = (Ng + CS - 1) / CS;
+    const int c0 = b * cpb;
+    const int nc = max(0, min(Ng, c0 + cpb) - c0);
+    double* v = rsm2;                           // m (zero outside rows j..m-1)
+    double* pub = v + m;                        // 2 x m published candidate copies
+    double* n2 = pub + 2 * (size_t)m;           // cpb
+    int* pos = reinterpret_cast<int*>(n2 + cpb);
+    int* dn = pos + cpb;
+    double col[CPW][KR];
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+        const int lc = warp + NW * q;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const int row = lane + 32 * k;
+            col[q][k] = (lc < nc && row < m) ? Ag[(size_t)(c0 + lc) * m + row] : 0.0;
+        }
+        double sq = 0.0;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) sq += col[q][k] * col[q][k];
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0 && lc < nc) {
+            n2[lc] = sq;
+            pos[lc] = c0 + lc;
+            dn[lc] = 0;
+        }
+    }
+    for (int i = tid; i < m; i += blockDim.x) v[i] = 0.0;
+    __syncthreads();
+    double r11 = 0.0;
+    int N = kmax;
+    cl.sync();
+    for (int j = 0; j < kmax; ++j) {
+        const int buf = j & 1;
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j] = clock64();
+        if (warp == 0) {
+            double bn = -1.0;
+            int bp = 1 << 30, bl = -1;
+            for (int lc = lane; lc < nc; lc += 32) {
+                if (dn[lc]) continue;
+                const double xx = n2[lc];
+                if (xx > bn || (xx == bn && pos[lc] < bp)) {
+                    bn = xx;
+                    bp = pos[lc];
+                    bl = lc;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                if (on > bn || (on == bn && op < bp)) {
+                    bn = on;
+                    bp = op;
+                    bl = ol;
+                }
+            }
+            if (lane == 0) s_lc = bl;
+            if (lane < CS) {
+                QrSlot sl;
+                sl.n2 = bn;
+                sl.pos = bp;
+                sl.col = bl >= 0 ? c0 + bl : -1;
+                cl.map_shared_rank(&allslot[0][0], lane)[buf * 16 + b] = sl;
+            }
+        }
+        __syncthreads();
+        {   // the owning warp publishes the candidate's rows j..m-1 from its registers and
+            // pushes its row j to every peer next to the slot
+            const int bl = s_lc;
+            if (bl >= 0 && warp == bl % NW) {
+                const int qs = bl / NW;
+                double xj = 0.0;
+#pragma unroll
+                for (int q = 0; q < CPW; ++q)
+                    if (q == qs)
+#pragma unroll
+                        for (int k = 0; k < KR; ++k) {
+                            const int row = lane + 32 * k;
+                            if (row >= j && row < m) pub[(size_t)buf * m + row] = col[q][k];
+                            if (row == j) xj = col[q][k];
+                        }
+                xj = __shfl_sync(0xffffffffu, xj, j & 31);
+                if (lane < CS) cl.map_shared_rank(&allx0[0][0], lane)[buf * 16 + b] = xj;
+            }
+        }
+        cl.sync();
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 1] = clock64();
+        if (warp == 0) {
+            double bn = -1.0;
+            int bp = 1 << 30, bs = -1, bc = -1;
+            if (lane < CS) {
+                const QrSlot sl = allslot[buf][lane];
+                if (sl.col >= 0) {
+                    bn = sl.n2;
+                    bp = sl.pos;
+                    bs = lane;
+                    bc = sl.col;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+                if (on > bn || (on == bn && op < bp)) {
+                    bn = on;
+                    bp = op;
+                    bs = os;
+                    bc = oc;
+                }
+            }
+            if (lane == 0) {
+                s_wn2 = bn;
+                s_pos = bp;
+                s_rank = bs;
+                s_col = bc;
+                s_x0 = bs >= 0 ? allx0[buf][bs] : 0.0;
+            }
+        }
+        __syncthreads();
+        const double wn2 = s_wn2;
+        const int pw = s_pos, ws = s_rank, cw = s_col;
+        const double rjj = sqrt(fmax(wn2, 0.0));
+        if (j == 0) r11 = rjj;
+        if (__syncthreads_or(ws < 0 || rjj == 0.0 || (fixed <= 0 && rjj < eps * r11))) {
+            N = j;
+            break;
+        }
+        // winner's rows j..m-1 from its owner CTA (one DSMEM read per row, by one thread each)
+        const double* x = cl.map_shared_rank(pub, ws) + (size_t)buf * m;
+        const double x0 = s_x0;
+        const double alpha = (x0 >= 0.0) ? -rjj : rjj;
+        const double v0 = x0 - alpha;
+        const double tau = 2.0 / (wn2 - x0 * x0 + v0 * v0);
+        for (int i = j + tid; i < m; i += blockDim.x) v[i] = (i == j) ? v0 : x[i];
+        if (j > 0 && tid == 0) v[j - 1] = 0.0;  // rows < j stay zero (cleared as j advances)
+        if (b == 0 && tid == 0) rdiag[j] = rjj;
+        __syncthreads();
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 2] = clock64();
+        double vr[KR];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const int row = lane + 32 * k;
+            vr[k] = row < m ? v[row] : 0.0;
+        }
+        // all CPW columns of the warp at once (independent dot / shuffle / norm chains -> ILP)
+        bool live[CPW];
+        double d[CPW];
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) {
+            const int lc = warp + NW * q;
+            const bool valid = lc < nc;
+            const bool piv = __all_sync(0xffffffffu, valid && c0 + lc == cw);
+            live[q] = __all_sync(0xffffffffu, valid && !piv && dn[valid ? lc : 0] == 0);
+            if (piv) {
+#pragma unroll
+                for (int k = 0; k < KR; ++k) {
+                    const int row = lane + 32 * k;
+                    if (row == j) col[q][k] = alpha;
+                    else if (row > j) col[q][k] = 0.0;
+                }
+                if (lane == 0) {
+                    pos[lc] = j;
+                    dn[lc] = 1;
+                }
+            }
+            d[q] = 0.0;
+#pragma unroll
+            for (int k = 0; k < KR; ++k) d[q] += vr[k] * col[q][k];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int q = 0; q < CPW; ++q) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+        double nn[CPW];
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) {
+            nn[q] = 0.0;
+            if (live[q]) {
+                const double f = tau * d[q];
+#pragma unroll
+                for (int k = 0; k < KR; ++k) {
+                    const double y = col[q][k] - f * vr[k];
+                    col[q][k] = y;
+                    if (lane + 32 * k > j) nn[q] += y * y;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int q = 0; q < CPW; ++q) nn[q] += __shfl_xor_sync(0xffffffffu, nn[q], o);
+        if (lane == 0) {
+#pragma unroll
+            for (int q = 0; q < CPW; ++q) {
+                const int lc = warp + NW * q;
+                if (live[q]) {
+                    n2[lc] = nn[q];
+                    if (pos[lc] == j) pos[lc] = pw;
+                }
+            }
+        }
+        __syncthreads();
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 3] = clock64();
+    }
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+        const int lc = warp + NW * q;
+        if (lc < nc)
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int row = lane + 32 * k;
+                if (row < m) Ag[(size_t)(c0 + lc) * m + row] = col[q][k];
+            }
+    }
+    for (int lc = tid; lc < nc; lc += blockDim.x) perm[pos[lc]] = c0 + lc;
+    if (b == 0 && tid == 0) *out_nmu = N;
+    cl.sync();
+}
+
 // T = R11^{-1} R12 by column-oriented back substitution, one WARP per trailing column c:
 // lane l keeps b_nu for nu = l, l+32, ... in registers; for mu = N-1..0 the owner lane forms
 // x_mu = b_mu / R_mu,mu, broadcasts it, and every lane updates b_nu -= R_nu,mu x_mu (nu < mu)
@@ -667,7 +909,61 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
         }
     }
     if (getenv("ACP_QRCP_GRID") || m > 256) csq = 0;  // test knob / register-resident update needs m <= 256
-    if (csq > 0) {
+    // register-resident variant: (CPW, KR) = (8, 2) for m <= 64, (5, 8) for m <= 256
+    int rcs = 0, rkind = 0;
+    if (!getenv("ACP_QRCP_GRID") && !getenv("ACP_QRCP_SMEM")) {
+        if (m <= 64 && cdiv(Ng, 16 * 8) <= 16) {
+            rkind = 1;
+            rcs = std::max(1, cdiv(Ng, 16 * 8));
+        } else if (m <= 256 && cdiv(Ng, 16 * 5) <= 16) {
+            rkind = 2;
+            rcs = std::max(1, cdiv(Ng, 16 * 5));
+        }
+    }
+    if (rkind) {
+        auto kern = rkind == 1 ? k_qrcp_reg<8, 2> : k_qrcp_reg<5, 8>;
+        const int cpb = cdiv(Ng, rcs);
+        const size_t rsm = (3 * (size_t)m + cpb) * sizeof(double) + 2 * (size_t)cpb * sizeof(int);
+        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(rcs, 1, 1);
+        cfg.blockDim = dim3(512, 1, 1);
+        cfg.dynamicSmemBytes = rsm;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = rcs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        long long* tprof = nullptr;
+        const char* tpath = getenv("ACP_QR_PROFILE");
+        if (tpath) {
+            tprof = reinterpret_cast<long long*>(ctx->ws("qr_tprof", 8 * 512 * sizeof(long long)));
+            ACP_CUDA(cudaMemsetAsync(tprof, 0, 8 * 512 * sizeof(long long), ctx->stream));
+        }
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, m, Ng, A, kmax, id_eps, n_fixed, perm, rdiag, d_nmu, tprof));
+        launched(ctx);
+        if (tpath) {
+            std::vector<long long> h(8 * 512);
+            ACP_CUDA(cudaMemcpyAsync(h.data(), tprof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (FILE* f = fopen(tpath, "a")) {
+                for (int j = 0; j < 512 && h[8 * j]; ++j) {
+                    for (int k = 0; k < 5; ++k) fprintf(f, "%lld ", h[8 * j + k]);
+                    fprintf(f, "\n");
+                }
+                fclose(f);
+            }
+        }
+        csq = -1;  // done
+    }
+    if (csq == -1) {
+        // register-resident kernel already launched
+    } else if (csq > 0) {
         auto kern = m <= 64 ? k_qrcp_cluster<2> : m <= 128 ? k_qrcp_cluster<4> : k_qrcp_cluster<8>;
         ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
