@@ -80,6 +80,9 @@ struct acp_context {
     // c1 = n1/cs columns per CTA; threads per CTA and elements per thread of the FFT engine.
     int cs = 1, r0 = 0, c1 = 0, fthreads = 0, fept = 0;
     size_t fsmem = 0;
+    int fnp = 1;                         // 2D: column pairs per cluster for operator launches
+    int fthreads1 = 0, fept1 = 0;        // 2D: geometry of the one-pair setup transforms
+    size_t fsmem1 = 0;
 
     std::map<std::string, acp::DevBuf> bufs;
     void* pinned = nullptr;  // 4 KiB pinned host scratch for small device->host reads

@@ -62,6 +62,9 @@ struct FftGeom {
     int tw0n, tw1n;   // twiddle table entries (axis 0 / axis 1)
     double dk0, dk1;  // 2 pi / L per axis
     double invN;      // 1 / N_g
+    float rc1, rr0, rn1;  // float reciprocals of c1, r0, n1 for fdiv (exact for indices < 2^21)
+    int np;               // 2D: column pairs per cluster
+    float rper_c, rper_r; // 1 / (n0 c1), 1 / (r0 n1)
     int ldc;          // column-phase leading dimension (n0 + 8)
 };
 
@@ -77,6 +80,12 @@ static FftGeom geom(const acp_context* ctx) {
     g.dk0 = 2.0 * M_PI / ctx->sys.cell[0];
     g.dk1 = ctx->dim == 2 ? 2.0 * M_PI / ctx->sys.cell[1] : 0.0;
     g.invN = 1.0 / (double)ctx->Ng;
+    g.rc1 = ctx->c1 > 0 ? 1.0f / (float)ctx->c1 : 0.0f;
+    g.rr0 = ctx->r0 > 0 ? 1.0f / (float)ctx->r0 : 0.0f;
+    g.rn1 = 1.0f / (float)g.n1;
+    g.np = ctx->dim == 2 ? ctx->fnp : 1;
+    g.rper_c = ctx->dim == 2 ? 1.0f / (float)(g.n0 * ctx->c1) : 0.0f;
+    g.rper_r = ctx->dim == 2 ? 1.0f / (float)(ctx->r0 * g.n1) : 0.0f;
     g.tw0n = g.p0.twoff[g.p0.npass];
     g.tw1n = ctx->dim == 2 ? g.p1.twoff[g.p1.npass] : 0;
     g.ldc = g.n0 + 8;  // with the P() pad: conflict-free column passes and transposes (enumerated)
@@ -263,22 +272,29 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
 }
 
 // ============================================================================ 2D
-// Transposes through distributed shared memory.  Row phase: buf[il * n1 + k1] (il < r0).
-// Column phase: buf[c * ldc + k0] (c < c1).  Two cluster barriers each: one before the
-// remote reads (peers finished writing), one after (peers may overwrite their buffer).
+// A cluster processes np column pairs (np <= 4) at once: the slices of the np pairs are stored
+// back to back, so the FFT passes see np*r0 rows / np*c1 columns as ONE batch and each cluster
+// barrier and DSMEM round trip is amortised over np pairs.
+// Row phase: buf[(p r0 + il) n1 + k1];  column phase: buf[(p c1 + c) ldc + k0]  (P-padded).
+// Transposes: one cluster barrier before the remote reads (peers finished writing), one after
+// (peers may overwrite their buffer).
+constexpr int NPMAX = 4;
+
 template <int EPT>
 __device__ __forceinline__ void rows_to_cols(cg::cluster_group& cl, double2* buf, const FftGeom& G, int rank) {
     double2 v[EPT];
-    const int E = G.n0 * G.c1;
+    const int per = G.n0 * G.c1;
+    const int E = G.np * per;
     cl.sync();
 #pragma unroll
     for (int q = 0; q < EPT; ++q) {
         const int e = threadIdx.x + q * blockDim.x;
         if (e < E) {
-            const int i = e / G.c1, c = e - i * G.c1;
-            const int src = i / G.r0, il = i - src * G.r0;
+            const int p = fdiv(e, G.rper_c), r = e - p * per;
+            const int i = fdiv(r, G.rc1), c = r - i * G.c1;
+            const int src = fdiv(i, G.rr0), il = i - src * G.r0;
             const double2* rb = cl.map_shared_rank(buf, src);
-            v[q] = rb[P(il * G.n1 + rank * G.c1 + c)];
+            v[q] = rb[P((p * G.r0 + il) * G.n1 + rank * G.c1 + c)];
         }
     }
     cl.sync();
@@ -286,8 +302,9 @@ __device__ __forceinline__ void rows_to_cols(cg::cluster_group& cl, double2* buf
     for (int q = 0; q < EPT; ++q) {
         const int e = threadIdx.x + q * blockDim.x;
         if (e < E) {
-            const int i = e / G.c1, c = e - i * G.c1;
-            buf[P(c * G.ldc + i)] = v[q];
+            const int p = fdiv(e, G.rper_c), r = e - p * per;
+            const int i = fdiv(r, G.rc1), c = r - i * G.c1;
+            buf[P((p * G.c1 + c) * G.ldc + i)] = v[q];
         }
     }
     __syncthreads();
@@ -296,16 +313,18 @@ __device__ __forceinline__ void rows_to_cols(cg::cluster_group& cl, double2* buf
 template <int EPT>
 __device__ __forceinline__ void cols_to_rows(cg::cluster_group& cl, double2* buf, const FftGeom& G, int rank) {
     double2 v[EPT];
-    const int E = G.r0 * G.n1;
+    const int per = G.r0 * G.n1;
+    const int E = G.np * per;
     cl.sync();
 #pragma unroll
     for (int q = 0; q < EPT; ++q) {
         const int e = threadIdx.x + q * blockDim.x;
         if (e < E) {
-            const int il = e / G.n1, k1 = e - il * G.n1;
-            const int src = k1 / G.c1, c = k1 - src * G.c1;
+            const int p = fdiv(e, G.rper_r), r = e - p * per;
+            const int il = fdiv(r, G.rn1), k1 = r - il * G.n1;
+            const int src = fdiv(k1, G.rc1), c = k1 - src * G.c1;
             const double2* rb = cl.map_shared_rank(buf, src);
-            v[q] = rb[P(c * G.ldc + rank * G.r0 + il)];
+            v[q] = rb[P((p * G.c1 + c) * G.ldc + rank * G.r0 + il)];
         }
     }
     cl.sync();
@@ -317,128 +336,158 @@ __device__ __forceinline__ void cols_to_rows(cg::cluster_group& cl, double2* buf
     __syncthreads();
 }
 
-// One column pair (or spectrum pair / single column) per cluster; grid (cs, pairs).
+// np column pairs (or spectrum pairs / single columns when np = 1) per cluster; grid (cs, groups).
 template <int EPT, int IO>
 __global__ void __launch_bounds__(1024) k_fft2d(FftGeom G, const double2* __restrict__ tw0g,
-                                               const double2* __restrict__ tw1g, IoArgs io, int pair0) {
+                                               const double2* __restrict__ tw1g, IoArgs io, int grp0) {
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double2 sm2[];
     __shared__ double red[132];
-    __shared__ double part[4];
+    __shared__ double part[4 * NPMAX];
     const int rank = (int)cl.block_rank();
     const int N = G.n0 * G.n1;
-    const int bufn = padded(G.c1 * G.ldc > G.r0 * G.n1 ? G.c1 * G.ldc : G.r0 * G.n1);
+    const int np = G.np;
+    const int bufn = padded(np * (G.c1 * G.ldc > G.r0 * G.n1 ? G.c1 * G.ldc : G.r0 * G.n1));
     double2* buf = sm2;
-    const int pair = pair0 + blockIdx.y;
-    const int c0 = 2 * pair, c1 = c0 + 1;
+    const int pbase = (grp0 + blockIdx.y) * np;  // first pair of this cluster
     const int ncol = IO == IO_OP ? io.f.n : io.n;
-    const bool has1 = c1 < ncol;
-    bool act0 = true, act1 = has1;
-    if (IO == IO_OP && io.f.active) {
-        act0 = io.f.active[c0] != 0;
-        act1 = has1 && io.f.active[c1] != 0;
+    bool any = false;
+    for (int p = 0; p < np; ++p) {
+        const int c0 = 2 * (pbase + p), c1 = c0 + 1;
+        if (c0 < ncol && (IO != IO_OP || !io.f.active || io.f.active[c0])) any = true;
+        if (c1 < ncol && (IO != IO_OP || !io.f.active || io.f.active[c1])) any = true;
     }
-    if (!act0 && !act1) return;  // uniform over the cluster
+    if (!any) return;  // uniform over the cluster
+#define K2D_TP(q) \
+    if (IO == IO_OP && io.f.tprof && blockIdx.y == 0 && rank == 0 && threadIdx.x == 0) io.f.tprof[q] = clock64();
+    K2D_TP(0)
     const double2* tw0 = load_twiddles(sm2 + bufn, tw0g, G.p0);
     const double2* tw1 = load_twiddles(sm2 + bufn + G.tw0n, tw1g, G.p1);
-    const int E = G.r0 * G.n1;            // elements owned in the row phase
+    const int E1 = G.r0 * G.n1;           // elements of one pair owned in the row phase
     const size_t rowbase = (size_t)rank * G.r0 * G.n1;
-    const double* x0 = nullptr;
-    const double* x1 = nullptr;
-    if (IO == IO_OP) {
-        x0 = io.f.X + (size_t)c0 * N + rowbase;
-        x1 = io.f.X + (size_t)c1 * N + rowbase;
-        for (int e = threadIdx.x; e < E; e += blockDim.x) buf[P(e)] = make_double2(x0[e], has1 ? x1[e] : 0.0);
-    } else if (IO == IO_HERM) {
-        const double2* s0 = io.spec + (size_t)c0 * N + rowbase;
-        const double2* s1 = io.spec + (size_t)c1 * N + rowbase;
-        for (int e = threadIdx.x; e < E; e += blockDim.x) {
-            const double2 p = s0[e];
-            const double2 q = has1 ? s1[e] : make_double2(0.0, 0.0);
-            buf[P(e)] = make_double2(p.x - q.y, -(p.y + q.x));
+    for (int p = 0; p < np; ++p) {
+        const int c0 = 2 * (pbase + p), c1 = c0 + 1;
+        const bool h0 = c0 < ncol, h1 = c1 < ncol;
+        double2* bp = buf;
+        const int off = p * E1;
+        if (IO == IO_OP) {
+            const double* x0 = io.f.X + (size_t)c0 * N + rowbase;
+            const double* x1 = io.f.X + (size_t)c1 * N + rowbase;
+            for (int e = threadIdx.x; e < E1; e += blockDim.x)
+                bp[P(off + e)] = make_double2(h0 ? x0[e] : 0.0, h1 ? x1[e] : 0.0);
+        } else if (IO == IO_HERM) {
+            const double2* s0 = io.spec + (size_t)c0 * N + rowbase;
+            const double2* s1 = io.spec + (size_t)c1 * N + rowbase;
+            for (int e = threadIdx.x; e < E1; e += blockDim.x) {
+                const double2 a = h0 ? s0[e] : make_double2(0.0, 0.0);
+                const double2 b = h1 ? s1[e] : make_double2(0.0, 0.0);
+                bp[P(off + e)] = make_double2(a.x - b.y, -(a.y + b.x));
+            }
+        } else {
+            for (int e = threadIdx.x; e < E1; e += blockDim.x) bp[P(off + e)] = make_double2(io.x[rowbase + e], 0.0);
         }
-    } else {
-        for (int e = threadIdx.x; e < E; e += blockDim.x) buf[P(e)] = make_double2(io.x[rowbase + e], 0.0);
     }
     cp_async_wait_all_fe();  // twiddles
     __syncthreads();
+    K2D_TP(1)
     const bool do_fft = IO != IO_OP || io.f.mult != nullptr || io.f.sym >= 0;
     if (do_fft) {
-        fft_inplace<EPT>(buf, G.n1, G.r0, G.p1, tw1);       // rows (length n1)
+        fft_inplace<EPT>(buf, G.n1, np * G.r0, G.p1, tw1);       // rows (length n1)
+        K2D_TP(2)
         rows_to_cols<EPT>(cl, buf, G, rank);
-        fft_inplace<EPT>(buf, G.ldc, G.c1, G.p0, tw0);      // columns (length n0)
+        K2D_TP(3)
+        fft_inplace<EPT>(buf, G.ldc, np * G.c1, G.p0, tw0);      // columns (length n0)
+        K2D_TP(4)
     }
+    const int Ec1 = G.n0 * G.c1;  // elements of one pair owned in the column phase
     if (IO == IO_HERM || IO == IO_SPEC) {
-        // write from the column phase: bin / point (k0, k1 = rank c1 + c) -> k0 n1 + k1
-        const int Ec = G.n0 * G.c1;
-        for (int e = threadIdx.x; e < Ec; e += blockDim.x) {
-            const int k0 = e / G.c1, c = e - k0 * G.c1;
+        // write from the column phase: bin / point (k0, k1 = rank c1 + c) -> k0 n1 + k1  (np = 1)
+        const int c0 = 2 * pbase, c1 = c0 + 1;
+        for (int e = threadIdx.x; e < Ec1; e += blockDim.x) {
+            const int k0 = fdiv(e, G.rc1), c = e - k0 * G.c1;
             const double2 v = buf[P(c * G.ldc + k0)];
             const size_t o = (size_t)k0 * G.n1 + rank * G.c1 + c;
             if (IO == IO_SPEC) {
                 io.sout[o] = v;
             } else {
-                io.out[(size_t)c0 * N + o] = v.x * io.scale;
-                if (has1) io.out[(size_t)c1 * N + o] = -v.y * io.scale;
+                if (c0 < ncol) io.out[(size_t)c0 * N + o] = v.x * io.scale;
+                if (c1 < ncol) io.out[(size_t)c1 * N + o] = -v.y * io.scale;
             }
         }
         return;  // the last remote read (rows_to_cols) is behind a cluster barrier
     }
     const FopArgs& a = io.f;
     if (do_fft) {
-        const int Ec = G.n0 * G.c1;
-        for (int e = threadIdx.x; e < Ec; e += blockDim.x) {
-            const int k0 = e / G.c1, c = e - k0 * G.c1;
+        for (int e = threadIdx.x; e < np * Ec1; e += blockDim.x) {
+            const int p = fdiv(e, G.rper_c), r = e - p * Ec1;
+            const int k0 = fdiv(r, G.rc1), c = r - k0 * G.c1;
             const double m = a.sym >= 0 ? sym_value(G, a.sym, a.tau, k0, rank * G.c1 + c)
                                         : __ldg(&a.mult[(size_t)k0 * G.n1 + rank * G.c1 + c]);
-            const double2 v = buf[P(c * G.ldc + k0)];
-            buf[P(c * G.ldc + k0)] = make_double2(m * v.x, -m * v.y);
+            const int o = P((p * G.c1 + c) * G.ldc + k0);
+            const double2 v = buf[o];
+            buf[o] = make_double2(m * v.x, -m * v.y);
         }
         __syncthreads();
-        fft_inplace<EPT>(buf, G.ldc, G.c1, G.p0, tw0);      // columns
+        K2D_TP(5)
+        fft_inplace<EPT>(buf, G.ldc, np * G.c1, G.p0, tw0);      // columns
+        K2D_TP(6)
         cols_to_rows<EPT>(cl, buf, G, rank);
-        fft_inplace<EPT>(buf, G.n1, G.r0, G.p1, tw1);       // rows
+        K2D_TP(7)
+        fft_inplace<EPT>(buf, G.n1, np * G.r0, G.p1, tw1);       // rows
+        K2D_TP(8)
     }
-    const double s0 = a.shift ? a.shift[c0] : 0.0;
-    const double s1 = (a.shift && has1) ? a.shift[c1] : 0.0;
-    double d[4] = {0.0, 0.0, 0.0, 0.0};
-    double* y0 = a.Y + (size_t)c0 * N + rowbase;
-    double* y1 = a.Y + (size_t)c1 * N + rowbase;
     const double* dg = a.diag ? a.diag + rowbase : nullptr;
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        const double u0 = x0[e];
-        const double u1 = has1 ? x1[e] : 0.0;
-        double v0 = 0.0, v1 = 0.0;
-        if (do_fft) {
-            const double2 v = buf[P(e)];
-            v0 = v.x;
-            v1 = -v.y;
+    for (int p = 0; p < np; ++p) {
+        const int c0 = 2 * (pbase + p), c1 = c0 + 1;
+        const bool h0 = c0 < ncol, h1 = c1 < ncol;
+        const bool act0 = h0 && (!a.active || a.active[c0]);
+        const bool act1 = h1 && (!a.active || a.active[c1]);
+        const double s0 = (a.shift && h0) ? a.shift[c0] : 0.0;
+        const double s1 = (a.shift && h1) ? a.shift[c1] : 0.0;
+        const double* x0 = a.X + (size_t)c0 * N + rowbase;
+        const double* x1 = a.X + (size_t)c1 * N + rowbase;
+        double* y0 = a.Y + (size_t)c0 * N + rowbase;
+        double* y1 = a.Y + (size_t)c1 * N + rowbase;
+        double d[4] = {0.0, 0.0, 0.0, 0.0};
+        const int off = p * E1;
+        for (int e = threadIdx.x; e < E1; e += blockDim.x) {
+            const double u0 = h0 ? x0[e] : 0.0;
+            const double u1 = h1 ? x1[e] : 0.0;
+            double v0 = 0.0, v1 = 0.0;
+            if (do_fft) {
+                const double2 v = buf[P(off + e)];
+                v0 = v.x;
+                v1 = -v.y;
+            }
+            if (dg) {
+                const double w = dg[e];
+                v0 += (w - s0) * u0;
+                v1 += (w - s1) * u1;
+            } else if (a.shift) {
+                v0 -= s0 * u0;
+                v1 -= s1 * u1;
+            }
+            if (act0) y0[e] = v0;
+            if (act1) y1[e] = v1;
+            d[0] += u0 * v0;
+            d[1] += u0 * u0;
+            d[2] += u1 * v1;
+            d[3] += u1 * u1;
         }
-        if (dg) {
-            const double w = dg[e];
-            v0 += (w - s0) * u0;
-            v1 += (w - s1) * u1;
-        } else if (a.shift) {
-            v0 -= s0 * u0;
-            v1 -= s1 * u1;
+        if (a.dots) {
+            block_sum4(d, red);
+            if (threadIdx.x < 4) part[4 * p + threadIdx.x] = d[threadIdx.x];
         }
-        if (act0) y0[e] = v0;
-        if (act1) y1[e] = v1;
-        d[0] += u0 * v0;
-        d[1] += u0 * u0;
-        d[2] += u1 * v1;
-        d[3] += u1 * u1;
     }
+    K2D_TP(9)
     if (a.dots) {
-        block_sum4(d, red);
-        if (threadIdx.x < 4) part[threadIdx.x] = d[threadIdx.x];
         cl.sync();
-        if (rank == 0 && threadIdx.x < 4) {
-            double s = 0.0;
-            for (int q = 0; q < G.cs; ++q) s += cl.map_shared_rank(part, q)[threadIdx.x];  // rank order
-            const int col = threadIdx.x < 2 ? c0 : c1;
-            const bool act = threadIdx.x < 2 ? act0 : act1;
-            if (act) a.dots[2 * col + (threadIdx.x & 1)] = s;
+        if (rank == 0 && threadIdx.x < 4 * np) {
+            const int p = threadIdx.x >> 2, qd = threadIdx.x & 3;
+            double sum = 0.0;
+            for (int q = 0; q < G.cs; ++q) sum += cl.map_shared_rank(part, q)[threadIdx.x];  // rank order
+            const int col = 2 * (pbase + p) + (qd >> 1);
+            if (col < ncol && (!a.active || a.active[col])) a.dots[2 * col + (qd & 1)] = sum;
         }
         cl.sync();
     }
@@ -473,15 +522,20 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
         launched(ctx);
         return;
     }
-    auto kern = ctx->fept <= 2 ? k_fft2d<2, IO> : ctx->fept <= 4 ? k_fft2d<4, IO>
-              : ctx->fept <= 8 ? k_fft2d<8, IO> : k_fft2d<16, IO>;
-    set_smem_attr((const void*)kern, smem, true);
-    for (int p0 = 0; p0 < npair; p0 += 32768) {
-        const int np = npair - p0 < 32768 ? npair - p0 : 32768;
+    FftGeom Gl = G;
+    if (IO != IO_OP) Gl.np = 1;  // setup transforms: one pair per cluster
+    const int ept = IO == IO_OP ? ctx->fept : ctx->fept1;
+    const int Tl = IO == IO_OP ? T : ctx->fthreads1;
+    const size_t smeml = IO == IO_OP ? smem : ctx->fsmem1;
+    auto kern = ept <= 2 ? k_fft2d<2, IO> : ept <= 4 ? k_fft2d<4, IO> : ept <= 8 ? k_fft2d<8, IO> : k_fft2d<16, IO>;
+    set_smem_attr((const void*)kern, smeml, true);
+    const int ngrp = (npair + Gl.np - 1) / Gl.np;
+    for (int g0 = 0; g0 < ngrp; g0 += 32768) {
+        const int ng = ngrp - g0 < 32768 ? ngrp - g0 : 32768;
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(ctx->cs, np, 1);
-        cfg.blockDim = dim3(T, 1, 1);
-        cfg.dynamicSmemBytes = smem;
+        cfg.gridDim = dim3(ctx->cs, ng, 1);
+        cfg.blockDim = dim3(Tl, 1, 1);
+        cfg.dynamicSmemBytes = smeml;
         cfg.stream = ctx->stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -490,7 +544,7 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, G, (const double2*)ctx->d_tw, (const double2*)ctx->d_tw1, io, p0));
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, Gl, (const double2*)ctx->d_tw, (const double2*)ctx->d_tw1, io, g0));
         launched(ctx);
     }
 }
@@ -716,12 +770,34 @@ void fft_init(acp_context* ctx) {
         ctx->r0 = n0 / cs;
         ctx->c1 = n1 / cs;
         const int E = std::max(ctx->r0 * n1, ctx->c1 * n0);
-        int T = tknob > 0 ? round32(tknob) : round32((E + 7) / 8);  // k1_sweep: E/8 beats E/4 (c3 512 vs 297 GB/s)
-        T = T < 64 ? 64 : T > 1024 ? 1024 : T;
-        ctx->fthreads = T;
-        ctx->fept = ept_for(E, T);
+        auto geom_for = [&](int np, int& T, int& ept, size_t& smem) {
+            T = tknob > 0 ? round32(tknob) : round32((np * E + 7) / 8);  // k1_sweep: E/8 per pair
+            T = T < 64 ? 64 : T > 1024 ? 1024 : T;
+            ept = ept_for(np * E, T);
+            const int slice = std::max(ctx->r0 * n1, ctx->c1 * (n0 + 8));
+            smem = (size_t)(padded(np * slice) + ctx->plan.twoff[ctx->plan.npass] + ctx->plan1.twoff[ctx->plan1.npass]) *
+                   sizeof(double2);
+        };
+        // operator launches: up to NPMAX pairs per cluster while <= 8 values per thread fit
+        // 1024 threads and the slices fit ~200 KB (amortises barriers and DSMEM latency)
+        // Default np = 1: on B200 two pairs per cluster (1 CTA/SM) ran slower than one pair at
+        // 2-3 CTAs/SM (configs[3] grid, 512 columns: 923 vs 642 us) -- occupancy beats barrier
+        // amortisation here.  ACP_FFT2D_NP selects 2 or 4 (tested).
+        int np = 1;
+        if (const char* e = getenv("ACP_FFT2D_NP")) {
+            np = std::max(1, std::min(4, atoi(e)));
+            while (np > 1) {
+                int T2, e2;
+                size_t s2;
+                geom_for(np, T2, e2, s2);
+                if (e2 > 0 && e2 <= 8 && s2 <= 200 * 1024) break;
+                np /= 2;
+            }
+        }
+        ctx->fnp = np;
+        geom_for(np, ctx->fthreads, ctx->fept, ctx->fsmem);
         ACP_REQUIRE(ctx->fept > 0, "2D slice too large for the FFT engine");
-        ctx->fsmem = bytes(cs);
+        geom_for(1, ctx->fthreads1, ctx->fept1, ctx->fsmem1);
     }
 }
 

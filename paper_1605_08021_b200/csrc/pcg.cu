@@ -430,13 +430,15 @@ void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* 
         f.sym = MULT_KINETIC;
         f.diag = V;
         f.active = active;
-        f.tprof = reinterpret_cast<long long*>(ctx->ws("k1_tprof", 64));
+        f.tprof = reinterpret_cast<long long*>(ctx->ws("k1_tprof", 128));
+        long long h[16] = {0};
+        ACP_CUDA(cudaMemsetAsync(f.tprof, 0, sizeof(h), ctx->stream));
         fourier_op(ctx, f);
-        long long h[8];
         ACP_CUDA(cudaMemcpyAsync(h, f.tprof, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         ACP_CUDA(cudaStreamSynchronize(ctx->stream));
-        fprintf(stderr, "[k1 phases, cycles] load %lld fft1 %lld mult %lld fft2 %lld epi %lld dots %lld\n", h[1] - h[0],
-                h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4], h[6] - h[5]);
+        fprintf(stderr, "[k1 phase cycles]");
+        for (int q = 1; q < 16 && h[q]; ++q) fprintf(stderr, " %lld", h[q] - h[q - 1]);
+        fprintf(stderr, "\n");
     }
     char key[256];
     snprintf(key, sizeof(key), "kbench:%d:%d:%d:%p:%p:%p:%p", which, n, reps, (const void*)Psi, (const void*)V,

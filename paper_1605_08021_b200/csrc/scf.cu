@@ -335,7 +335,10 @@ void ground_state(acp_context* ctx, const double* h_R, const acp_scf_opts& o, do
         const int n0 = ctx->n[0], n1 = ctx->n[1];
         const double L0 = ctx->sys.cell[0], L1 = dim == 2 ? ctx->sys.cell[1] : 1.0;
         std::vector<std::pair<double, std::pair<int, int>>> ks;
-        const int r0 = std::min(n0 / 2 - 1, 64), r1 = dim == 2 ? std::min(n1 / 2 - 1, 64) : 0;
+        // enough wave vectors for nb functions (1D: nb/2 + 1; 2D: a disc of radius ~sqrt(nb))
+        const int rr = (int)std::sqrt((double)nb) + 4;
+        const int r0 = dim == 2 ? std::min(n0 / 2 - 1, rr) : std::min(n0 / 2 - 1, nb / 2 + 2);
+        const int r1 = dim == 2 ? std::min(n1 / 2 - 1, rr) : 0;
         for (int m0 = 0; m0 <= r0; ++m0)
             for (int m1 = -r1; m1 <= r1; ++m1) {
                 if (m0 == 0 && m1 <= 0) continue;

@@ -111,7 +111,9 @@ def test_ground_state_full_size_properties(name):
     assert res.max() < 1e-8
     assert rel(rho, m.f * np.sum(Psi * Psi, axis=1)) < 1e-12
     V_o = m.yukawa(rho + m.pseudocharge())                     # V = K * (rho + m), Eq. effV
-    assert rel(V, V_o) < 1e-8  # K^ amplifies the 1e-12 SCF residual by up to ~1e3 at the smallest k
+    # V is built from the last INPUT density; K^ amplifies the SCF residual by up to ~1e4-1e5 at
+    # the smallest k (configs[2]: 4 pi / (eps0 ((2 pi/768)^2 + kappa^2)) ~ 7.5e3; observed 2.5e4)
+    assert rel(V, V_o) < max(1e-8, 1e5 * gs["residual"])
     assert gs["gap"] > 0.0
     assert rel(gs["G"].cpu().numpy().T, m.G_matrix()) < 1e-12
     ctx.close()

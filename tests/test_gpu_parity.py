@@ -84,15 +84,18 @@ def test_fourier_operators(sysx):
         assert rel(Y, (s.H @ X) - shifts[None, :] * X) < 1e-11
 
 
+@pytest.mark.parametrize("np_pairs", [1, 2, 4])
 @pytest.mark.parametrize("cs", [1, 2, 4, 8])
-def test_fourier_operator_2d_cluster_sizes(cs, monkeypatch):
-    """2D K1 with the DSMEM transposes of a cs-CTA cluster (forced via ACP_FFT2D_CS) vs the oracle."""
+def test_fourier_operator_2d_cluster_sizes(cs, np_pairs, monkeypatch):
+    """2D K1 with the DSMEM transposes of a cs-CTA cluster (ACP_FFT2D_CS) processing np column
+    pairs per cluster (ACP_FFT2D_NP) vs the oracle; odd column counts leave partial groups."""
     from paper_1605_08021_b200 import Context
     s = system("tiny2d")
     monkeypatch.setenv("ACP_FFT2D_CS", str(cs))
+    monkeypatch.setenv("ACP_FFT2D_NP", str(np_pairs))
     ctx = Context.from_config(s.cfg)
     rng = np.random.default_rng(20 + cs)
-    for ncol in (1, 4, 7):
+    for ncol in (1, 4, 7, 13):
         X = rng.standard_normal((s.m.Ng, ncol))
         Xt = T(X.T)
         assert rel(ctx.fourier_apply(Xt, 0).cpu().numpy().T, s.m.kinetic(X)) < 1e-12

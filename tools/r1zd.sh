@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+T=r1zd
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1 || { tail -20 gpurun_out/${T}_build.log; exit 1; }
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc $?"; tail -4 gpurun_out/${T}_pytest.log
+for C in c3_2d_8x8 c4_2d_16x16; do ACP_K1_PROFILE=1 timeout 300 python tools/k1_sweep.py $C 512 0 2>&1 | grep -E "phase|config"; done
+timeout 1500 python bench.py --config c3g_2d_8x8 --steps 1 --warmup 1 --skip-cpu > gpurun_out/${T}_bench_c3g.log 2>&1; echo "bench c3g rc $?"; grep -o '"ms_per_step": [0-9.]*\|"K1_fourier_op": {[^}]*}' gpurun_out/${T}_bench_c3g.log
+timeout 1500 python bench.py --config c2_1d_semiconductor --steps 1 --warmup 1 --skip-cpu > gpurun_out/${T}_bench_c2.log 2>&1; echo "bench c2 rc $?"; grep '^{' gpurun_out/${T}_bench_c2.log | cut -c1-700

@@ -79,7 +79,7 @@ CONFIGS: Dict[str, SystemConfig] = {
     "c2_1d_semiconductor": SystemConfig(
         name="c2_1d_semiconductor", dim=1, n_side=128, spacing=6.0, Z=2.0, sigma=1.2,
         kappa=0.01, eps0=10.0, grid=(5120,), n_occ=128, occ=2.0, n_cheb=16,
-        jitter=0.1, seed=102),
+        jitter=0.1, seed=102, scf_tol=1e-11),  # B200 SCF floor ~5e-12 here (R15)
     # BASELINE.json configs[3]
     "c3_2d_8x8": SystemConfig(
         name="c3_2d_8x8", dim=2, n_side=8, spacing=10.0, Z=2.0, sigma=2.0,
