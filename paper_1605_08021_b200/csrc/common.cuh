@@ -238,6 +238,8 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols,
 void lu_solve(acp_context* ctx, double* A, int n, double* B, int nrhs);
 // Same for [A | B] stored as ONE n x (n + nrhs) column-major array (multi-kernel blocked LU, any n).
 void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs);
+// U X = B for upper-triangular U stored as the first n columns of AB (n x (n + nrhs), ld n).
+void upper_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs);
 // Symmetric eigenvalues (and optionally vectors) of A (n x n col-major, destroyed) by Jacobi.
 void sym_eig(acp_context* ctx, double* A, int n, double* w, double* V);
 // Cholesky A = L L^T in place (lower), returns false if not SPD.

@@ -337,7 +337,8 @@ __global__ void __launch_bounds__(256) k_lu_trsm12(double* __restrict__ AB, int 
 
 // X_b = U_bb^{-1} B_b for the rows [q0, q0 + qb) (qb <= 32): one warp per right-hand side, the
 // diagonal block of U staged in shared memory with reciprocal diagonal.
-__global__ void __launch_bounds__(256) k_lu_bsub(double* __restrict__ AB, int n, int nrhs, int q0, int qb) {
+__global__ void __launch_bounds__(256) k_lu_bsub(double* __restrict__ AB, int n, int nrhs, int q0, int qb,
+                                                 int r0) {
     __shared__ double Us[32][33];
     __shared__ double rd[32];
     for (int e = threadIdx.x; e < qb * qb; e += blockDim.x) {
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(256) k_lu_bsub(double* __restrict__ AB, int n,
     const int w = blockIdx.x * (blockDim.x >> 5) + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     if (w >= nrhs) return;
-    double* bj = AB + (size_t)(n + w) * n + q0;
+    double* bj = AB + (size_t)(n + r0 + w) * n + q0;
     double x = lane < qb ? bj[lane] : 0.0;
     for (int k = qb - 1; k >= 0; --k) {
         const double xk = __shfl_sync(0xffffffffu, x, k) * rd[k];
@@ -358,6 +359,22 @@ __global__ void __launch_bounds__(256) k_lu_bsub(double* __restrict__ AB, int n,
         if (lane < k) x -= Us[k][lane] * xk;
     }
     if (lane < qb) bj[lane] = x;
+}
+
+// U X = B in place for upper-triangular U (first n columns of AB, n x (n + nrhs), ld n): 32-row
+// blocks from the bottom, k_lu_bsub (warp per right-hand side) + DMMA gemm_nn for the rows above.
+void upper_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
+    for (int q1 = n; q1 > 0; q1 -= 32) {
+        const int q0 = std::max(0, q1 - 32);
+        for (int r0 = 0; r0 < nrhs; r0 += 65535 * 8) {  // grid.x limit
+            const int nr = std::min(nrhs - r0, 65535 * 8);
+            k_lu_bsub<<<cdiv((long long)nr * 32, 256), 256, 0, ctx->stream>>>(AB, n, nr, q0, q1 - q0, r0);
+            launched(ctx);
+        }
+        if (q0 > 0)
+            gemm_nn(ctx, q0, q1 - q0, nrhs, -1.0, AB + (size_t)q0 * n, n, AB + (size_t)n * n + q0, n, 1.0,
+                    AB + (size_t)n * n, n);
+    }
 }
 
 // Solve A X = B in place; AB is n x (n + nrhs) column-major ([A | B], ld n).
@@ -389,14 +406,7 @@ void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
             gemm_nn(ctx, n - r0, pw, ntot - r0, -1.0, AB + (size_t)p0 * n + r0, n, AB + (size_t)r0 * n + p0, n, 1.0,
                     AB + (size_t)r0 * n + r0, n);
     }
-    for (int q1 = n; q1 > 0; q1 -= 32) {
-        const int q0 = std::max(0, q1 - 32);
-        k_lu_bsub<<<cdiv((long long)nrhs * 32, 256), 256, 0, ctx->stream>>>(AB, n, nrhs, q0, q1 - q0);
-        launched(ctx);
-        if (q0 > 0)
-            gemm_nn(ctx, q0, q1 - q0, nrhs, -1.0, AB + (size_t)q0 * n, n, AB + (size_t)n * n + q0, n, 1.0,
-                    AB + (size_t)n * n, n);
-    }
+    upper_solve_blocked(ctx, AB, n, nrhs);
     int* hp = static_cast<int*>(ctx->pinned);
     ACP_CUDA(cudaMemcpyAsync(hp, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ACP_CUDA(cudaStreamSynchronize(ctx->stream));

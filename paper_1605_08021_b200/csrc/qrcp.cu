@@ -739,45 +739,11 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
     cl.sync();
 }
 
-// T = R11^{-1} R12 by column-oriented back substitution, one WARP per trailing column c:
-// lane l keeps b_nu for nu = l, l+32, ... in registers; for mu = N-1..0 the owner lane forms
-// x_mu = b_mu / R_mu,mu, broadcasts it, and every lane updates b_nu -= R_nu,mu x_mu (nu < mu)
-// reading column mu of R (contiguous, shared by all warps through L1/L2).  T row-major (mu, c').
-template <int SLOTS>
-__global__ void __launch_bounds__(256) k_trsm_warp(int m, int Ng, int N, const double* __restrict__ A,
-                                                   const int* __restrict__ perm, double* __restrict__ T) {
-    const int wglob = blockIdx.x * (blockDim.x >> 5) + uniform_warp();
-    const int l = threadIdx.x & 31;
-    const int c = N + wglob;
-    if (c >= Ng) return;
-    const int nc = Ng - N, cc = c - N;
-    double b[SLOTS];
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-        const int nu = s * 32 + l;
-        b[s] = (nu < N) ? A[(size_t)perm[c] * m + nu] : 0.0;
-    }
-    for (int mu = N - 1; mu >= 0; --mu) {
-        const int owner = mu & 31, slot = mu >> 5;
-        double bm = 0.0;
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s)
-            if (s == slot) bm = b[s];
-        const double* rcol = A + (size_t)perm[mu] * m;
-        double x = bm / rcol[mu];
-        x = __shfl_sync(0xffffffffu, x, owner);
-        if (l == owner) T[(size_t)mu * nc + cc] = x;
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s) {
-            const int nu = s * 32 + l;
-            if (nu < mu) b[s] -= rcol[nu] * x;
-        }
-    }
-}
-
-// Same back substitution with R11 staged in shared memory (one CTA per SM, 32 warps, columns
-// strided over the grid) and the reciprocals of its diagonal precomputed: the per-column chain
-// then runs on shared-memory latency instead of L2 latency.  Used when N^2 doubles fit.
+// T = R11^{-1} R12 by column-oriented back substitution, one WARP per trailing column c (lane l
+// keeps b_nu for nu = l, l+32, ... in registers), with R11 staged in shared memory (one CTA per
+// SM, 32 warps, columns strided over the grid) and the reciprocals of its diagonal precomputed,
+// so the per-column chain runs on shared-memory latency.  Used when N^2 doubles fit (N <= 160);
+// larger N go through the blocked solve below.
 template <int SLOTS>
 __global__ void __launch_bounds__(1024) k_trsm_smem(int m, int Ng, int N, const double* __restrict__ A,
                                                    const int* __restrict__ perm, double* __restrict__ T) {
@@ -820,8 +786,21 @@ __global__ void __launch_bounds__(1024) k_trsm_smem(int m, int Ng, int N, const 
     }
 }
 
-static void trsm_cols(acp_context* ctx, int m, int Ng, int N, const double* A, const int* perm, double* T) {
+// [R11 | R12] gathered contiguously (N x Ng, ld N; R11 upper triangle only) for the blocked solve.
+__global__ void k_gather_R(int m, int Ng, int N, const double* __restrict__ A, const int* __restrict__ perm,
+                           double* __restrict__ AB) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y + gridDim.y * blockIdx.z;
+    if (i >= N || j >= Ng) return;
+    AB[(size_t)j * N + i] = (j >= N || i <= j) ? A[(size_t)perm[j] * m + i] : 0.0;
+}
+
+// T = R11^{-1} R12.  Returns the strides of T(mu, c'): element at T[mu * tsm + c' * tsc].
+static void trsm_cols(acp_context* ctx, int m, int Ng, int N, const double* A, const int* perm, double*& T,
+                      size_t& tsm, size_t& tsc) {
     const int warps = Ng - N;
+    tsm = (size_t)(Ng - N > 0 ? Ng - N : 1);
+    tsc = 1;
     if (warps <= 0) return;
     const size_t smem = ((size_t)N * N + N) * sizeof(double);
     if (smem <= 200 * 1024) {
@@ -838,25 +817,28 @@ static void trsm_cols(acp_context* ctx, int m, int Ng, int N, const double* A, c
         launched(ctx);
         return;
     }
-    const int blocks = cdiv((long long)warps * 32, 256);
-    if (N <= 128) k_trsm_warp<4><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
-    else if (N <= 256) k_trsm_warp<8><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
-    else if (N <= 512) k_trsm_warp<16><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
-    else if (N <= 1024) k_trsm_warp<32><<<blocks, 256, 0, ctx->stream>>>(m, Ng, N, A, perm, T);
-    else throw Error(ACP_ERR_UNSUPPORTED, "N_mu > 1024 is not supported by the TRSM kernel");
+    // N > 160: gather [R11 | R12] and run the blocked upper-triangular solve (bsub + DMMA GEMM);
+    // T is then column-major N x (Ng - N) inside the gathered array.
+    double* AB = ctx->wsd("qr_RAB", (size_t)N * Ng);
+    const int gz = cdiv(Ng, 65535);
+    k_gather_R<<<dim3(cdiv(N, 128), cdiv(Ng, gz), gz), 128, 0, ctx->stream>>>(m, Ng, N, A, perm, AB);
     launched(ctx);
+    upper_solve_blocked(ctx, AB, N, Ng - N);
+    T = AB + (size_t)N * N;
+    tsm = 1;
+    tsc = (size_t)N;
 }
 
-// Xi[perm[c], mu] = T[mu, c - N] (c >= N) or delta_{c mu} (c < N);  S[mu] = perm[mu].
-__global__ void k_scatter_xi(int Ng, int N, const int* __restrict__ perm, const double* __restrict__ T,
-                             double* __restrict__ Xi, int* __restrict__ S) {
+// Xi[perm[c], mu] = T(mu, c - N) (c >= N) or delta_{c mu} (c < N);  S[mu] = perm[mu].
+__global__ void k_scatter_xi(int Ng, int N, const int* __restrict__ perm, const double* __restrict__ T, size_t tsm,
+                             size_t tsc, double* __restrict__ Xi, int* __restrict__ S) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int mu = blockIdx.y;
     if (c >= Ng) return;
     const int row = perm[c];
     double v;
     if (c < N) v = (c == mu) ? 1.0 : 0.0;
-    else v = T[(size_t)mu * (Ng - N) + (c - N)];
+    else v = T[(size_t)mu * tsm + (size_t)(c - N) * tsc];
     Xi[(size_t)mu * Ng + row] = v;
     if (c == 0) S[mu] = perm[mu];
 }
@@ -1029,8 +1011,9 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
         throw Error(ACP_ERR_INVALID, "N_mu = " + std::to_string(N) + " exceeds n_mu_max = " + std::to_string(n_mu_max));
     // Xi
     double* T = ctx->wsd("qr_T", (size_t)N * (Ng - N > 0 ? Ng - N : 1));
-    trsm_cols(ctx, m, Ng, N, A, perm, T);
-    k_scatter_xi<<<dim3(cdiv(Ng, 256), N), 256, 0, ctx->stream>>>(Ng, N, perm, T, Xi, S);
+    size_t tsm = 0, tsc = 0;
+    trsm_cols(ctx, m, Ng, N, A, perm, T, tsm, tsc);
+    k_scatter_xi<<<dim3(cdiv(Ng, 256), N), 256, 0, ctx->stream>>>(Ng, N, perm, T, tsm, tsc, Xi, S);
     launched(ctx);
     return N;
 }

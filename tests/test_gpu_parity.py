@@ -273,6 +273,41 @@ def test_ground_state(sysx):
     assert np.abs(s.m.dV * Psi.T @ Psi - np.eye(n)).max() < 1e-10
 
 
+@pytest.mark.slow
+def test_compress_large_nmu_blocked_trsm():
+    """configs[1] with a fixed N_mu = 200 > 160: the interpolation vectors go through the blocked
+    upper-triangular solve (gathered [R11 | R12], bsub + DMMA GEMM)."""
+    s = system("c1_1d_insulator")
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, 0.0, n_fixed=200)
+    S_g, Xi_g, n = s.ctx.compress(s.Psi_t, s.G_t, th, nu, n_mu_fixed=200)
+    assert n == 200 and np.array_equal(S_g.cpu().numpy(), S_o)
+    assert rel(Xi_g.cpu().numpy().T, Xi_o) < 1e-8
+
+
+def test_apply_chi0_empty_shard(sysx):
+    """An empty mu-range (a rank with no columns) is a no-op that leaves W untouched."""
+    s = sysx
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    W = torch.full((len(S_o), s.m.Ng), 7.0, dtype=torch.float64, device="cuda")
+    _, info = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, T(S_o, torch.int32), T(Xi_o.T), s.cfg.n_cheb,
+                               mu_range=(1, 1), W=W)
+    assert info["n_solved"] == 0 and bool(torch.all(W == 7.0))
+
+
+def test_compress_capacity_error(sysx):
+    """N_mu larger than the caller's capacity is reported (ACP_ERR_INVALID), not truncated."""
+    from paper_1605_08021_b200 import AcpError
+    s = sysx
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, _, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    if len(S_o) < 2:
+        pytest.skip("needs N_mu >= 2")
+    with pytest.raises(AcpError):
+        s.ctx.compress(s.Psi_t, s.G_t, th, nu, id_eps=s.cfg.id_eps, n_mu_max=len(S_o) - 1)
+
+
 # ---------------------------------------------------------------- full size (bench config)
 @pytest.mark.slow
 def test_bench_config_end_to_end():
