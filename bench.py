@@ -286,6 +286,11 @@ def run_acp(args, cfg):
             byts = 24.0 * Ng * ncols
             kern[name] = dict(bound="hbm", us=us, bytes=byts, achieved=byts / us / 1e3, unit="GB/s",
                               peak=peaks["hbm_gbs"])
+            # the same launch as an FP64 DMMA GEMM (Psi C, 2 N_g N_occ flops per column): the bound
+            # once N_occ >= 64 (configs[2..4])
+            fl = 2.0 * Ng * No * ncols
+            kern[name]["tensor"] = dict(flops=fl, achieved=fl / us / 1e6, unit="TFLOP/s", peak=peaks["fp64_tflops"],
+                                        frac=fl / us / 1e6 / peaks["fp64_tflops"])
         kern[name]["frac"] = kern[name]["achieved"] / kern[name]["peak"]
     dom_name = os.environ.get("ACP_DOMINANT_KERNEL", "K1_fourier_op")
     dom = kern[dom_name]

@@ -119,10 +119,27 @@ __global__ void __launch_bounds__(128) k_gemm_nn(int M, int K, int n, const doub
     nn_tile(M, K, n, A, lda, B, ldb, blockIdx.x * NN_BM, blockIdx.y * NN_BN, ep);
 }
 
+__global__ void __launch_bounds__(256) k_gemm_nn_big(int M, int K, int n, const double* __restrict__ A, int lda,
+                                                     const double* __restrict__ B, int ldb, EpAxpby ep) {
+    nn_tile_big(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, blockIdx.y * GB_BN, ep);
+}
+
 void gemm_nn(acp_context* ctx, int M, int K, int n, double alpha, const double* A, int lda, const double* B,
              int ldb, double beta, double* C, int ldc) {
     if (M <= 0 || n <= 0) return;
     EpAxpby ep{alpha, beta, C, ldc};
+    if (K >= 64) {  // genuine GEMM (SMW products at large N_mu): 64 x 64 multistage tiles
+        static bool attr = false;
+        if (!attr) {
+            ACP_CUDA(cudaFuncSetAttribute(k_gemm_nn_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)nn_big_smem()));
+            attr = true;
+        }
+        k_gemm_nn_big<<<dim3(cdiv(M, GB_BM), cdiv(n, GB_BN)), 256, nn_big_smem(), ctx->stream>>>(M, K, n, A, lda, B,
+                                                                                                 ldb, ep);
+        launched(ctx);
+        return;
+    }
     dim3 grid(cdiv(M, NN_BM), cdiv(n, NN_BN));
     k_gemm_nn<<<grid, 128, 0, ctx->stream>>>(M, K, n, A, lda, B, ldb, ep);
     launched(ctx);

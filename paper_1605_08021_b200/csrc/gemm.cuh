@@ -18,6 +18,17 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                  : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 // NN tile: C_tile(64 x 32) = A(64 x K) * B(K x 32); A col-major (lda), B col-major (ldb).
 // 128 threads = 4 warps as 2 (m) x 2 (n); each warp owns 32 x 16 = 4 x 2 DMMA tiles.
 // Epilogue functor interface (two phases, so that all global reads of a thread's 16 output
@@ -164,6 +175,110 @@ __device__ __forceinline__ void nn_tile_pf(int M, int K, int n, const double* __
             }
 }
 
+// 64 x 64 NN tile for LARGE K (the PCG update at N_occ >= 64 and the SMW products are genuine
+// FP64 GEMMs there): 256 threads = 8 warps as 2 (m) x 4 (n), warp tile 32 x 16 = 4 x 2 DMMA tiles,
+// a GB_ST-stage cp.async ring of 32-deep K slices, then the two-phase epilogue.
+constexpr int GB_BM = 64, GB_BN = 64, GB_BK = 32, GB_ST = 3, GB_LDA = GB_BM + 4, GB_LDB = GB_BK + 4;
+
+constexpr size_t nn_big_smem() { return (size_t)GB_ST * (GB_BK * GB_LDA + GB_BN * GB_LDB) * sizeof(double); }
+
+template <class Ep>
+__device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* __restrict__ A, int lda,
+                                            const double* __restrict__ B, int ldb, int m0, int n0, const Ep& ep) {
+    extern __shared__ __align__(16) double gsm[];
+    double* As = gsm;                              // [GB_ST][GB_BK][GB_LDA]  (k-major: A(m, k) at [k][m])
+    double* Bs = gsm + GB_ST * GB_BK * GB_LDA;     // [GB_ST][GB_BN][GB_LDB]  (B(k, n) at [n][k])
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int nk = (K + GB_BK - 1) / GB_BK;
+    const bool vecA = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
+    const bool vecB = ((ldb & 1) == 0) && ((((uintptr_t)B) & 15) == 0);
+    auto load_stage = [&](int st, int k0) {
+        double* as = As + st * GB_BK * GB_LDA;
+        double* bs = Bs + st * GB_BN * GB_LDB;
+        // A tile: GB_BK columns (k) of GB_BM contiguous rows (m)
+        for (int c = tid; c < GB_BK * (GB_BM / 2); c += 256) {
+            const int kk = c / (GB_BM / 2), mm = 2 * (c % (GB_BM / 2));
+            const int gm = m0 + mm, gk = k0 + kk;
+            if (vecA && gm + 1 < M && gk < K) {
+                cp_async16(as + kk * GB_LDA + mm, A + (size_t)gk * lda + gm, true);
+            } else {
+                as[kk * GB_LDA + mm] = (gm < M && gk < K) ? A[(size_t)gk * lda + gm] : 0.0;
+                as[kk * GB_LDA + mm + 1] = (gm + 1 < M && gk < K) ? A[(size_t)gk * lda + gm + 1] : 0.0;
+            }
+        }
+        // B tile: GB_BN columns (n) of GB_BK contiguous k
+        for (int c = tid; c < GB_BN * (GB_BK / 2); c += 256) {
+            const int nn = c / (GB_BK / 2), kk = 2 * (c % (GB_BK / 2));
+            const int gn = n0 + nn, gk = k0 + kk;
+            if (vecB && gn < n && gk + 1 < K) {
+                cp_async16(bs + nn * GB_LDB + kk, B + (size_t)gn * ldb + gk, true);
+            } else {
+                bs[nn * GB_LDB + kk] = (gn < n && gk < K) ? B[(size_t)gn * ldb + gk] : 0.0;
+                bs[nn * GB_LDB + kk + 1] = (gn < n && gk + 1 < K) ? B[(size_t)gn * ldb + gk + 1] : 0.0;
+            }
+        }
+    };
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int st = 0; st < GB_ST - 1; ++st) {
+        if (st < nk) load_stage(st, st * GB_BK);
+        cp_async_commit();
+    }
+    for (int it = 0; it < nk; ++it) {
+        const int nxt = it + GB_ST - 1;
+        if (nxt < nk) load_stage(nxt % GB_ST, nxt * GB_BK);
+        cp_async_commit();
+        cp_async_wait<GB_ST - 1>();
+        __syncthreads();
+        const double* as = As + (it % GB_ST) * GB_BK * GB_LDA;
+        const double* bs = Bs + (it % GB_ST) * GB_BN * GB_LDB;
+#pragma unroll
+        for (int ks = 0; ks < GB_BK; ks += 4) {
+            double af[4], bf[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = as[(ks + t) * GB_LDA + wm * 32 + i * 8 + g];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) bf[j] = bs[(wn * 16 + j * 8 + g) * GB_LDB + ks + t];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int ih = 0; ih < 4; ih += 2) {
+        typename Ep::Regs regs[2][2][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = m0 + wm * 32 + (ih + i) * 8 + g;
+                    const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
+                    if (row < M && col < n) ep.load(row, col, regs[i][j][e]);
+                }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = m0 + wm * 32 + (ih + i) * 8 + g;
+                    const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
+                    if (row < M && col < n) ep.store(row, col, acc[ih + i][j][e], regs[i][j][e]);
+                }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Split-K TN GEMM with the K-split reduced through distributed shared memory.
 //   C(m x n, ld ldc) = alpha * A(:, m)^T B(:, n),  A: K x m (lda), B: K x n (ldb).
@@ -174,17 +289,6 @@ __device__ __forceinline__ void nn_tile_pf(int M, int K, int n, const double* __
 // DSMEM.  No global partials, no atomics: the result depends only on (K, CS), not on n.
 // `hook(col)` runs once per output column (rank 0, m-tile 0) after the tile is final.
 constexpr int TC_BN = 32, TC_BK = 32, TC_PAD = 4, TC_ST = 4;  // TC_ST-stage cp.async ring
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    const int sz = valid ? 16 : 0;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 struct NoHook {
     __device__ __forceinline__ void operator()(int) const {}

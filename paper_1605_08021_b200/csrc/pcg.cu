@@ -182,6 +182,40 @@ __global__ void __launch_bounds__(128, 4) k_pcg_update(int M, int K, int n, cons
     nn_tile_pf(M, K, n, A, lda, B, ldb, blockIdx.x * NP_BM, n0, ep);
 }
 
+// Large-K variant (N_occ >= 64): 64 x 64 tiles, multistage cp.async, 256 threads.
+template <class Ep>
+__global__ void __launch_bounds__(256, 2) k_pcg_update_big(int M, int K, int n, const double* __restrict__ A, int lda,
+                                                        const double* __restrict__ B, int ldb, Ep ep) {
+    const int n0 = blockIdx.y * GB_BN;
+    __shared__ int any;
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int c = n0; c < min(n, n0 + GB_BN); ++c) a |= ep.active[c];
+        any = a;
+    }
+    __syncthreads();
+    if (!any) return;
+    nn_tile_big(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, n0, ep);
+}
+
+template <class Ep>
+static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const double* A, int lda, const double* B,
+                              int ldb, const Ep& ep) {
+    if (K >= 64) {
+        static bool attr = false;
+        if (!attr) {
+            ACP_CUDA(cudaFuncSetAttribute(k_pcg_update_big<Ep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)nn_big_smem()));
+            attr = true;
+        }
+        k_pcg_update_big<Ep><<<dim3(cdiv(M, GB_BM), cdiv(n, GB_BN)), 256, nn_big_smem(), ctx->stream>>>(
+            M, K, n, A, lda, B, ldb, ep);
+    } else {
+        k_pcg_update<Ep><<<dim3(cdiv(M, NP_BM), cdiv(n, NP_BN)), 128, 0, ctx->stream>>>(M, K, n, A, lda, B, ldb, ep);
+    }
+    launched(ctx);
+}
+
 __global__ void k_count_active(const int* __restrict__ active, int n, int* __restrict__ out) {
     __shared__ int red[32];
     int s = 0;
@@ -264,7 +298,6 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         launched(ctx);
     }
     const double tol2 = tol * tol;
-    dim3 ugrid(cdiv(Ng, NP_BM), cdiv(n, NP_BN));
 
     auto precond_half = [&](int mode) {
         FopArgs f;
@@ -280,8 +313,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
                                       ScalHook{mode, s, tol2, nvalid, nmu_p}),
                     "projection GEMM needs an even grid");
         EpBeta ep{Y, P, s.beta, s.active, Ng, mode == SC_INIT ? 1 : 0};
-        k_pcg_update<EpBeta><<<ugrid, 128, 0, ctx->stream>>>(Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
-        launched(ctx);
+        launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
     };
     auto hamiltonian_half = [&]() {
         FopArgs f;
@@ -298,8 +330,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
                                       ScalHook{SC_ALPHA, s, tol2, nvalid, nmu_p}),
                     "projection GEMM needs an even grid");
         EpAlpha ep{Y, P, X, R, s.alpha, s.active, Ng};
-        k_pcg_update<EpAlpha><<<ugrid, 128, 0, ctx->stream>>>(Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
-        launched(ctx);
+        launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
     };
 
     // r0 = b, z0 = Q M r0, p0 = z0
@@ -416,9 +447,7 @@ void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* 
                 launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, X, Ng, C, n_occ, NoHook{});
             } else {
                 EpBeta ep{X, Y, beta, active, Ng, 0};
-                dim3 ugrid(cdiv(Ng, NP_BM), cdiv(n, NP_BN));
-                k_pcg_update<EpBeta><<<ugrid, 128, 0, ctx->stream>>>(Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
-                launched(ctx);
+                launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
             }
         }
     };

@@ -138,6 +138,18 @@ def test_gemms(sysx):
         assert rel(Z, Z0 - s.gs.Psi @ Cm) < 1e-12
 
 
+@pytest.mark.parametrize("M,K,n", [(300, 100, 70), (301, 97, 65), (128, 64, 64)])
+def test_gemm_nn_large_k(M, K, n):
+    """The 64 x 64 multistage DMMA tile (K >= 64), aligned and unaligned (odd ld) operands."""
+    s = system("tiny4")
+    rng = np.random.default_rng(M + K + n)
+    A = rng.standard_normal((M, K))
+    B = rng.standard_normal((K, n))
+    C0 = rng.standard_normal((M, n))
+    C = s.ctx.gemm_nn(T(A.T), T(B.T), C=T(C0.T), alpha=-0.5, beta=2.0).cpu().numpy().T
+    assert rel(C, 2.0 * C0 - 0.5 * A @ B) < 1e-13
+
+
 def test_perturbation_matrix(sysx):
     s = sysx
     G = s.ctx.perturbations(s.R).cpu().numpy().T
