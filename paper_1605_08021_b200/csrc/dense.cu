@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace acp {
 
@@ -393,7 +394,7 @@ void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
         const int R = n - p0;
         const size_t pbytes = (size_t)R * pw * sizeof(double);
         const int use_smem = pbytes <= 200 * 1024;
-        const int T = 1024;
+        const int T = R <= 512 ? 256 : 1024;  // fewer warps -> cheaper barriers on short panels
         k_lu_panel<<<1, T, use_smem ? pbytes : 0, ctx->stream>>>(AB, n, p0, pw, use_smem, piv, st);
         launched(ctx);
         k_lu_swap<<<cdiv(ntot, 128), 128, 0, ctx->stream>>>(AB, n, ntot, p0, pw, piv);
@@ -569,7 +570,101 @@ __global__ void k_permute_cols(int n, const double* __restrict__ Vin, const int*
     Vout[e] = Vin[(size_t)order[j] * n + i];
 }
 
+// Eigenvalues only, n <= 32: cyclic Jacobi inside ONE warp with the matrix in registers (lane l
+// holds column l), no block barriers.  Round r of a sweep rotates the disjoint pairs of the circle
+// ordering (m = 32 slots, slots >= n are dummies); lane l learns its partner and the pair's
+// rotation by shuffles, updates its column (rows p, q) locally and combines with its partner's
+// column for the column rotation.  Sweeps stop when the off-diagonal Frobenius norm is
+// <= 1e-14 of the total (same criterion as k_jacobi).  Ascending sort by rank at the end.
+__global__ void __launch_bounds__(32) k_jacobi_warp(const double* __restrict__ Ag, int n, double* __restrict__ w,
+                                                    int max_sweeps) {
+    const int l = threadIdx.x;
+    double a[32];  // a[i] = A(i, l)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = (l < n && i < n) ? Ag[(size_t)l * n + i] : (i == l ? 1.0 : 0.0) * 0.0;
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+        double off = 0.0, tot = 0.0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            tot += a[i] * a[i];
+            if (i != l) off += a[i] * a[i];
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            off += __shfl_xor_sync(0xffffffffu, off, o);
+            tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        }
+        if (off <= 1e-28 * tot) break;
+        for (int r = 0; r < 31; ++r) {
+            // partner of slot l in round r of the circle method on 32 slots (slot 31 fixed)
+            int q;
+            if (l == 31) q = r;
+            else if (l == r) q = 31;
+            else q = ((2 * r - l) % 31 + 31) % 31;
+            const int p = min(l, q), qq = max(l, q);
+            // a_pp, a_qq, a_pq from the owners: lane p holds column p (a_pp = a[p], a_pq = a[qq])
+            double app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (i == l) app = a[i];          // diagonal of my column
+                if (i == q) apq = a[i];          // A(q, l)
+            }
+            aqq = __shfl_sync(0xffffffffu, app, q);
+            // my diagonal is app (column l); rotation angle from the pair (p, qq)
+            const double dpp = l == p ? app : aqq, dqq = l == p ? aqq : app;
+            double c = 1.0, sn = 0.0;
+            if (qq < n && fabs(apq) > 1e-300 && fabs(apq) > 1e-18 * (fabs(dpp) + fabs(dqq))) {
+                const double th = (dqq - dpp) / (2.0 * apq);
+                const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                c = 1.0 / sqrt(t * t + 1.0);
+                sn = t * c;
+            }
+            // the pair's rotation is the one computed by its lower lane p (rounding could make the
+            // two lanes' copies of a_pq differ slightly)
+            c = __shfl_sync(0xffffffffu, c, p);
+            sn = __shfl_sync(0xffffffffu, sn, p);
+            // column rotation: A <- A J; column p' = c col_p - s col_q, column q' = s col_p + c col_q
+            const double sgn = l == p ? -1.0 : 1.0;  // p: c*mine - s*partner ; q: c*mine + s*partner
+            double partner[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) partner[i] = __shfl_sync(0xffffffffu, a[i], q);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) a[i] = c * a[i] + sgn * sn * partner[i];
+            // row rotation: A <- J^T A on rows (p_k, q_k) of every pair k, in my column.  The pair
+            // of row i is (i, partner(i)) with the rotation owned by lanes i / partner(i).
+#pragma unroll
+            for (int i = 0; i < 32; ++i) partner[i] = a[i];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                int qi;
+                if (i == 31) qi = r;
+                else if (i == r) qi = 31;
+                else qi = ((2 * r - i) % 31 + 31) % 31;
+                const double ci = __shfl_sync(0xffffffffu, c, i);   // (c, s) already uniform per pair
+                const double si = __shfl_sync(0xffffffffu, sn, i);
+                const double sg = i < qi ? -1.0 : 1.0;
+                a[i] = ci * partner[i] + sg * si * partner[qi];
+            }
+        }
+    }
+    // eigenvalues: diagonal entries, sorted ascending by rank (stable by index)
+    double d = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+        if (i == l) d = a[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+        const double dj = __shfl_sync(0xffffffffu, d, j);
+        if (dj < d || (dj == d && j < l)) ++rank;
+    }
+    if (l < n) w[rank] = d;
+}
+
 void sym_eig(acp_context* ctx, double* A, int n, double* w, double* V) {
+    if (!V && n <= 32 && !getenv("ACP_EIG_BLOCK")) {
+        k_jacobi_warp<<<1, 32, 0, ctx->stream>>>(A, n, w, 40);
+        launched(ctx);
+        return;
+    }
     double* Vt = V ? ctx->wsd("eig_Vt", (size_t)n * n) : nullptr;
     int* order = ctx->wsi("eig_order", n + 2);
     double* rot = ctx->wsd("eig_rot", 4 * (size_t)(n / 2 + 2));

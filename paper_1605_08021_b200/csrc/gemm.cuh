@@ -292,6 +292,7 @@ constexpr int TC_BN = 32, TC_BK = 32, TC_PAD = 4, TC_ST = 4;  // TC_ST-stage cp.
 
 struct NoHook {
     __device__ __forceinline__ void operator()(int) const {}
+    __device__ __forceinline__ bool tile_active(int, int) const { return true; }
 };
 
 template <int BM>
@@ -317,6 +318,9 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     const int CS = gridDim.x;
     const int rank = blockIdx.x;              // == cluster rank (cluster = (CS,1,1))
     const int n0 = blockIdx.y * TC_BN, m0 = blockIdx.z * BM;
+    // column tiles whose columns have all converged are skipped (uniform over the cluster: its
+    // CTAs share blockIdx.y, and nothing has synchronised yet)
+    if (!hook.tile_active(n0, n)) return;
     const int kb = rank * kchunk;
     const int ke = min(K, kb + kchunk);
     const int nk = ke > kb ? (ke - kb + TC_BK - 1) / TC_BK : 0;

@@ -6,11 +6,13 @@
 // on range(Q) because every node lies in [eps_1, eps_Nocc] below the gap).
 // Preconditioner: z = Q M r, M = IFFT (|k|^2/2 + tau)^{-1} FFT (Fourier diagonal).
 //
-// One CG iteration over the whole batch = 8 launches captured in a CUDA graph:
-//   K1 y = (H - eps_c) p  (+ p.y)          K2 C  = dV Psi^T y (split-K DMMA)
-//   S  alpha = rz / p.y  (split reduce)     K3 Ap = y - Psi C ; x += alpha p ; r -= alpha Ap
-//   K1 zh = M r (+ r.zh, r.r)               K2 Cz = dV Psi^T zh
-//   S  convergence / beta                   K3 p = (zh - Psi Cz) + beta p
+// One CG iteration over the whole batch = 6 launches (the CG scalars run inside K2):
+//   K1 y = (H - eps_c) p  (+ p.y)          K2 C  = dV Psi^T y, alpha = rz / p.y (hook)
+//   K3 Ap = y - Psi C ; x += alpha p ; r -= alpha Ap
+//   K1 zh = M r (+ r.zh, r.r)               K2 Cz = dV Psi^T zh, convergence / beta (hook)
+//   K3 p = (zh - Psi Cz) + beta p
+// The iteration loop is one CUDA graph whose while node re-runs a 4-iteration body until every
+// column has converged (device-side condition, no host round trips).
 // p.y equals p.Q(H-eps)Q p and r.zh equals r.z because p, r stay in range(Q).
 // Per-column activity flags freeze converged columns; every reduction has a
 // fixed order, so results do not depend on scheduling.
@@ -81,6 +83,12 @@ struct ScalHook {
     double tol2;
     int n_valid_mu;
     int nmu_p;
+    __device__ __forceinline__ bool tile_active(int n0, int n) const {
+        if (mode == SC_INIT) return true;
+        int a = 0;
+        for (int c = n0; c < min(n, n0 + 32); ++c) a |= s.active[c];
+        return a != 0;
+    }
     __device__ __forceinline__ void operator()(int j) const {
         if (mode == SC_INIT) {
             const double rz = s.dots[2 * j], bb = s.dots[2 * j + 1];
@@ -216,7 +224,10 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
     launched(ctx);
 }
 
-__global__ void k_count_active(const int* __restrict__ active, int n, int* __restrict__ out) {
+// Number of still-active columns; sets the while-node condition of the PCG graph (continue while
+// columns remain and fewer than max_chunks chunks ran) and counts the trips.
+__global__ void k_count_active(const int* __restrict__ active, int n, int* __restrict__ out,
+                               cudaGraphConditionalHandle h, int* __restrict__ chunks, int max_chunks) {
     __shared__ int red[32];
     int s = 0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) s += active[j];
@@ -227,6 +238,8 @@ __global__ void k_count_active(const int* __restrict__ active, int n, int* __res
         int t = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
         *out = t;
+        const int c = ++(*chunks);
+        if (max_chunks > 0) cudaGraphSetConditional(h, (t > 0 && c < max_chunks) ? 1u : 0u);
     }
 }
 
@@ -285,7 +298,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     s.active = ctx->wsi("pcg_active", n);
     s.iters = ctx->wsi("pcg_iters", n);
     s.dots = dots;
-    int* d_nact = ctx->wsi("pcg_nact", 1);
+    int* d_nact = ctx->wsi("pcg_nact", 2);  // [0] active columns, [1] while-loop trips
     int* h_nact = static_cast<int*>(ctx->pinned);
 
 
@@ -336,32 +349,94 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     // r0 = b, z0 = Q M r0, p0 = z0
     precond_half(SC_INIT);
 
-    // `chunk` iterations captured once into a cached graph, replayed until every column converged.
+    // The whole iteration loop is ONE CUDA graph with a device-side while node: its body is
+    // `chunk` CG iterations + k_count_active, which sets the loop condition (columns still active
+    // and fewer than max_iter iterations done) -- no host round trip until every column has
+    // converged.  Cached per shapes/pointers; the chunk counter is reset before each launch.
     const int chunk = 4;
+    const int max_chunks = (max_iter + chunk - 1) / chunk;
+    int* d_chunks = d_nact + 1;
     char key[512];
-    snprintf(key, sizeof(key), "pcg:%d:%d:%d:%d:%d:%.17g:%.17g:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p", Ng, n, n_occ,
-             nmu_p, nvalid, tol2, tau, (void*)Psi, (void*)V, (void*)R, (void*)P, (void*)Y, (void*)X, (void*)C,
-             (void*)shift, (void*)dots, (void*)s.rz, (void*)s.active, (void*)d_nact);
-    cudaGraphExec_t exec = graph_cached(ctx, key, [&]() {
-        for (int it = 0; it < chunk; ++it) {
-            hamiltonian_half();
-            precond_half(SC_BETA);
+    snprintf(key, sizeof(key), "pcgw:%d:%d:%d:%d:%d:%d:%.17g:%.17g:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p", Ng, n,
+             n_occ, nmu_p, nvalid, max_chunks, tol2, tau, (void*)Psi, (void*)V, (void*)R, (void*)P, (void*)Y,
+             (void*)X, (void*)C, (void*)shift, (void*)dots, (void*)s.rz, (void*)s.active, (void*)d_nact);
+    // ACP_PCG_HOSTLOOP=1: the same body as a plain graph replayed from the host (ncu cannot
+    // profile kernels inside conditional-node bodies; the launch lists in profiles/ use this)
+    if (getenv("ACP_PCG_HOSTLOOP")) key[0] = 'H';
+    cudaGraphExec_t exec = nullptr;
+    auto it_g = ctx->graphs.find(key);
+    bool hostloop = key[0] == 'H';
+    if (hostloop) {
+        ACP_CUDA(cudaMemsetAsync(d_chunks, 0, sizeof(int), ctx->stream));
+        exec = graph_cached(ctx, key, [&]() {
+            for (int it = 0; it < chunk; ++it) {
+                hamiltonian_half();
+                precond_half(SC_BETA);
+            }
+            k_count_active<<<1, 256, 0, ctx->stream>>>(s.active, n, d_nact, (cudaGraphConditionalHandle)0, d_chunks,
+                                                       -1);
+            launched(ctx);
+        });
+        bool conv = false;
+        for (int c = 0; c < max_chunks; ++c) {
+            graph_launch(ctx, key, exec);
+            ACP_CUDA(cudaMemcpyAsync(h_nact, d_nact, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (h_nact[0] == 0) {
+                conv = true;
+                break;
+            }
         }
-        k_count_active<<<1, 256, 0, ctx->stream>>>(s.active, n, d_nact);
-        launched(ctx);
-    });
-    int done_iter = 0;
-    bool converged = false;
-    while (done_iter < max_iter) {
-        graph_launch(ctx, key, exec);
-        done_iter += chunk;
-        ACP_CUDA(cudaMemcpyAsync(h_nact, d_nact, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        ACP_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (*h_nact == 0) {
-            converged = true;
-            break;
+        h_nact[0] = conv ? 0 : 1;
+    } else if (it_g != ctx->graphs.end()) {
+        exec = it_g->second.exec;
+    } else {
+        cudaGraph_t g = nullptr;
+        ACP_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        ACP_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        ACP_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        const long long before = ctx->launches;
+        ACP_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal));
+        try {
+            for (int it = 0; it < chunk; ++it) {
+                hamiltonian_half();
+                precond_half(SC_BETA);
+            }
+            k_count_active<<<1, 256, 0, ctx->stream>>>(s.active, n, d_nact, h, d_chunks, max_chunks);
+            launched(ctx);
+        } catch (...) {
+            cudaGraph_t tmp = nullptr;
+            cudaStreamEndCapture(ctx->stream, &tmp);
+            cudaGraphDestroy(g);
+            throw;
         }
+        cudaGraph_t body2 = nullptr;
+        ACP_CUDA(cudaStreamEndCapture(ctx->stream, &body2));
+        ACP_CUDA(cudaGraphInstantiate(&exec, g, 0));
+        cudaGraphDestroy(g);
+        auto& ent = ctx->graphs[key];
+        ent.exec = exec;
+        ent.launches = ctx->launches - before;  // per loop trip; scaled by the trip count below
+        ctx->launches = before;
     }
+    if (!hostloop) {
+        ACP_CUDA(cudaMemsetAsync(d_chunks, 0, sizeof(int), ctx->stream));
+        ACP_CUDA(cudaGraphLaunch(exec, ctx->stream));
+        ACP_CUDA(cudaMemcpyAsync(h_nact, d_nact, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+        const int trips = h_nact[1];
+        ctx->launches += ctx->graphs[key].launches * trips;
+    }
+    const bool converged = h_nact[0] == 0;
     if (st) {
         std::vector<int> it(n);
         std::vector<double> res(n), bb(n);

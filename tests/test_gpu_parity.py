@@ -297,6 +297,22 @@ def test_compress_large_nmu_blocked_trsm():
     assert rel(Xi_g.cpu().numpy().T, Xi_o) < 1e-8
 
 
+def test_apply_chi0_hostloop_equals_while_node(sysx, monkeypatch):
+    """The device-side while-node PCG loop and the host-driven replay (ACP_PCG_HOSTLOOP, used for
+    ncu launch lists) run the same kernels in the same order: bitwise-identical W."""
+    from paper_1605_08021_b200 import Context
+    s = sysx
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    St, Xt = T(S_o, torch.int32), T(Xi_o.T)
+    W1, i1 = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    monkeypatch.setenv("ACP_PCG_HOSTLOOP", "1")
+    ctx = Context.from_config(s.cfg)
+    W2, i2 = ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    ctx.close()
+    assert torch.equal(W1, W2) and i1["total_iter"] == i2["total_iter"]
+
+
 def test_apply_chi0_empty_shard(sysx):
     """An empty mu-range (a rank with no columns) is a no-op that leaves W untouched."""
     s = sysx

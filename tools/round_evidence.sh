@@ -9,8 +9,8 @@ timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/$
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc $?"; tail -1 gpurun_out/${T}_smoke.log
 timeout 900 python bench.py > gpurun_out/${T}_bench.log 2>&1; echo "bench rc $?"; grep '^{' gpurun_out/${T}_bench.log | cut -c1-400
 timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/${T}_bench_ref.log 2>&1; echo "ref rc $?"; grep '^{' gpurun_out/${T}_bench_ref.log | cut -c1-300
-timeout 600 python bench.py --steps 1 --warmup 3 --skip-cpu > gpurun_out/${T}_plain.log 2>&1 && \
-  timeout 900 ncu --nvtx --nvtx-include "acp_step/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv \
+ACP_PCG_HOSTLOOP=1 timeout 600 python bench.py --steps 1 --warmup 3 --skip-cpu > gpurun_out/${T}_plain.log 2>&1 && \
+  ACP_PCG_HOSTLOOP=1 timeout 900 ncu --nvtx --nvtx-include "acp_step/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv \
     python bench.py --steps 1 --warmup 3 --skip-cpu > gpurun_out/${T}_ncu_launch.log 2>&1
 echo "launch list rc $?"
 for W in 0 1 2; do
