@@ -81,6 +81,7 @@ struct acp_context {
     int cs = 1, r0 = 0, c1 = 0, fthreads = 0, fept = 0;
     size_t fsmem = 0;
     int fnp = 1;                         // 2D: column pairs per cluster for operator launches
+    bool pdl = false;                    // launch with programmatic dependent launch (PCG graph)
     int fthreads1 = 0, fept1 = 0;        // 2D: geometry of the one-pair setup transforms
     size_t fsmem1 = 0;
 
@@ -115,6 +116,13 @@ struct acp_context {
 };
 
 namespace acp {
+
+// Programmatic dependent launch (PDL, sm_90+): kernels of the PCG loop are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, wait for their predecessor's results with
+// griddepcontrol.wait (a no-op without the attribute) and let their successor be scheduled early
+// with griddepcontrol.launch_dependents.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Record one kernel launch (call right after <<<>>>); checks launch errors.
 inline void launched(acp_context* ctx, int n = 1) {

@@ -140,6 +140,8 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
     const int c0 = 2 * blockIdx.x, c1 = c0 + 1;
     const int ncol = IO == IO_OP ? io.f.n : io.n;
     const bool has1 = c1 < ncol;
+    pdl_wait();
+    pdl_trigger();
     bool act0 = true, act1 = has1;
     if (IO == IO_OP && io.f.active) {
         act0 = io.f.active[c0] != 0;
@@ -351,6 +353,8 @@ __global__ void __launch_bounds__(1024) k_fft2d(FftGeom G, const double2* __rest
     double2* buf = sm2;
     const int pbase = (grp0 + blockIdx.y) * np;  // first pair of this cluster
     const int ncol = IO == IO_OP ? io.f.n : io.n;
+    pdl_wait();
+    pdl_trigger();
     bool any = false;
     for (int p = 0; p < np; ++p) {
         const int c0 = 2 * (pbase + p), c1 = c0 + 1;
@@ -518,7 +522,17 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
                   : ctx->fept <= 2 ? k_fft1d<2, true, IO> : ctx->fept <= 4 ? k_fft1d<4, true, IO>
                   : k_fft1d<8, true, IO>;
         set_smem_attr((const void*)kern, smem, false);
-        kern<<<npair, T, smem, ctx->stream>>>(G, ctx->d_tw, io);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(npair, 1, 1);
+        cfg.blockDim = dim3(T, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = ctx->pdl ? 1 : 0;
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, G, (const double2*)ctx->d_tw, io));
         launched(ctx);
         return;
     }
@@ -537,13 +551,15 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
         cfg.blockDim = dim3(Tl, 1, 1);
         cfg.dynamicSmemBytes = smeml;
         cfg.stream = ctx->stream;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = ctx->cs;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = ctx->pdl ? 2 : 1;
         ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, Gl, (const double2*)ctx->d_tw, (const double2*)ctx->d_tw1, io, g0));
         launched(ctx);
     }

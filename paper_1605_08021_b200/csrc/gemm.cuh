@@ -318,6 +318,8 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     const int CS = gridDim.x;
     const int rank = blockIdx.x;              // == cluster rank (cluster = (CS,1,1))
     const int n0 = blockIdx.y * TC_BN, m0 = blockIdx.z * BM;
+    pdl_wait();
+    pdl_trigger();
     // column tiles whose columns have all converged are skipped (uniform over the cluster: its
     // CTAs share blockIdx.y, and nothing has synchronised yet)
     if (!hook.tile_active(n0, n)) return;
@@ -420,13 +422,15 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(128, 1, 1);
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = ctx->pdl ? 2 : 1;
     if (m <= 32) {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
         cfg.dynamicSmemBytes = tn_cluster_smem<32>();

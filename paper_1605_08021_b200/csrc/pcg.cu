@@ -177,6 +177,8 @@ struct EpBeta {
 template <class Ep>
 __global__ void __launch_bounds__(128, 4) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
                                                        const double* __restrict__ B, int ldb, Ep ep) {
+    pdl_wait();
+    pdl_trigger();
     // skip tiles whose columns are all inactive (uniform per CTA)
     const int n0 = blockIdx.y * NP_BN;
     __shared__ int any;
@@ -194,6 +196,8 @@ __global__ void __launch_bounds__(128, 4) k_pcg_update(int M, int K, int n, cons
 template <class Ep>
 __global__ void __launch_bounds__(256, 2) k_pcg_update_big(int M, int K, int n, const double* __restrict__ A, int lda,
                                                         const double* __restrict__ B, int ldb, Ep ep) {
+    pdl_wait();
+    pdl_trigger();
     const int n0 = blockIdx.y * GB_BN;
     __shared__ int any;
     if (threadIdx.x == 0) {
@@ -209,6 +213,13 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update_big(int M, int K, int n, 
 template <class Ep>
 static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const double* A, int lda, const double* B,
                               int ldb, const Ep& ep) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = ctx->pdl ? 1 : 0;
     if (K >= 64) {
         static bool attr = false;
         if (!attr) {
@@ -216,10 +227,15 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
                                           (int)nn_big_smem()));
             attr = true;
         }
-        k_pcg_update_big<Ep><<<dim3(cdiv(M, GB_BM), cdiv(n, GB_BN)), 256, nn_big_smem(), ctx->stream>>>(
-            M, K, n, A, lda, B, ldb, ep);
+        cfg.gridDim = dim3(cdiv(M, GB_BM), cdiv(n, GB_BN), 1);
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.dynamicSmemBytes = nn_big_smem();
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_pcg_update_big<Ep>, M, K, n, A, lda, B, ldb, ep));
     } else {
-        k_pcg_update<Ep><<<dim3(cdiv(M, NP_BM), cdiv(n, NP_BN)), 128, 0, ctx->stream>>>(M, K, n, A, lda, B, ldb, ep);
+        cfg.gridDim = dim3(cdiv(M, NP_BM), cdiv(n, NP_BN), 1);
+        cfg.blockDim = dim3(128, 1, 1);
+        cfg.dynamicSmemBytes = 0;
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_pcg_update<Ep>, M, K, n, A, lda, B, ldb, ep));
     }
     launched(ctx);
 }
@@ -228,6 +244,7 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
 // columns remain and fewer than max_chunks chunks ran) and counts the trips.
 __global__ void k_count_active(const int* __restrict__ active, int n, int* __restrict__ out,
                                cudaGraphConditionalHandle h, int* __restrict__ chunks, int max_chunks) {
+    pdl_wait();
     __shared__ int red[32];
     int s = 0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) s += active[j];
@@ -407,13 +424,18 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         ACP_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
                                                cudaStreamCaptureModeThreadLocal));
         try {
+            // PDL measured slower on configs[1] (14.25 vs 13.84-14.03 ms/step: the early-scheduled
+            // dependent CTAs take SM slots from the 4-CTA/SM FFT wave), so it is opt-in
+            ctx->pdl = getenv("ACP_PDL") != nullptr;
             for (int it = 0; it < chunk; ++it) {
                 hamiltonian_half();
                 precond_half(SC_BETA);
             }
+            ctx->pdl = false;
             k_count_active<<<1, 256, 0, ctx->stream>>>(s.active, n, d_nact, h, d_chunks, max_chunks);
             launched(ctx);
         } catch (...) {
+            ctx->pdl = false;
             cudaGraph_t tmp = nullptr;
             cudaStreamEndCapture(ctx->stream, &tmp);
             cudaGraphDestroy(g);
