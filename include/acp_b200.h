@@ -196,6 +196,18 @@ int acp_gemm_tn(acp_context* ctx, int K, int m, int n, double alpha, const doubl
 int acp_gemm_nn(acp_context* ctx, int M, int K, int n, double alpha, const double* d_A, int lda,
                 const double* d_B, int ldb, double beta, double* d_C, int ldc);
 
+/* Solve A X = B in place for the n x n column-major d_A (overwritten by its LU factors) and the
+ * n x nrhs column-major d_B (overwritten by X) -- the dense SMW core solve of Eq. dyson4
+ * (PAPER.md:640-650): blocked right-looking LU with partial pivoting (largest magnitude, lowest
+ * row on ties) and blocked back substitution.  ACP_ERR_SINGULAR for an exactly singular A. */
+int acp_lu_solve(acp_context* ctx, int n, int nrhs, double* d_A, double* d_B);
+
+/* Eigenvalues (ascending) of the symmetric n x n column-major d_A -- the phonon spectrum step
+ * lambda = eig(D).  d_A is not modified (a workspace copy is reduced);
+ * d_w: out, n values.  n <= 32: one-warp Jacobi; larger: Householder tridiagonalisation and
+ * Sturm multisection (accuracy ~ eps ||A||).  ACP_ERR_INVALID for n < 1 or NULL pointers. */
+int acp_sym_eigvals(acp_context* ctx, int n, const double* d_A, double* d_w);
+
 /* Enqueue `reps` back-to-back launches of one hot-path kernel on the context
  * stream and return WITHOUT synchronising, so the caller can bracket them with
  * its own CUDA events on that stream (bench.py's live roofline timing).

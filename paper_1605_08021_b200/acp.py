@@ -71,6 +71,8 @@ _sig = {
     "acp_fourier_apply": [_V, _V, ctypes.c_int, ctypes.c_int, ctypes.c_double, _V, _V, _V],
     "acp_gemm_tn": [_V, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, _V, ctypes.c_int, _V,
                     ctypes.c_int, _V],
+    "acp_sym_eigvals": [_V, ctypes.c_int, _V, _V],
+    "acp_lu_solve": [_V, ctypes.c_int, ctypes.c_int, _V, _V],
     "acp_kernel_bench": [_V, ctypes.c_int, _V, _V, _V, ctypes.c_int, _V, ctypes.c_int],
     "acp_get_stream": [_V],
     "acp_gemm_nn": [_V, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, _V, ctypes.c_int, _V,
@@ -288,6 +290,25 @@ class Context:
         C = self._empty(n, m)
         self._check(_lib.acp_gemm_tn(self._h, K, m, n, alpha, _ptr(A), K, _ptr(B), K, _ptr(C)), "acp_gemm_tn")
         return C
+
+    def lu_solve(self, A, B):
+        """X with A X = B for column-major A (n x n: tensor (n, n) holding A^T) and B (n x nrhs:
+        tensor (nrhs, n)); returns (LU factors, X) as new tensors in the same layout."""
+        self._pre()
+        A = A.clone()
+        B = B.clone()
+        n = A.shape[0]
+        nrhs = B.shape[0]
+        self._check(_lib.acp_lu_solve(self._h, n, nrhs, _ptr(A), _ptr(B)), "acp_lu_solve")
+        return A, B
+
+    def sym_eigvals(self, A):
+        """Ascending eigenvalues of the symmetric matrix A (n x n tensor on the device)."""
+        self._pre()
+        n = A.shape[0]
+        w = self._empty(n)
+        self._check(_lib.acp_sym_eigvals(self._h, n, _ptr(A), _ptr(w)), "acp_sym_eigvals")
+        return w
 
     def gemm_nn(self, A, B, C=None, alpha=1.0, beta=0.0):
         """C = beta C + alpha A B, A (M x K) column-major = tensor (K, M); B (K x n) = tensor (n, K)."""

@@ -195,6 +195,33 @@ int acp_gemm_nn(acp_context* ctx, int M, int K, int n, double alpha, const doubl
     });
 }
 
+int acp_lu_solve(acp_context* ctx, int n, int nrhs, double* d_A, double* d_B) {
+    if (!ctx || !d_A || (nrhs > 0 && !d_B) || n < 1 || nrhs < 0) return ACP_ERR_INVALID;
+    return guarded(ctx, [&] {
+        double* AB = ctx->wsd("api_luAB", (size_t)n * (n + nrhs));
+        ACP_CUDA(cudaMemcpyAsync(AB, d_A, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        if (nrhs)
+            ACP_CUDA(cudaMemcpyAsync(AB + (size_t)n * n, d_B, (size_t)n * nrhs * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+        acp::lu_solve_blocked(ctx, AB, n, nrhs);
+        ACP_CUDA(cudaMemcpyAsync(d_A, AB, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        if (nrhs)
+            ACP_CUDA(cudaMemcpyAsync(d_B, AB + (size_t)n * n, (size_t)n * nrhs * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+        acp::sync(ctx);
+    });
+}
+
+int acp_sym_eigvals(acp_context* ctx, int n, const double* d_A, double* d_w) {
+    if (!ctx || !d_A || !d_w || n < 1) return ACP_ERR_INVALID;
+    return guarded(ctx, [&] {
+        double* Aw = ctx->wsd("api_eigA", (size_t)n * n);
+        ACP_CUDA(cudaMemcpyAsync(Aw, d_A, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        acp::sym_eig(ctx, Aw, n, d_w, nullptr);
+        acp::sync(ctx);
+    });
+}
+
 int acp_kernel_bench(acp_context* ctx, int which, const double* d_Psi, const double* d_V, const double* d_X,
                      int n_cols, double* d_Y, int reps) {
     if (!ctx || !d_Psi || !d_V || !d_X || !d_Y || n_cols < 1 || reps < 1 || which < 0 || which > 2)

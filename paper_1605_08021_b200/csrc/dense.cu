@@ -5,6 +5,8 @@
 // critical loop); reductions use fixed orders, so results are deterministic.
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -379,6 +381,126 @@ void upper_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
 }
 
 // Solve A X = B in place; AB is n x (n + nrhs) column-major ([A | B], ld n).
+// Warp-row panel (R <= 512 rows): warp w owns panel rows [w*RPW, (w+1)*RPW) with lane j holding
+// column j of each of them in registers, so a row operation is one instruction across the warp
+// and a column costs ONE barrier: the lane of column k finds the warp's best row (first max),
+// the warp publishes (|a_ik|, row) and that row into a parity double-buffered slot, the warp
+// owning row k publishes row k; after the barrier every warp selects the same winner (largest
+// magnitude, lowest row on ties), swaps rows k <-> p from the published copies and eliminates its
+// rows (multiplier broadcast from lane k).  Same pivots and per-element operations as k_lu_panel.
+template <int RPW>
+__global__ void __launch_bounds__(512) k_lu_panel_warp(double* __restrict__ AB, int n, int p0, int pw,
+                                                       int* __restrict__ piv, int* __restrict__ status) {
+    extern __shared__ double lsm[];  // staging [32][R + 1] for coalesced load / store
+    __shared__ double cand_v[2][16];
+    __shared__ int cand_i[2][16];
+    __shared__ double cand_row[2][16][32];
+    __shared__ double krow[2][32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int R = n - p0, LS = R + 1;
+    for (int e = tid; e < R * pw; e += blockDim.x) {
+        const int jj = e / R, i = e - jj * R;
+        lsm[jj * LS + i] = AB[(size_t)(p0 + jj) * n + p0 + i];
+    }
+    __syncthreads();
+    const int r0 = warp * RPW;
+    double a[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        const int i = r0 + r;
+        a[r] = (i < R && lane < pw) ? lsm[lane * LS + i] : 0.0;
+    }
+    int sing = 0;
+    for (int kk = 0; kk < pw; ++kk) {
+        const int par = kk & 1;
+        double bv = -1.0;
+        int bi = 1 << 30, br = -1;
+        if (lane == kk) {
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) {
+                const int i = r0 + r;
+                const double v = fabs(a[r]);
+                if (i >= kk && i < R && v > bv) {
+                    bv = v;
+                    bi = i;
+                    br = r;
+                }
+            }
+        }
+        bv = __shfl_sync(0xffffffffu, bv, kk);
+        bi = __shfl_sync(0xffffffffu, bi, kk);
+        br = __shfl_sync(0xffffffffu, br, kk);
+        if (br >= 0) {
+            double val = 0.0;
+#pragma unroll
+            for (int r = 0; r < RPW; ++r)
+                if (r == br) val = a[r];
+            cand_row[par][warp][lane] = val;
+        }
+        if (lane == 0) {
+            cand_v[par][warp] = bv;
+            cand_i[par][warp] = bi;
+        }
+        if (kk >= r0 && kk < r0 + RPW) {
+            double val = 0.0;
+#pragma unroll
+            for (int r = 0; r < RPW; ++r)
+                if (r0 + r == kk) val = a[r];
+            krow[par][lane] = val;
+        }
+        __syncthreads();
+        double wv = lane < nw ? cand_v[par][lane] : -1.0;
+        int wi = lane < nw ? cand_i[par][lane] : (1 << 30), ww = lane;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {  // nw <= 16
+            const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, ww, o);
+            if (ov > wv || (ov == wv && oi < wi)) {
+                wv = ov;
+                wi = oi;
+                ww = ow;
+            }
+        }
+        wv = __shfl_sync(0xffffffffu, wv, 0);  // lanes 16..31 reduced only their padding
+        wi = __shfl_sync(0xffffffffu, wi, 0);
+        ww = __shfl_sync(0xffffffffu, ww, 0);
+        const bool zero = !(wv > 0.0);
+        const int pr = zero ? kk : wi;
+        if (tid == 0) piv[p0 + kk] = p0 + pr;
+        sing |= zero;
+        const double kj = krow[par][lane];
+        const double pj = zero ? kj : cand_row[par][ww][lane];
+        const double pk = __shfl_sync(0xffffffffu, pj, kk);
+        const double rp = zero ? 0.0 : 1.0 / pk;
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const int i = r0 + r;
+            if (pr != kk) {
+                if (i == kk) a[r] = pj;
+                else if (i == pr) a[r] = kj;
+            }
+            if (i > kk && i < R) {
+                const double l = __shfl_sync(0xffffffffu, a[r], kk) * rp;
+                if (lane == kk) a[r] = l;
+                else if (lane > kk) a[r] -= l * pj;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        const int i = r0 + r;
+        if (i < R && lane < pw) lsm[lane * LS + i] = a[r];
+    }
+    __syncthreads();
+    for (int e = tid; e < R * pw; e += blockDim.x) {
+        const int jj = e / R, i = e - jj * R;
+        AB[(size_t)(p0 + jj) * n + p0 + i] = lsm[jj * LS + i];
+    }
+    if (tid == 0 && sing) *status = 1;
+}
+
 void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
     const int ntot = n + nrhs;
     int* piv = ctx->wsi("lu_piv", n);
@@ -394,8 +516,26 @@ void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
         const int R = n - p0;
         const size_t pbytes = (size_t)R * pw * sizeof(double);
         const int use_smem = pbytes <= 200 * 1024;
-        const int T = R <= 512 ? 256 : 1024;  // fewer warps -> cheaper barriers on short panels
-        k_lu_panel<<<1, T, use_smem ? pbytes : 0, ctx->stream>>>(AB, n, p0, pw, use_smem, piv, st);
+        if (R <= 512 && getenv("ACP_LU_WARP_PANEL")) {  // opt-in: measured no faster end to end
+            static bool wattr = false;
+            if (!wattr) {
+                for (const void* f : {(const void*)k_lu_panel_warp<8>, (const void*)k_lu_panel_warp<16>,
+                                      (const void*)k_lu_panel_warp<32>})
+                    ACP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  32 * 513 * (int)sizeof(double)));
+                wattr = true;
+            }
+            const size_t ls = (size_t)32 * (R + 1) * sizeof(double);
+            if (R <= 128)
+                k_lu_panel_warp<8><<<1, 32 * cdiv(R, 8), ls, ctx->stream>>>(AB, n, p0, pw, piv, st);
+            else if (R <= 256)
+                k_lu_panel_warp<16><<<1, 32 * cdiv(R, 16), ls, ctx->stream>>>(AB, n, p0, pw, piv, st);
+            else
+                k_lu_panel_warp<32><<<1, 32 * cdiv(R, 32), ls, ctx->stream>>>(AB, n, p0, pw, piv, st);
+        } else {
+            const int T = R <= 512 ? 256 : 1024;  // fewer warps -> cheaper barriers on short panels
+            k_lu_panel<<<1, T, use_smem ? pbytes : 0, ctx->stream>>>(AB, n, p0, pw, use_smem, piv, st);
+        }
         launched(ctx);
         k_lu_swap<<<cdiv(ntot, 128), 128, 0, ctx->stream>>>(AB, n, ntot, p0, pw, piv);
         launched(ctx);
@@ -659,10 +799,210 @@ __global__ void __launch_bounds__(32) k_jacobi_warp(const double* __restrict__ A
     if (l < n) w[rank] = d;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Eigenvalues only (the phonon spectrum lambda of D): Householder reduction to
+// tridiagonal form, then Sturm-count multisection.  Block Jacobi needs O(n^3) work per sweep and
+// ~10 sweeps; this is one O(4n^3/3) reduction plus an O(n^2) eigenvalue search.
+//
+// k_tridiag<GRID>: lower Householder tridiagonalisation of the full symmetric column-major A.
+// Step k: x = A(k+1:, k); beta = -sign(x0) ||x||; v = [1, x(1:)/(x0-beta)]; tau = (beta-x0)/beta;
+// p = tau A22 v; w = p - (tau/2)(p.v) v; A22 -= v w^T + w v^T.  Every CTA derives v (and w) itself
+// from the same data with the same fixed-order reduction, so the copies agree bitwise and only the
+// matvec and the rank-2 update are distributed (one warp per column).  GRID=false: one CTA, A in
+// shared memory, __syncthreads; GRID=true: cooperative grid over A in global memory, grid.sync().
+template <bool GRID>
+__global__ void __launch_bounds__(1024) k_tridiag(double* __restrict__ Ag, int n, double* __restrict__ pg,
+                                                   double* __restrict__ dout, double* __restrict__ eout) {
+    namespace cg = cooperative_groups;
+    extern __shared__ double tsm[];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    double* vs = tsm;           // n
+    double* ws = vs + n;        // n
+    double* red = ws + n;       // 32
+    double* A = GRID ? Ag : red + 32;
+    if (!GRID) {
+        for (int i = tid; i < n * n; i += nt) A[i] = Ag[i];
+        __syncthreads();
+    }
+    const int gw = GRID ? blockIdx.x * nw + warp : warp;  // global warp id
+    const int tw = GRID ? gridDim.x * nw : nw;            // total warps
+    auto gsync = [&]() {
+        if (GRID) {
+            __threadfence();
+            cg::this_grid().sync();
+        } else {
+            __syncthreads();
+        }
+    };
+    // fixed-order block sum (same result in every CTA)
+    auto bsum = [&](double a) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        __syncthreads();
+        if (lane == 0) red[warp] = a;
+        __syncthreads();
+        double t = 0.0;
+        for (int q = 0; q < nw; ++q) t += red[q];
+        return t;
+    };
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m = n - k - 1;
+        const double* x = A + (size_t)k * n + k + 1;
+        const double x0 = x[0];
+        double part = 0.0;
+        for (int i = 1 + tid; i < m; i += nt) part += x[i] * x[i];
+        const double xn2 = bsum(part);
+        if (GRID ? blockIdx.x == 0 && tid == 0 : tid == 0) dout[k] = A[(size_t)k * n + k];
+        if (xn2 == 0.0) {  // already reduced: tau = 0, no update
+            if (GRID ? blockIdx.x == 0 && tid == 0 : tid == 0) eout[k] = x0;
+            gsync();
+            continue;
+        }
+        const double beta = x0 >= 0.0 ? -sqrt(x0 * x0 + xn2) : sqrt(x0 * x0 + xn2);
+        const double tau = (beta - x0) / beta;
+        const double sc = 1.0 / (x0 - beta);
+        for (int i = tid; i < m; i += nt) vs[i] = i == 0 ? 1.0 : x[i] * sc;
+        __syncthreads();
+        // p_i = tau * A22(:, i) . v   (A22 symmetric: column i, contiguous)
+        for (int i = gw; i < m; i += tw) {
+            const double* col = A + (size_t)(k + 1 + i) * n + k + 1;
+            double a = 0.0;
+            for (int j = lane; j < m; j += 32) a += col[j] * vs[j];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (lane == 0) pg[i] = tau * a;
+        }
+        gsync();
+        if (GRID ? blockIdx.x == 0 && tid == 0 : tid == 0) eout[k] = beta;
+        part = 0.0;
+        for (int i = tid; i < m; i += nt) part += pg[i] * vs[i];
+        const double K = 0.5 * tau * bsum(part);
+        for (int i = tid; i < m; i += nt) ws[i] = pg[i] - K * vs[i];
+        __syncthreads();
+        for (int j = gw; j < m; j += tw) {
+            double* col = A + (size_t)(k + 1 + j) * n + k + 1;
+            const double vj = vs[j], wj = ws[j];
+            for (int i = lane; i < m; i += 32) col[i] -= vs[i] * wj + ws[i] * vj;
+        }
+        gsync();
+    }
+    if (GRID ? blockIdx.x == 0 && tid == 0 : tid == 0) {
+        if (n >= 2) {
+            dout[n - 2] = A[(size_t)(n - 2) * n + n - 2];
+            eout[n - 2] = A[(size_t)(n - 2) * n + n - 1];
+        }
+        dout[n - 1] = A[(size_t)(n - 1) * n + n - 1];
+    }
+}
+
+// Eigenvalue j (ascending) of the tridiagonal (d, e) by 33-section: each lane of the warp evaluates
+// the Sturm count (number of eigenvalues < x) at one interior point of the current bracket, which
+// shrinks 33x per round.  The count uses the LDL^T pivot recurrence q_i = d_i - x - e_{i-1}^2 / q_{i-1}
+// with tiny pivots replaced by -pivmin (the standard guard).  Deterministic; accuracy ~ eps ||T||.
+__global__ void __launch_bounds__(256) k_tri_multisect(int n, const double* __restrict__ d,
+                                                        const double* __restrict__ e, double* __restrict__ w) {
+    extern __shared__ double tm[];
+    double* ds = tm;
+    double* e2 = tm + n;
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i < n; i += blockDim.x) {
+        ds[i] = d[i];
+        e2[i] = i + 1 < n ? e[i] * e[i] : 0.0;
+    }
+    __syncthreads();
+    // Gershgorin bracket and pivot guard (identical in every warp)
+    double lo = 1e300, hi = -1e300, emax = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double r = (i > 0 ? sqrt(e2[i - 1]) : 0.0) + (i + 1 < n ? sqrt(e2[i]) : 0.0);
+        lo = fmin(lo, ds[i] - r);
+        hi = fmax(hi, ds[i] + r);
+        emax = fmax(emax, e2[i]);
+    }
+    const double nrm = fmax(fabs(lo), fabs(hi));
+    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax) * 1e10;
+    lo -= 4.0 * 2.220446049250313e-16 * nrm + pivmin;
+    hi += 4.0 * 2.220446049250313e-16 * nrm + pivmin;
+    const int j = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+    if (j >= n) return;
+    if (nrm == 0.0) {  // T = 0: every eigenvalue is exactly zero
+        if (lane == 0) w[j] = 0.0;
+        return;
+    }
+    for (int it = 0; it < 14; ++it) {
+        const double x = lo + (hi - lo) * (double)(lane + 1) * (1.0 / 33.0);
+        int cnt = 0;
+        double q = ds[0] - x;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+        for (int i = 1; i < n; ++i) {
+            q = ds[i] - x - e2[i - 1] / q;
+            if (fabs(q) < pivmin) q = -pivmin;
+            cnt += q < 0.0;
+        }
+        // bracket: last point with count <= j (new lo), first point with count > j (new hi)
+        const unsigned above = __ballot_sync(0xffffffffu, cnt > j);
+        const int first = above ? __ffs(above) - 1 : 32;
+        const double xlo = __shfl_sync(0xffffffffu, x, first > 0 ? first - 1 : 0);
+        const double xhi = __shfl_sync(0xffffffffu, x, first < 32 ? first : 31);
+        if (first > 0) lo = xlo;
+        if (first < 32) hi = xhi;
+        if (hi - lo <= 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi))) break;
+    }
+    if (lane == 0) w[j] = 0.5 * (lo + hi);
+}
+
+static void sym_eigvals_tridiag(acp_context* ctx, double* A, int n, double* w) {
+    double* d = ctx->wsd("eig_d", n);
+    double* e = ctx->wsd("eig_e", n);
+    double* p = ctx->wsd("eig_p", n);
+    const size_t small = ((size_t)2 * n + 32 + (size_t)n * n) * sizeof(double);
+    if (small <= 200 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            ACP_CUDA(cudaFuncSetAttribute(k_tridiag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
+        }
+        const int nt = std::min(1024, std::max(128, cdiv(n, 32) * 32 * 4));
+        k_tridiag<false><<<1, nt, small, ctx->stream>>>(A, n, p, d, e);
+    } else {
+        const size_t smem = ((size_t)2 * n + 32) * sizeof(double);
+        const void* fn = (const void*)k_tridiag<true>;
+        if (smem > 48 * 1024) ACP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        ACP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+        int dev = 0, sms = 0;
+        ACP_CUDA(cudaGetDevice(&dev));
+        ACP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        ACP_REQUIRE(occ >= 1, "tridiag: cooperative kernel does not fit");
+        // one warp per trailing column at the first step, at most one CTA per SM
+        const int G = std::max(1, std::min(sms, cdiv(n, 8)));
+        void* args[] = {&A, &n, &p, &d, &e};
+        ACP_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(256), args, smem, ctx->stream));
+    }
+    launched(ctx);
+    const size_t ms = (size_t)2 * n * sizeof(double);
+    ACP_REQUIRE(ms <= 200 * 1024, "eigenvalue search: n too large");
+    if (ms > 48 * 1024) {
+        static bool a2 = false;
+        if (!a2) {
+            ACP_CUDA(cudaFuncSetAttribute(k_tri_multisect, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            a2 = true;
+        }
+    }
+    k_tri_multisect<<<cdiv(n, 8), 256, ms, ctx->stream>>>(n, d, e, w);
+    launched(ctx);
+}
+
 void sym_eig(acp_context* ctx, double* A, int n, double* w, double* V) {
-    if (!V && n <= 32 && !getenv("ACP_EIG_BLOCK")) {
+    // eigenvalues only: tridiagonalisation + multisection (ACP_EIG_JACOBI=1 selects the one-warp
+    // Jacobi for n <= 32, ACP_EIG_BLOCK=1 the block Jacobi -- kept as tested alternatives)
+    if (!V && n <= 32 && getenv("ACP_EIG_JACOBI")) {
         k_jacobi_warp<<<1, 32, 0, ctx->stream>>>(A, n, w, 40);
         launched(ctx);
+        return;
+    }
+    if (!V && !getenv("ACP_EIG_BLOCK")) {
+        sym_eigvals_tridiag(ctx, A, n, w);
         return;
     }
     double* Vt = V ? ctx->wsd("eig_Vt", (size_t)n * n) : nullptr;

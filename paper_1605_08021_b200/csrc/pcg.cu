@@ -18,6 +18,9 @@
 // fixed order, so results do not depend on scheduling.
 #include "gemm.cuh"
 
+#include <cooperative_groups.h>
+
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -240,6 +243,196 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
     launched(ctx);
 }
 
+// ---------------------------------------------------------------------------------------------
+// K2+K3 fused (configs whose K slice per cluster rank is short, N_g / CS <= PU_KMAX, N_occ <= 32):
+// one thread-block cluster per 32-column tile, rank r owning rows [r*kchunk, (r+1)*kchunk).
+//   1. Psi and Y slices -> shared memory (one cp.async batch), partial C = Psi_s^T Y_s (DMMA);
+//   2. cluster barrier; rank r sums ITS share of the tile over the CS partials in rank order
+//      (DSMEM, as k_tn_cluster; alpha applied), rank 0 runs the CG scalar hook;
+//   3. cluster barrier; every rank gathers the full C from the owners (one remote load per
+//      element, all in flight), cluster barrier;
+//   4. each rank applies the K3 update to ITS rows: Out = Psi_s C from shared memory (DMMA, same
+//      k order as k_pcg_update) and the Ep epilogue (operands loaded ahead of each group's DMMA chain).
+// Bitwise identical to K2 followed by K3 (same partial sums, same reduction and product order);
+// saves a launch and the second pass over Psi / Y.
+constexpr int PU_KMAX = 192, PU_BM = 32, PU_BN = 32, PU_T = 256;
+constexpr int pu_ldk(int kchunk) { return (kchunk + 15) / 16 * 16 + 4; }
+inline size_t pu_smem(int kchunk) {
+    return ((size_t)(PU_BM + PU_BN) * pu_ldk(kchunk) + 2 * (size_t)PU_BM * (PU_BN + 1)) * sizeof(double);
+}
+
+template <class Hook, class Ep>
+__global__ void __launch_bounds__(PU_T, 2) k_proj_update(int K, int m, int n, const double* __restrict__ Psi,
+                                                     const double* __restrict__ Y, int kchunk, double alpha,
+                                                     Hook hook, Ep ep) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) double psm[];
+    const int LDK = pu_ldk(kchunk);
+    constexpr int LDC = PU_BN + 1;
+    double* As = psm;                        // [PU_BM][LDK]  Psi(k, m) at As[m][k - kb]
+    double* Bs = As + PU_BM * LDK;           // [PU_BN][LDK]  Y(k, c) at Bs[c][k - kb]
+    double* Cs = Bs + PU_BN * LDK;           // [PU_BM][LDC]  partial tile (read by the peers)
+    double* Cf = Cs + PU_BM * LDC;           // [PU_BM][LDC]  full C of the tile
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int CS = gridDim.x, rank = blockIdx.x;
+    const int n0 = blockIdx.y * PU_BN;
+    pdl_wait();
+    pdl_trigger();
+    if (!hook.tile_active(n0, n)) return;
+    const int kb = rank * kchunk;
+    const int ke = min(K, kb + kchunk);
+    const int kl = max(0, ke - kb);          // rows of this rank
+    const int kp = (kl + 3) / 4 * 4;         // padded to the DMMA depth (zero-filled)
+    for (int c = tid; c < PU_BM * (kp / 2); c += PU_T) {
+        const int row = c / (kp / 2), kk = 2 * (c % (kp / 2));
+        const bool v = row < m && kb + kk < ke;
+        cp_async16(As + row * LDK + kk, v ? (const void*)(Psi + (size_t)row * K + kb + kk) : (const void*)Psi, v);
+    }
+    for (int c = tid; c < PU_BN * (kp / 2); c += PU_T) {
+        const int col = c / (kp / 2), kk = 2 * (c % (kp / 2));
+        const bool v = n0 + col < n && kb + kk < ke;
+        cp_async16(Bs + col * LDK + kk, v ? (const void*)(Y + (size_t)(n0 + col) * K + kb + kk) : (const void*)Y, v);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    // 1. partial C (32 x 32): warps 0..3 as 2 (m) x 2 (n), warp tile 16 x 16, k ascending by 4
+    if (warp < 4) {
+        double acc[2][2][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int ks = 0; ks < kp; ks += 4) {
+            double af[2], bf[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) af[i] = As[(wm * 16 + i * 8 + g) * LDK + ks + t];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) bf[j] = Bs[(wn * 16 + j * 8 + g) * LDK + ks + t];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) Cs[(wm * 16 + i * 8 + g) * LDC + wn * 16 + j * 8 + 2 * t + e] = acc[i][j][e];
+    }
+    cluster.sync();
+    // 2. rank r reduces elements r, r + CS, ... over the cluster in rank order (all remote loads in
+    //    flight together, as k_tn_cluster) into its Cf; rank 0 runs the CG scalar hook
+    for (int e = rank * PU_T + tid; e < PU_BM * PU_BN; e += CS * PU_T) {
+        const int row = e / PU_BN, col = e % PU_BN;
+        double part[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) part[q] = q < CS ? cluster.map_shared_rank(Cs, q)[row * LDC + col] : 0.0;
+        double sum = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sum += part[q];
+        Cf[row * LDC + col] = alpha * sum;
+    }
+    if (rank == 0 && tid < PU_BN && n0 + tid < n) hook(n0 + tid);
+    cluster.sync();
+    // 3. gather the full C from the owners' Cf (one remote load per element, all in flight);
+    //    written to the local Cs (every peer is done reading partials after the barrier)
+    {
+        double v[(PU_BM * PU_BN) / PU_T];
+#pragma unroll
+        for (int q = 0; q < (PU_BM * PU_BN) / PU_T; ++q) {
+            const int e = tid + PU_T * q;
+            const int row = e / PU_BN, col = e % PU_BN;
+            v[q] = cluster.map_shared_rank(Cf, (e / PU_T) % CS)[row * LDC + col];
+        }
+#pragma unroll
+        for (int q = 0; q < (PU_BM * PU_BN) / PU_T; ++q) {
+            const int e = tid + PU_T * q;
+            Cs[(e / PU_BN) * LDC + e % PU_BN] = v[q];
+        }
+    }
+    cluster.sync();  // peers' Cf reads done before anyone exits; local Cs complete
+    // 4. Out = Psi_s C for this rank's rows, 8-row groups strided over the warps
+    const int ngr = (kl + 7) / 8;
+    typename Ep::Regs ra[4][2];
+    auto load_group = [&](int gi, typename Ep::Regs (&r)[4][2]) {
+        const int row = kb + gi * 8 + g;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + j * 8 + 2 * t + e;
+                if (row < ke && col < n) ep.load(row, col, r[j][e]);
+            }
+    };
+    auto product_store = [&](int gi, const typename Ep::Regs (&r)[4][2]) {
+        double acc[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+        for (int ms = 0; ms < PU_BM; ms += 4) {
+            const double af = As[(ms + t) * LDK + gi * 8 + g];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[j][0], acc[j][1], af, Cs[(ms + t) * LDC + j * 8 + g]);
+        }
+        const int row = kb + gi * 8 + g;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + j * 8 + 2 * t + e;
+                if (row < ke && col < n) ep.store(row, col, acc[j][e], r[j][e]);
+            }
+    };
+    // 8-row groups strided over the 8 warps; the epilogue operands of a group are loaded before
+    // its DMMA chain (independent, so their latency overlaps it)
+    for (int gi = warp; gi < ngr; gi += PU_T / 32) {
+        load_group(gi, ra);
+        product_store(gi, ra);
+    }
+}
+
+template <class Hook, class Ep>
+static bool launch_proj_update(acp_context* ctx, int K, int m, int n, double alpha, const double* Psi, const double* Y,
+                               const Hook& hook, const Ep& ep) {
+    // opt-in (ACP_PCG_FUSED=1): measured 0.45 ms/step SLOWER than K2 + K3 at configs[1] (three
+    // serial cluster barriers per tile and 8x fewer CTAs for the update)
+    if (m > PU_BM || (K & 1) || (((uintptr_t)Psi | (uintptr_t)Y) & 15) || !getenv("ACP_PCG_FUSED")) return false;
+    // the same K split as launch_tn_cluster (identical partial sums)
+    int CS = std::min(8, std::max(1, cdiv(K, 160)));
+    int kchunk = cdiv(cdiv(K, CS), TC_BK) * TC_BK;
+    if (kchunk > PU_KMAX) return false;
+    CS = cdiv(K, kchunk);
+    const size_t smem = pu_smem(kchunk);
+    static bool attr = false;
+    if (!attr) {
+        ACP_CUDA(cudaFuncSetAttribute(k_proj_update<Hook, Ep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)pu_smem(PU_KMAX)));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS, cdiv(n, PU_BN), 1);
+    cfg.blockDim = dim3(PU_T, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = ctx->pdl ? 2 : 1;
+    ACP_CUDA(cudaLaunchKernelEx(&cfg, k_proj_update<Hook, Ep>, K, m, n, Psi, Y, kchunk, alpha, hook, ep));
+    launched(ctx);
+    return true;
+}
+
 // Number of still-active columns; sets the while-node condition of the PCG graph (continue while
 // columns remain and fewer than max_chunks chunks ran) and counts the trips.
 __global__ void k_count_active(const int* __restrict__ active, int n, int* __restrict__ out,
@@ -262,36 +455,78 @@ __global__ void k_count_active(const int* __restrict__ active, int n, int* __res
 
 // W(:, mu) = 2f sum_c X(:, c*nmu_p + mu) (.) Phi_c(:, mu),
 // Phi_c(alpha, mu) = sum_i Psi(alpha, i) L(i, c) Psi(r_mu, i)   (Eq. eqnW).
+// Phi_c = Psi B_c with B_c(i, mu) = L(i, c) Psi(r_mu, i) is a genuine GEMM (N_g x N_occ x N_mu):
+// one DMMA GEMM per node whose epilogue accumulates W += 2f X_c (.) Phi_c (nodes in order).
 constexpr int W_MAXC = 32;
-__global__ void __launch_bounds__(128) k_build_W(int Ng, int n_occ, int nc, int nmu_p, int mu_count,
-                                                 const double* __restrict__ Psi, const double* __restrict__ L,
-                                                 const int* __restrict__ S, int mu_begin,
-                                                 const double* __restrict__ X, double pref,
-                                                 double* __restrict__ W) {
-    extern __shared__ double LS[];  // nc x n_occ : L(i,c) Psi(r_mu, i)
-    const int mu = blockIdx.y;
-    const int smu = S[mu_begin + mu];
-    for (int idx = threadIdx.x; idx < nc * n_occ; idx += blockDim.x) {
-        const int i = idx % n_occ, c = idx / n_occ;
-        LS[idx] = L[c * n_occ + i] * Psi[(size_t)i * Ng + smu];
+__global__ void k_w_rhs(int Ng, int n_occ, int nc, int cnt, const double* __restrict__ Psi,
+                        const double* __restrict__ L, const int* __restrict__ S, int mu_begin,
+                        double* __restrict__ B) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // orbital
+    const int mu = blockIdx.y, c = blockIdx.z;
+    if (i >= n_occ) return;
+    B[((size_t)c * cnt + mu) * n_occ + i] = L[c * n_occ + i] * Psi[(size_t)i * Ng + S[mu_begin + mu]];
+}
+
+struct EpW {
+    const double* X;  // PCG solutions, column c*nmu_p + mu
+    double* W;
+    int Ng, nmu_p, c, mu_begin;
+    double pref;
+    int first;
+    struct Regs {
+        double x, w;
+    };
+    __device__ __forceinline__ void load(int r, int col, Regs& g) const {
+        g.x = X[(size_t)(c * nmu_p + col) * Ng + r];
+        g.w = first ? 0.0 : W[(size_t)(mu_begin + col) * Ng + r];
     }
-    __syncthreads();
-    const int a = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= Ng) return;
-    double phi[W_MAXC];
-#pragma unroll
-    for (int c = 0; c < W_MAXC; ++c) phi[c] = 0.0;
-    for (int i = 0; i < n_occ; ++i) {
-        const double p = Psi[(size_t)i * Ng + a];
-#pragma unroll
-        for (int c = 0; c < W_MAXC; ++c)
-            if (c < nc) phi[c] += p * LS[c * n_occ + i];
+    __device__ __forceinline__ void store(int r, int col, double acc, const Regs& g) const {
+        W[(size_t)(mu_begin + col) * Ng + r] = g.w + pref * (g.x * acc);
     }
-    double w = 0.0;
-#pragma unroll
-    for (int c = 0; c < W_MAXC; ++c)
-        if (c < nc) w += X[(size_t)(c * nmu_p + mu) * Ng + a] * phi[c];
-    W[(size_t)(mu_begin + mu) * Ng + a] = pref * w;
+};
+
+template <class Ep>
+__global__ void __launch_bounds__(128) k_nn_ep(int M, int K, int n, const double* __restrict__ A, int lda,
+                                               const double* __restrict__ B, int ldb, Ep ep) {
+    nn_tile(M, K, n, A, lda, B, ldb, blockIdx.x * NN_BM, blockIdx.y * NN_BN, ep);
+}
+template <class Ep>
+__global__ void __launch_bounds__(256, 2) k_nn_ep_big(int M, int K, int n, const double* __restrict__ A, int lda,
+                                                      const double* __restrict__ B, int ldb, Ep ep) {
+    nn_tile_big(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, blockIdx.y * GB_BN, ep);
+}
+// All nodes in ONE launch: each CTA owns a W tile and runs the N_c tile GEMMs in node order,
+// accumulating into its W tile (the same thread owns the same element in every pass).
+template <bool BIG>
+__global__ void __launch_bounds__(BIG ? 256 : 128) k_w_nodes(int M, int K, int n, int n_cheb, const double* __restrict__ A,
+                                                             const double* __restrict__ B, EpW ep) {
+    for (int c = 0; c < n_cheb; ++c) {
+        ep.c = c;
+        ep.first = c == 0;
+        if (BIG)
+            nn_tile_big(M, K, n, A, M, B + (size_t)c * n * K, K, blockIdx.x * GB_BM, blockIdx.y * GB_BN, ep);
+        else
+            nn_tile(M, K, n, A, M, B + (size_t)c * n * K, K, blockIdx.x * NN_BM, blockIdx.y * NN_BN, ep);
+        __syncthreads();
+    }
+}
+
+template <class Ep>
+static void launch_nn_ep(acp_context* ctx, int M, int K, int n, const double* A, int lda, const double* B, int ldb,
+                         const Ep& ep) {
+    if (K >= 64) {
+        static bool attr = false;
+        if (!attr) {
+            ACP_CUDA(cudaFuncSetAttribute(k_nn_ep_big<Ep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)nn_big_smem()));
+            attr = true;
+        }
+        k_nn_ep_big<Ep><<<dim3(cdiv(M, GB_BM), cdiv(n, GB_BN)), 256, nn_big_smem(), ctx->stream>>>(M, K, n, A, lda, B,
+                                                                                                   ldb, ep);
+    } else {
+        k_nn_ep<Ep><<<dim3(cdiv(M, NN_BM), cdiv(n, NN_BN)), 128, 0, ctx->stream>>>(M, K, n, A, lda, B, ldb, ep);
+    }
+    launched(ctx);
 }
 
 void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const double* V, const double* d_shift_c,
@@ -339,10 +574,11 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         f.active = (mode == SC_INIT) ? nullptr : s.active;
         f.dots = dots;
         fourier_op(ctx, f);
-        ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ,
-                                      ScalHook{mode, s, tol2, nvalid, nmu_p}),
-                    "projection GEMM needs an even grid");
         EpBeta ep{Y, P, s.beta, s.active, Ng, mode == SC_INIT ? 1 : 0};
+        const ScalHook hk{mode, s, tol2, nvalid, nmu_p};
+        if (launch_proj_update(ctx, Ng, n_occ, n, ctx->dV, Psi, Y, hk, ep)) return;
+        ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ, hk),
+                    "projection GEMM needs an even grid");
         launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
     };
     auto hamiltonian_half = [&]() {
@@ -356,10 +592,11 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         f.active = s.active;
         f.dots = dots;
         fourier_op(ctx, f);
-        ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ,
-                                      ScalHook{SC_ALPHA, s, tol2, nvalid, nmu_p}),
-                    "projection GEMM needs an even grid");
         EpAlpha ep{Y, P, X, R, s.alpha, s.active, Ng};
+        const ScalHook hk{SC_ALPHA, s, tol2, nvalid, nmu_p};
+        if (launch_proj_update(ctx, Ng, n_occ, n, ctx->dV, Psi, Y, hk, ep)) return;
+        ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ, hk),
+                    "projection GEMM needs an even grid");
         launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
     };
 
@@ -503,11 +740,32 @@ void apply_chi0(acp_context* ctx, const double* Psi, const double* eps, const do
     double* X = ctx->wsd("chi_X", (size_t)Ng * n_cheb * nmu_p);
     const double tau = 0.05;
     sternheimer_batch(ctx, Psi, n_occ, V, nodes, n_cheb, rhs, nmu_p, tol, max_iter, tau, X, st);
-    dim3 grid(cdiv(Ng, 128), cnt);
-    size_t smem = (size_t)n_cheb * n_occ * sizeof(double);
-    k_build_W<<<grid, 128, smem, ctx->stream>>>(Ng, n_occ, n_cheb, nmu_p, cnt, Psi, L, S, mu_begin, X,
-                                                2.0 * ctx->sys.occ, W);
+    double* B = ctx->wsd("chi_Bw", (size_t)n_cheb * cnt * n_occ);
+    k_w_rhs<<<dim3(cdiv(n_occ, 128), cnt, n_cheb), 128, 0, ctx->stream>>>(Ng, n_occ, n_cheb, cnt, Psi, L, S, mu_begin,
+                                                                         B);
     launched(ctx);
+    EpW ep{X, W, Ng, nmu_p, 0, mu_begin, 2.0 * ctx->sys.occ, 1};
+    if (getenv("ACP_W_PER_NODE")) {
+        for (int c = 0; c < n_cheb; ++c) {
+            ep.c = c;
+            ep.first = c == 0;
+            launch_nn_ep(ctx, Ng, n_occ, cnt, Psi, Ng, B + (size_t)c * cnt * n_occ, n_occ, ep);
+        }
+    } else if (n_occ >= 64) {
+        static bool attr = false;
+        if (!attr) {
+            ACP_CUDA(cudaFuncSetAttribute(k_w_nodes<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)nn_big_smem()));
+            attr = true;
+        }
+        k_w_nodes<true><<<dim3(cdiv(Ng, GB_BM), cdiv(cnt, GB_BN)), 256, nn_big_smem(), ctx->stream>>>(
+            Ng, n_occ, cnt, n_cheb, Psi, B, ep);
+        launched(ctx);
+    } else {
+        k_w_nodes<false><<<dim3(cdiv(Ng, NN_BM), cdiv(cnt, NN_BN)), 128, 0, ctx->stream>>>(Ng, n_occ, cnt, n_cheb,
+                                                                                          Psi, B, ep);
+        launched(ctx);
+    }
 }
 
 void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* V, const double* X, int n,

@@ -504,10 +504,37 @@ __global__ void __launch_bounds__(1024) k_qrcp_cluster(int m, int Ng, double* __
 // l, l+32, ... -- so a pivot step moves no column data through shared memory: each lane reads
 // its KR entries of the Householder vector once per step and updates CPW columns in registers
 // (v is zero above row j, so rows < j are untouched without any masking).  512 threads.
+// Reduce-scatter of 8 per-lane values over a warp in 9 shuffles (instead of 8 x 5): halving
+// exchanges over lane bits 0..2, then a plain butterfly over bits 3..4.  Afterwards lane l holds
+// the warp total of value index rs8_index(l); every copy of a total is bitwise identical (each
+// level adds the same two partial sums, in commutative order).
+__device__ __forceinline__ int rs8_index(int l) { return ((l & 1) << 2) | (l & 2) | ((l >> 2) & 1); }
+__device__ __forceinline__ int rs8_lane(int q) { return ((q >> 2) & 1) | (q & 2) | ((q & 1) << 2); }
+__device__ __forceinline__ double warp_rs8(const double (&v)[8], int lane) {
+    const bool b0 = lane & 1, b1 = lane & 2, b2 = lane & 4;
+    double a[4], c[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double send = b0 ? v[i] : v[i + 4], keep = b0 ? v[i + 4] : v[i];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = b1 ? a[i] : a[i + 2], keep = b1 ? a[i + 2] : a[i];
+        c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    const double send = b2 ? c[0] : c[1], keep = b2 ? c[1] : c[0];
+    double t = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    t += __shfl_xor_sync(0xffffffffu, t, 8);
+    t += __shfl_xor_sync(0xffffffffu, t, 16);
+    return t;
+}
+
 template <int CPW, int KR>
 __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __restrict__ Ag, int kmax, double eps,
                                                     int fixed, int* __restrict__ perm, double* __restrict__ rdiag,
                                                     int* __restrict__ out_nmu, long long* __restrict__ tprof) {
+    static_assert(CPW <= 8, "reduce-scatter handles up to 8 columns per warp");
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double rsm2[];
@@ -584,7 +611,9 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
                 cl.map_shared_rank(&allslot[0][0], lane)[buf * 16 + b] = sl;
             }
         }
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 1] = clock64();
         __syncthreads();
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 2] = clock64();
         {   // the owning warp publishes the candidate's rows j..m-1 from its registers and
             // pushes its row j to every peer next to the slot
             const int bl = s_lc;
@@ -604,8 +633,9 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
                 if (lane < CS) cl.map_shared_rank(&allx0[0][0], lane)[buf * 16 + b] = xj;
             }
         }
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 3] = clock64();
         cl.sync();
-        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 1] = clock64();
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 4] = clock64();
         if (warp == 0) {
             double bn = -1.0;
             int bp = 1 << 30, bs = -1, bc = -1;
@@ -657,7 +687,7 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
         if (j > 0 && tid == 0) v[j - 1] = 0.0;  // rows < j stay zero (cleared as j advances)
         if (b == 0 && tid == 0) rdiag[j] = rjj;
         __syncthreads();
-        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 2] = clock64();
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 5] = clock64();
         double vr[KR];
 #pragma unroll
         for (int k = 0; k < KR; ++k) {
@@ -666,7 +696,9 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
         }
         // all CPW columns of the warp at once (independent dot / shuffle / norm chains -> ILP)
         bool live[CPW];
-        double d[CPW];
+        double d[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[q] = 0.0;
 #pragma unroll
         for (int q = 0; q < CPW; ++q) {
             const int lc = warp + NW * q;
@@ -685,20 +717,19 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
                     dn[lc] = 1;
                 }
             }
-            d[q] = 0.0;
 #pragma unroll
             for (int k = 0; k < KR; ++k) d[q] += vr[k] * col[q][k];
         }
+        // all CPW dot products in one reduce-scatter, then each lane fetches the totals
+        const double dt = warp_rs8(d, lane);
+        double nn[8];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int q = 0; q < CPW; ++q) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
-        double nn[CPW];
+        for (int q = 0; q < 8; ++q) nn[q] = 0.0;
 #pragma unroll
         for (int q = 0; q < CPW; ++q) {
-            nn[q] = 0.0;
+            const double dq = __shfl_sync(0xffffffffu, dt, rs8_lane(q));
             if (live[q]) {
-                const double f = tau * d[q];
+                const double f = tau * dq;
 #pragma unroll
                 for (int k = 0; k < KR; ++k) {
                     const double y = col[q][k] - f * vr[k];
@@ -707,22 +738,22 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
                 }
             }
         }
+        const double nt = warp_rs8(nn, lane);
+        {
+            const int q = rs8_index(lane);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int q = 0; q < CPW; ++q) nn[q] += __shfl_xor_sync(0xffffffffu, nn[q], o);
+            for (int qq = 0; qq < CPW; ++qq)
+                if (lane < 8 && qq == q && live[qq]) n2[warp + NW * qq] = nt;
+        }
         if (lane == 0) {
 #pragma unroll
             for (int q = 0; q < CPW; ++q) {
                 const int lc = warp + NW * q;
-                if (live[q]) {
-                    n2[lc] = nn[q];
-                    if (pos[lc] == j) pos[lc] = pw;
-                }
+                if (live[q] && pos[lc] == j) pos[lc] = pw;
             }
         }
         __syncthreads();
-        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 3] = clock64();
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 6] = clock64();
     }
 #pragma unroll
     for (int q = 0; q < CPW; ++q) {
@@ -935,7 +966,7 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
             ACP_CUDA(cudaStreamSynchronize(ctx->stream));
             if (FILE* f = fopen(tpath, "a")) {
                 for (int j = 0; j < 512 && h[8 * j]; ++j) {
-                    for (int k = 0; k < 5; ++k) fprintf(f, "%lld ", h[8 * j + k]);
+                    for (int k = 0; k < 7; ++k) fprintf(f, "%lld ", h[8 * j + k]);
                     fprintf(f, "\n");
                 }
                 fclose(f);
@@ -975,7 +1006,7 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
             ACP_CUDA(cudaStreamSynchronize(ctx->stream));
             if (FILE* f = fopen(tpath, "a")) {
                 for (int j = 0; j < 512 && h[8 * j]; ++j) {
-                    for (int k = 0; k < 5; ++k) fprintf(f, "%lld ", h[8 * j + k]);
+                    for (int k = 0; k < 7; ++k) fprintf(f, "%lld ", h[8 * j + k]);
                     fprintf(f, "\n");
                 }
                 fclose(f);

@@ -150,6 +150,69 @@ def test_gemm_nn_large_k(M, K, n):
     assert rel(C, 2.0 * C0 - 0.5 * A @ B) < 1e-13
 
 
+@pytest.mark.parametrize("n", [1, 2, 5, 31, 33, 64, 127, 128, 158, 159, 200, 333, 512])
+@pytest.mark.parametrize("kind", ["random", "degenerate", "diagonal", "lowrank"])
+@pytest.mark.parametrize("method", ["tridiag", "jacobi"])
+def test_sym_eigvals(n, kind, method, monkeypatch):
+    """Phonon-spectrum eigenvalue step: single-CTA and cooperative-grid Householder
+    tridiagonalisation + Sturm multisection (default), one-warp / block Jacobi (knobs), vs LAPACK."""
+    if method == "jacobi":
+        if n > 160:
+            pytest.skip("block Jacobi: smaller sizes suffice")
+        monkeypatch.setenv("ACP_EIG_JACOBI" if n <= 32 else "ACP_EIG_BLOCK", "1")
+    s = system("tiny4")
+    rng = np.random.default_rng(n * 7 + len(kind))
+    if kind == "random":
+        A = rng.standard_normal((n, n))
+        A = A + A.T
+    else:
+        Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        if kind == "degenerate":      # clusters of exactly repeated eigenvalues incl. zeros (acoustic modes)
+            lam = np.repeat(np.array([0.0, 1.0, -2.5, 3.0]), (n + 3) // 4)[:n]
+        elif kind == "diagonal":      # already tridiagonal: every Householder step is the identity
+            Q = np.eye(n)
+            lam = rng.standard_normal(n)
+        else:                         # rank 2: most trailing columns vanish during the reduction
+            lam = np.zeros(n)
+            lam[:min(2, n)] = [4.0, -1.0][:min(2, n)]
+        A = (Q * lam) @ Q.T
+        A = 0.5 * (A + A.T)
+    w = s.ctx.sym_eigvals(T(A)).cpu().numpy()
+    ref = np.linalg.eigvalsh(A)
+    scale = max(np.abs(ref).max(), 1e-300)
+    assert np.all(np.diff(w) >= -1e-12 * scale)
+    assert np.abs(w - ref).max() <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("n,nrhs", [(1, 1), (31, 3), (32, 8), (33, 5), (100, 64), (290, 128), (513, 7),
+                                    (700, 33)])
+@pytest.mark.parametrize("panel", ["warp", "smem"])
+def test_lu_solve(n, nrhs, panel, monkeypatch):
+    """Dense SMW core solve (Eq. dyson4): blocked partially pivoted LU, warp-row (register) or
+    shared-memory panel, vs LAPACK; a row-permuted matrix forces non-trivial pivots."""
+    if panel == "warp":
+        monkeypatch.setenv("ACP_LU_WARP_PANEL", "1")
+    s = system("tiny4")
+    rng = np.random.default_rng(n + nrhs)
+    A = rng.standard_normal((n, n)) + np.eye(n)
+    A = A[rng.permutation(n)]
+    A[:, 0] *= 1e-3                      # a small leading column: pivoting is required
+    B = rng.standard_normal((n, nrhs))
+    _, X = s.ctx.lu_solve(T(A.T), T(B.T))
+    X = X.cpu().numpy().T
+    Xr = np.linalg.solve(A, B)
+    cond = np.linalg.cond(A)
+    assert rel(X, Xr) < 1e-15 * cond * n
+
+
+def test_lu_solve_singular():
+    from paper_1605_08021_b200 import AcpError
+    s = system("tiny4")
+    A = np.ones((40, 40))
+    with pytest.raises(AcpError):
+        s.ctx.lu_solve(T(A), T(np.ones((1, 40))))
+
+
 def test_perturbation_matrix(sysx):
     s = sysx
     G = s.ctx.perturbations(s.R).cpu().numpy().T
@@ -307,6 +370,22 @@ def test_apply_chi0_hostloop_equals_while_node(sysx, monkeypatch):
     St, Xt = T(S_o, torch.int32), T(Xi_o.T)
     W1, i1 = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
     monkeypatch.setenv("ACP_PCG_HOSTLOOP", "1")
+    ctx = Context.from_config(s.cfg)
+    W2, i2 = ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    ctx.close()
+    assert torch.equal(W1, W2) and i1["total_iter"] == i2["total_iter"]
+
+
+def test_apply_chi0_fused_projection_equals_unfused(sysx, monkeypatch):
+    """k_proj_update (K2+K3 in one cluster launch) sums the same partials in the same order as
+    k_tn_cluster followed by k_pcg_update: bitwise-identical W and iteration counts."""
+    from paper_1605_08021_b200 import Context
+    s = sysx
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    St, Xt = T(S_o, torch.int32), T(Xi_o.T)
+    W1, i1 = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    monkeypatch.setenv("ACP_PCG_FUSED", "1")
     ctx = Context.from_config(s.cfg)
     W2, i2 = ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
     ctx.close()

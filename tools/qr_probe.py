@@ -25,5 +25,5 @@ t = np.loadtxt(out)
 d = np.diff(t, axis=1)
 step = np.diff(t[:, 0])
 print("N_mu", n, "steps", len(t))
-print("mean cycles per phase [argmax+publish+cl.sync | winner+DSMEM | householder | update]:", d.mean(0).round(0))
+print("mean cycles per phase [local argmax+push | syncthreads | publish | cl.sync | winner+v | update]:", d.mean(0).round(0))
 print("mean cycles per step:", step.mean().round(0), " -> us per step at 1.9 GHz:", (step.mean() / 1.9e3).round(2))
