@@ -99,7 +99,15 @@ struct acp_context {
     void* ws(const std::string& name, size_t bytes) {
         acp::DevBuf& b = bufs[name];
         if (b.bytes < bytes) {
-            if (b.ptr) cudaFree(b.ptr);
+            // a cached graph may hold this buffer's old address (and a later allocation may reuse
+            // it, so pointer-keyed lookups cannot tell): drop every cached graph on reallocation
+            if (b.ptr) {
+                cudaStreamSynchronize(stream);
+                for (auto& kv : graphs)
+                    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+                graphs.clear();
+                cudaFree(b.ptr);
+            }
             b.ptr = nullptr;
             b.bytes = 0;
             size_t nb = bytes < 256 ? 256 : bytes;

@@ -120,7 +120,55 @@ __device__ __forceinline__ void qr_update_cols(ColP colp, int warp, int nc, int 
     }
 }
 
-template <bool SMEM>
+// Global-memory variant for long columns (m <= 32*KR): ONE warp per column with the column's
+// trailing rows in registers (lane l: rows l, l+32, ...), so a step reads and writes each column
+// once with KR independent loads in flight per lane -- the 16-lane version above re-reads the
+// column for the update and keeps too few loads in flight to reach HBM bandwidth.
+template <int KR, class ColP>
+__device__ __forceinline__ void qr_update_cols_warp(ColP colp, int warp, int nc, int c0, int cw, int j, int m,
+                                                    double alpha, double tau, const double* __restrict__ v,
+                                                    const int* __restrict__ dn, double* __restrict__ n2) {
+    const int nwarp = blockDim.x >> 5, lane = threadIdx.x & 31;
+    for (int lc = warp; lc < nc; lc += nwarp) {
+        const bool piv = c0 + lc == cw;
+        const bool live = !piv && !dn[lc];
+        double* c = colp(lc);
+        if (live) {
+            double y[KR];
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int i = lane + 32 * k;
+                y[k] = (i >= j && i < m) ? c[i] : 0.0;
+            }
+            double d = 0.0;
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int i = lane + 32 * k;
+                if (i >= j && i < m) d += v[i] * y[k];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            const double f = tau * d;
+            double nn = 0.0;
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int i = lane + 32 * k;
+                if (i >= j && i < m) {
+                    const double yy = y[k] - f * v[i];
+                    c[i] = yy;
+                    if (i > j) nn += yy * yy;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+            if (lane == 0) n2[lc] = nn;
+        } else if (piv) {
+            for (int i = j + lane; i < m; i += 32) c[i] = (i == j) ? alpha : 0.0;
+        }
+    }
+}
+
+template <bool SMEM, int KR>
 __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* __restrict__ Ag, int kmax, double eps,
                                                          int fixed, QrSlot* __restrict__ slots,
                                                          double* __restrict__ cand, int* __restrict__ perm,
@@ -290,7 +338,10 @@ __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* 
         }
         __syncthreads();
         // ---- trailing update of the remaining owned columns (16 threads per column)
-        qr_update_cols(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
+        if (KR > 0)
+            qr_update_cols_warp<(KR > 0 ? KR : 1)>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
+        else
+            qr_update_cols(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
         __syncthreads();
     }
     if (SMEM)
@@ -1019,13 +1070,18 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
         G = cdiv(Ng, cpb);
         const size_t tail = (size_t)m * sizeof(double) + (size_t)cpb * (sizeof(double) + 2 * sizeof(int)) + 64;
         const size_t smem_full = (size_t)cpb * m * sizeof(double) + tail;
-        const bool use_smem = smem_full <= 200 * 1024;
+        const bool use_smem = smem_full <= 200 * 1024 && !getenv("ACP_QRCP_NOSMEM");  // knob: tests
         const size_t smem = use_smem ? smem_full : tail;
         QrSlot* slots = static_cast<QrSlot*>(ctx->ws("qr_slots", 2 * (size_t)G * sizeof(QrSlot)));
         double* cand = ctx->wsd("qr_cand", 2 * (size_t)G * m);
         void* args[] = {(void*)&m, (void*)&Ng, (void*)&A, (void*)&kmax, (void*)&id_eps, (void*)&n_fixed,
                         (void*)&slots, (void*)&cand, (void*)&perm, (void*)&rdiag, (void*)&d_nmu};
-        const void* fn = use_smem ? (const void*)k_qrcp_persistent<true> : (const void*)k_qrcp_persistent<false>;
+        // global-memory columns: one warp per column, rows in registers, when m <= 2048
+        const int kr = (use_smem || getenv("ACP_QRCP_GRID16")) ? 0 : m <= 1024 ? 32 : m <= 2048 ? 64 : 0;
+        const void* fn = use_smem ? (const void*)k_qrcp_persistent<true, 0>
+                         : kr == 32 ? (const void*)k_qrcp_persistent<false, 32>
+                         : kr == 64 ? (const void*)k_qrcp_persistent<false, 64>
+                                    : (const void*)k_qrcp_persistent<false, 0>;
         ACP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
         ACP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));

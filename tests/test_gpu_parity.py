@@ -237,16 +237,19 @@ def test_compress_pivots_bit_exact(sysx):
         assert rel(Xi_g2.cpu().numpy().T, Xi_o2) < 1e-9
 
 
-@pytest.mark.parametrize("knob", ["ACP_QRCP_GRID", "ACP_QRCP_SMEM"])
+@pytest.mark.parametrize("knob", ["ACP_QRCP_GRID", "ACP_QRCP_SMEM", "ACP_QRCP_GRID+ACP_QRCP_NOSMEM",
+                                  "ACP_QRCP_GRID+ACP_QRCP_NOSMEM+ACP_QRCP_GRID16"])
 def test_compress_alternative_qrcp_kernels_agree(sysx, monkeypatch, knob):
-    """The three QRCP kernels -- register-resident cluster (default for small problems),
-    shared-memory cluster (ACP_QRCP_SMEM) and grid-wide persistent (ACP_QRCP_GRID) -- pick the
-    same pivots and agree with the oracle."""
+    """The QRCP kernels -- register-resident cluster (default for small problems), shared-memory
+    cluster (ACP_QRCP_SMEM) and grid-wide persistent (ACP_QRCP_GRID; columns in shared memory, or
+    in global memory with one warp per column (default for large m) or 16 lanes per column) --
+    pick the same pivots and agree with the oracle."""
     from paper_1605_08021_b200 import Context
     s = sysx
     th, nu = s.draws(0, s.G.shape[1])
     S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
-    monkeypatch.setenv(knob, "1")
+    for k in knob.split("+"):
+        monkeypatch.setenv(k, "1")
     ctx = Context.from_config(s.cfg)
     S_g, Xi_g, n = ctx.compress(s.Psi_t, s.G_t, th, nu, id_eps=s.cfg.id_eps)
     ctx.close()
