@@ -133,10 +133,26 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Record one kernel launch (call right after <<<>>>); checks launch errors.
-inline void launched(acp_context* ctx, int n = 1) {
+// Debug knob ACP_SYNC_CHECK=1: synchronise after every launch outside stream capture, so a
+// faulting kernel is reported at its own launch site (with ACP_PCG_NOGRAPH=1 for the PCG loop).
+#define launched(ctx, ...) launched_at(ctx, __FILE__, __LINE__, ##__VA_ARGS__)
+inline void launched_at(acp_context* ctx, const char* file, int line, int n = 1) {
     ctx->launches += n;
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) throw Error(ACP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess)
+        throw Error(ACP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e) + " @" + file + ":" +
+                                      std::to_string(line));
+    static const bool chk = getenv("ACP_SYNC_CHECK") != nullptr;
+    if (chk) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(ctx->stream, &cs);
+        if (cs == cudaStreamCaptureStatusNone) {
+            e = cudaStreamSynchronize(ctx->stream);
+            if (e != cudaSuccess)
+                throw Error(ACP_ERR_CUDA, std::string("kernel execution: ") + cudaGetErrorString(e) + " @" + file +
+                                              ":" + std::to_string(line));
+        }
+    }
 }
 
 inline void sync(acp_context* ctx) { ACP_CUDA(cudaStreamSynchronize(ctx->stream)); }
@@ -200,6 +216,8 @@ struct FopArgs {
 };
 // Y = IFFT(mult * FFT(X)) + (diag - shift_j) (.) X, two real columns per complex FFT.
 void fourier_op(acp_context* ctx, const FopArgs& a);
+// Pre-allocate fourier_op's workspace for n columns (call before capturing it into a graph).
+void fourier_reserve(acp_context* ctx, int n);
 // Fill ctx->d_mult with a multiplier of the given kind (scaled by 1/N); returns it.
 const double* multiplier(acp_context* ctx, MultKind kind, double tau);
 // Real grid functions from Hermitian spectra given as complex coefficients per bin:

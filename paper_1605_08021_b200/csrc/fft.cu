@@ -565,7 +565,197 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
     }
 }
 
+// ============================================================================ 2D, three passes
+// K1 for 2D grids as three grid-wide passes through an HBM/L2 intermediate Z (one complex field
+// per column pair, layout [i0][k1]) instead of one thread-block cluster per pair: the cluster
+// kernel spends its time in cluster barriers and index arithmetic (ncu, profiles/r1zu), while
+// each pass here is a plain batched 1D FFT with coalesced 8-column / 8-row tiles.
+//   A  rows:    Z[i0][.] = FFT_row(x0 + i x1)               (RB = 8 rows of one pair per CTA)
+//   B  columns: Z[.][k1] = FFT_col(conj(m (.) FFT_col(Z)))  (CB = 8 columns of one pair per CTA)
+//   C  rows:    y = conj(FFT_row(Z)) + (V - shift) x, per-CTA partial dots; k_f2_dots sums the
+//               partials of a column in row-block order (fixed order, deterministic).
+// Same transform and inverse-by-conjugation as k_fft2d; different rounding order.
+constexpr int F2_RB = 8, F2_CB = 8;  // 8 x n values per CTA: <= 256 threads, 3 CTAs/SM
+
+__device__ __forceinline__ bool f2_pair_active(const FopArgs& a, int c0) {
+    const bool h1 = c0 + 1 < a.n;
+    return !a.active || a.active[c0] || (h1 && a.active[c0 + 1]);
+}
+
+template <int EPT>
+__global__ void __launch_bounds__(256, 3) k_f2_rows_fwd(FftGeom G, const double2* __restrict__ twg, FopArgs a,
+                                                     double2* __restrict__ Z, int pair0) {
+    extern __shared__ __align__(16) double2 f2s[];
+    const int pr = pair0 + blockIdx.y, c0 = 2 * pr;
+    if (!f2_pair_active(a, c0)) return;
+    const int n1 = G.n1, N = G.n0 * n1, E = F2_RB * n1;
+    double2* buf = f2s;
+    const double2* tw = load_twiddles(f2s + padded(E), twg, G.p1);
+    const size_t rb = (size_t)blockIdx.x * E;
+    const bool h1 = c0 + 1 < a.n;
+    const double* x0 = a.X + (size_t)c0 * N + rb;
+    const double* x1 = a.X + (size_t)(c0 + 1) * N + rb;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) buf[P(e)] = make_double2(x0[e], h1 ? x1[e] : 0.0);
+    cp_async_wait_all_fe();
+    __syncthreads();
+    fft_inplace<EPT>(buf, n1, F2_RB, G.p1, tw);
+    double2* z = Z + (size_t)blockIdx.y * N + rb;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) z[e] = buf[P(e)];
+}
+
+template <int EPT>
+__global__ void __launch_bounds__(256, 3) k_f2_cols(FftGeom G, const double2* __restrict__ twg, FopArgs a,
+                                                 double2* __restrict__ Z, int pair0) {
+    extern __shared__ __align__(16) double2 f2s[];
+    const int pr = pair0 + blockIdx.y, c0 = 2 * pr;
+    if (!f2_pair_active(a, c0)) return;
+    const int n0 = G.n0, n1 = G.n1, ld = G.ldc, E = F2_CB * n0;
+    double2* buf = f2s;
+    const double2* tw = load_twiddles(f2s + padded(F2_CB * ld), twg, G.p0);
+    const int k1b = blockIdx.x * F2_CB;
+    double2* z = Z + (size_t)blockIdx.y * n0 * n1 + k1b;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const int i0 = e / F2_CB, c = e - i0 * F2_CB;
+        buf[P(c * ld + i0)] = z[(size_t)i0 * n1 + c];
+    }
+    cp_async_wait_all_fe();
+    __syncthreads();
+    fft_inplace<EPT>(buf, ld, F2_CB, G.p0, tw);
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const int c = e / n0, k0 = e - c * n0;
+        const int k1 = k1b + c;
+        const double m = a.sym >= 0 ? sym_value(G, a.sym, a.tau, k0, k1) : __ldg(&a.mult[(size_t)k0 * n1 + k1]);
+        const int o = P(c * ld + k0);
+        const double2 v = buf[o];
+        buf[o] = make_double2(m * v.x, -m * v.y);
+    }
+    __syncthreads();
+    fft_inplace<EPT>(buf, ld, F2_CB, G.p0, tw);
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const int i0 = e / F2_CB, c = e - i0 * F2_CB;
+        z[(size_t)i0 * n1 + c] = buf[P(c * ld + i0)];
+    }
+}
+
+template <int EPT>
+__global__ void __launch_bounds__(256, 3) k_f2_rows_inv(FftGeom G, const double2* __restrict__ twg, FopArgs a,
+                                                     const double2* __restrict__ Z, int pair0,
+                                                     double* __restrict__ part) {
+    extern __shared__ __align__(16) double2 f2s[];
+    __shared__ double red[132];
+    const int pr = pair0 + blockIdx.y, c0 = 2 * pr, c1 = c0 + 1;
+    if (!f2_pair_active(a, c0)) return;
+    const int n1 = G.n1, N = G.n0 * n1, E = F2_RB * n1;
+    double2* buf = f2s;
+    const double2* tw = load_twiddles(f2s + padded(E), twg, G.p1);
+    const size_t rb = (size_t)blockIdx.x * E;
+    const double2* z = Z + (size_t)blockIdx.y * N + rb;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) buf[P(e)] = z[e];
+    cp_async_wait_all_fe();
+    __syncthreads();
+    fft_inplace<EPT>(buf, n1, F2_RB, G.p1, tw);
+    const bool h1 = c1 < a.n;
+    const bool act0 = !a.active || a.active[c0];
+    const bool act1 = h1 && (!a.active || a.active[c1]);
+    const double s0 = a.shift ? a.shift[c0] : 0.0;
+    const double s1 = (a.shift && h1) ? a.shift[c1] : 0.0;
+    const double* x0 = a.X + (size_t)c0 * N + rb;
+    const double* x1 = a.X + (size_t)c1 * N + rb;
+    double* y0 = a.Y + (size_t)c0 * N + rb;
+    double* y1 = a.Y + (size_t)c1 * N + rb;
+    const double* dg = a.diag ? a.diag + rb : nullptr;
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const double u0 = x0[e];
+        const double u1 = h1 ? x1[e] : 0.0;
+        const double2 v = buf[P(e)];
+        double v0 = v.x, v1 = -v.y;
+        if (dg) {
+            const double w = dg[e];
+            v0 += (w - s0) * u0;
+            v1 += (w - s1) * u1;
+        } else if (a.shift) {
+            v0 -= s0 * u0;
+            v1 -= s1 * u1;
+        }
+        if (act0) y0[e] = v0;
+        if (act1) y1[e] = v1;
+        d[0] += u0 * v0;
+        d[1] += u0 * u0;
+        d[2] += u1 * v1;
+        d[3] += u1 * u1;
+    }
+    if (a.dots) {
+        block_sum4(d, red);
+        if (threadIdx.x < 4) part[((size_t)pr * gridDim.x + blockIdx.x) * 4 + threadIdx.x] = d[threadIdx.x];
+    }
+}
+
+// dots[2c + q] = sum over row blocks (in order) of the pair's partials, active columns only.
+__global__ void k_f2_dots(int n, int nrb, const double* __restrict__ part, const int* __restrict__ active,
+                          double* __restrict__ dots) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (column, q)
+    if (i >= 2 * n) return;
+    const int col = i >> 1, q = i & 1;
+    if (active && !active[col]) return;
+    const int pr = col >> 1, w = 2 * (col & 1) + q;
+    double s = 0.0;
+    for (int b = 0; b < nrb; ++b) s += part[((size_t)pr * nrb + b) * 4 + w];
+    dots[i] = s;
+}
+
+// Workspace of the three-pass 2D operator for n columns, allocated ahead of a stream capture
+// (allocation is not permitted while capturing).
+void fourier_reserve(acp_context* ctx, int n) {
+    if (ctx->dim != 2 || n <= 0) return;
+    const int npair = (n + 1) / 2;
+    ctx->ws("f2_Z", (size_t)npair * ctx->n[0] * ctx->n[1] * sizeof(double2));
+    ctx->wsd("f2_part", (size_t)npair * (ctx->n[0] / F2_RB) * 4);
+}
+
+static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
+    const FftGeom G = geom(ctx);
+    const int n0 = G.n0, n1 = G.n1;
+    if (getenv("ACP_FFT2D_CLUSTER") || n0 % F2_CB || n1 % F2_RB) return false;
+    if (a.mult == nullptr && a.sym < 0) return false;  // no transform: the cluster kernel's epilogue only
+    const int npair = (a.n + 1) / 2;
+    const int Tr = std::min(256, std::max(64, (F2_RB * n1 / 8 + 31) / 32 * 32));
+    const int Tc = std::min(256, std::max(64, (F2_CB * n0 / 8 + 31) / 32 * 32));
+    const int er = (F2_RB * n1 + Tr - 1) / Tr, ec = (F2_CB * n0 + Tc - 1) / Tc;
+    if (er > 16 || ec > 16) return false;
+    const size_t sr = (size_t)(padded(F2_RB * n1) + G.tw1n) * sizeof(double2);
+    const size_t sc = (size_t)(padded(F2_CB * G.ldc) + G.tw0n) * sizeof(double2);
+    if (sr > 200 * 1024 || sc > 200 * 1024) return false;
+    const int nrb = n0 / F2_RB, ncb = n1 / F2_CB;
+    double2* Z = static_cast<double2*>(ctx->ws("f2_Z", (size_t)npair * n0 * n1 * sizeof(double2)));
+    double* part = a.dots ? ctx->wsd("f2_part", (size_t)npair * nrb * 4) : nullptr;
+    auto ra = er <= 8 ? k_f2_rows_fwd<8> : k_f2_rows_fwd<16>;
+    auto cb = ec <= 8 ? k_f2_cols<8> : k_f2_cols<16>;
+    auto rc = er <= 8 ? k_f2_rows_inv<8> : k_f2_rows_inv<16>;
+    set_smem_attr((const void*)ra, sr, false);
+    set_smem_attr((const void*)cb, sc, false);
+    set_smem_attr((const void*)rc, sr, false);
+    const double2* tw0 = (const double2*)ctx->d_tw;
+    const double2* tw1 = (const double2*)ctx->d_tw1;
+    for (int p0 = 0; p0 < npair; p0 += 65535) {
+        const int np = std::min(65535, npair - p0);
+        ra<<<dim3(nrb, np), Tr, sr, ctx->stream>>>(G, tw1, a, Z + (size_t)p0 * n0 * n1, p0);
+        launched(ctx);
+        cb<<<dim3(ncb, np), Tc, sc, ctx->stream>>>(G, tw0, a, Z + (size_t)p0 * n0 * n1, p0);
+        launched(ctx);
+        rc<<<dim3(nrb, np), Tr, sr, ctx->stream>>>(G, tw1, a, Z + (size_t)p0 * n0 * n1, p0, part);
+        launched(ctx);
+    }
+    if (a.dots) {
+        k_f2_dots<<<cdiv(2 * a.n, 256), 256, 0, ctx->stream>>>(a.n, nrb, part, a.active, a.dots);
+        launched(ctx);
+    }
+    return true;
+}
+
 void fourier_op(acp_context* ctx, const FopArgs& a) {
+    if (a.n <= 0) return;
+    if (ctx->dim == 2 && launch_fft2d_passes(ctx, a)) return;
     IoArgs io;
     io.f = a;
     io.n = a.n;

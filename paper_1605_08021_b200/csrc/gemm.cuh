@@ -320,9 +320,24 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     const int n0 = blockIdx.y * TC_BN, m0 = blockIdx.z * BM;
     pdl_wait();
     pdl_trigger();
-    // column tiles whose columns have all converged are skipped (uniform over the cluster: its
-    // CTAs share blockIdx.y, and nothing has synchronised yet)
-    if (!hook.tile_active(n0, n)) return;
+    // Column tiles whose columns have all converged are skipped.  The decision must be uniform
+    // over the cluster (a CTA that leaves early would strand its peers at the cluster barrier and
+    // DSMEM reads).  With one m-tile (gridDim.z == 1) the only writer of the flags is this
+    // cluster's own hook, which runs after the barrier below, so every rank reads the same
+    // values.  With several m-tiles the hook of the z = 0 cluster may flip the flags while the
+    // z > 0 clusters of the same column tile read them: there rank 0 decides and pushes its
+    // decision to every peer before a cluster barrier.
+    if (gridDim.z == 1) {
+        if (!hook.tile_active(n0, n)) return;
+    } else {
+        __shared__ int s_act;
+        if (rank == 0 && tid < CS) {
+            const int act = hook.tile_active(n0, n) ? 1 : 0;
+            *cluster.map_shared_rank(&s_act, tid) = act;
+        }
+        cluster.sync();
+        if (!s_act) return;
+    }
     const int kb = rank * kchunk;
     const int ke = min(K, kb + kchunk);
     const int nk = ke > kb ? (ke - kb + TC_BK - 1) / TC_BK : 0;

@@ -600,6 +600,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
     };
 
+    fourier_reserve(ctx, n);  // before any capture below
     // r0 = b, z0 = Q M r0, p0 = z0
     precond_half(SC_INIT);
 
@@ -620,7 +621,27 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     cudaGraphExec_t exec = nullptr;
     auto it_g = ctx->graphs.find(key);
     bool hostloop = key[0] == 'H';
-    if (hostloop) {
+    if (getenv("ACP_PCG_NOGRAPH")) {  // debug: the same body launched eagerly from the host
+        hostloop = true;
+        ACP_CUDA(cudaMemsetAsync(d_chunks, 0, sizeof(int), ctx->stream));
+        bool conv = false;
+        for (int c = 0; c < max_chunks; ++c) {
+            for (int it = 0; it < chunk; ++it) {
+                hamiltonian_half();
+                precond_half(SC_BETA);
+            }
+            k_count_active<<<1, 256, 0, ctx->stream>>>(s.active, n, d_nact, (cudaGraphConditionalHandle)0, d_chunks,
+                                                       -1);
+            launched(ctx);
+            ACP_CUDA(cudaMemcpyAsync(h_nact, d_nact, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (h_nact[0] == 0) {
+                conv = true;
+                break;
+            }
+        }
+        h_nact[0] = conv ? 0 : 1;
+    } else if (hostloop) {
         ACP_CUDA(cudaMemsetAsync(d_chunks, 0, sizeof(int), ctx->stream));
         exec = graph_cached(ctx, key, [&]() {
             for (int it = 0; it < chunk; ++it) {
@@ -784,6 +805,7 @@ void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* 
         ACP_CUDA(cudaStreamSynchronize(ctx->stream));
         ctx->graphs[skey] = acp_context::GraphEntry{};
     }
+    fourier_reserve(ctx, n);
     // The reps launches are captured into a CUDA graph (cached per shape) and replayed, so the
     // caller's events time device execution back to back, not host launch overhead.
     auto body = [&]() {

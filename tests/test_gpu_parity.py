@@ -91,6 +91,7 @@ def test_fourier_operator_2d_cluster_sizes(cs, np_pairs, monkeypatch):
     pairs per cluster (ACP_FFT2D_NP) vs the oracle; odd column counts leave partial groups."""
     from paper_1605_08021_b200 import Context
     s = system("tiny2d")
+    monkeypatch.setenv("ACP_FFT2D_CLUSTER", "1")
     monkeypatch.setenv("ACP_FFT2D_CS", str(cs))
     monkeypatch.setenv("ACP_FFT2D_NP", str(np_pairs))
     ctx = Context.from_config(s.cfg)
@@ -107,11 +108,29 @@ def test_fourier_operator_2d_cluster_sizes(cs, np_pairs, monkeypatch):
     ctx.close()
 
 
-@pytest.mark.parametrize("cs", [1, 8])
+def test_fourier_operator_2d_three_pass():
+    """Default 2D K1: row pass, column pass (symbol), row pass + epilogue through the HBM
+    intermediate, vs the oracle's operators; odd column counts leave a half-empty last pair."""
+    s = system("tiny2d")
+    rng = np.random.default_rng(31)
+    for ncol in (1, 4, 7, 13):
+        X = rng.standard_normal((s.m.Ng, ncol))
+        Xt = T(X.T)
+        assert rel(s.ctx.fourier_apply(Xt, 0).cpu().numpy().T, s.m.kinetic(X)) < 1e-12
+        assert rel(s.ctx.fourier_apply(Xt, 1).cpu().numpy().T, s.m.yukawa(X)) < 1e-12
+        shifts = rng.uniform(-0.1, 0.1, ncol)
+        Y = s.ctx.fourier_apply(Xt, 0, diag=s.V_t, shift=T(shifts)).cpu().numpy().T
+        assert rel(Y, (s.H @ X) - shifts[None, :] * X) < 1e-11
+
+
+@pytest.mark.parametrize("cs", [0, 1, 8])
 def test_fourier_operator_rectangular_grid(cs, monkeypatch):
-    """Non-square 2D grid and cell (axis bookkeeping): kinetic symbol vs numpy's FFT."""
+    """Non-square 2D grid and cell (axis bookkeeping): kinetic symbol vs numpy's FFT; cs = 0 is
+    the default three-pass path, cs > 0 the cluster kernel with that cluster size."""
     from paper_1605_08021_b200 import Context
-    monkeypatch.setenv("ACP_FFT2D_CS", str(cs))
+    if cs:
+        monkeypatch.setenv("ACP_FFT2D_CLUSTER", "1")
+        monkeypatch.setenv("ACP_FFT2D_CS", str(cs))
     n0, n1, L0, L1 = 24, 40, 10.0, 16.0
     ctx = Context(2, (n0, n1), (L0, L1), 2, 2, 2.0, 2.0, 1.0, 0.01, 1.0)
     rng = np.random.default_rng(5)
