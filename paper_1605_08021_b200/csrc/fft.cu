@@ -737,8 +737,11 @@ static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
     set_smem_attr((const void*)rc, sr, false);
     const double2* tw0 = (const double2*)ctx->d_tw;
     const double2* tw1 = (const double2*)ctx->d_tw1;
-    for (int p0 = 0; p0 < npair; p0 += 65535) {
-        const int np = std::min(65535, npair - p0);
+    // pairs per chunk: ACP_F2_CHUNK keeps a chunk's intermediate L2-resident between the passes
+    static const int chunk_env = getenv("ACP_F2_CHUNK") ? atoi(getenv("ACP_F2_CHUNK")) : 0;
+    const int chunk = chunk_env > 0 ? std::min(chunk_env, 65535) : 65535;
+    for (int p0 = 0; p0 < npair; p0 += chunk) {
+        const int np = std::min(chunk, npair - p0);
         ra<<<dim3(nrb, np), Tr, sr, ctx->stream>>>(G, tw1, a, Z + (size_t)p0 * n0 * n1, p0);
         launched(ctx);
         cb<<<dim3(ncb, np), Tc, sc, ctx->stream>>>(G, tw0, a, Z + (size_t)p0 * n0 * n1, p0);

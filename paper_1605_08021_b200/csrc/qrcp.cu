@@ -593,6 +593,8 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
     __shared__ double allx0[2][16];   // row j of each peer's candidate (pushed with the slot)
     __shared__ double s_wn2, s_x0;
     __shared__ int s_pos, s_rank, s_col, s_lc;
+    __shared__ double wb_n2[16];      // per-warp best remaining column after each update
+    __shared__ int wb_pos[16], wb_lc[16];
     const int CS = (int)cl.num_blocks(), b = (int)cl.block_rank(), tid = threadIdx.x;
     const int lane = tid & 31, warp = uniform_warp();
     constexpr int NW = 16;
@@ -634,14 +636,19 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
         if (warp == 0) {
             double bn = -1.0;
             int bp = 1 << 30, bl = -1;
-            for (int lc = lane; lc < nc; lc += 32) {
-                if (dn[lc]) continue;
-                const double xx = n2[lc];
-                if (xx > bn || (xx == bn && pos[lc] < bp)) {
-                    bn = xx;
-                    bp = pos[lc];
-                    bl = lc;
+            if (j == 0) {  // initial norms: scan the CTA's columns
+                for (int lc = lane; lc < nc; lc += 32) {
+                    const double xx = n2[lc];
+                    if (xx > bn || (xx == bn && pos[lc] < bp)) {
+                        bn = xx;
+                        bp = pos[lc];
+                        bl = lc;
+                    }
                 }
+            } else if (lane < NW) {  // later steps: the warps' bests from the previous update
+                bn = wb_n2[lane];
+                bp = wb_pos[lane];
+                bl = wb_lc[lane];
             }
             for (int o = 16; o > 0; o >>= 1) {
                 const double on = __shfl_xor_sync(0xffffffffu, bn, o);
@@ -791,16 +798,43 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
         }
         const double nt = warp_rs8(nn, lane);
         {
+            // lane l < 8 holds column q = rs8_index(l): store its norm and position (swap
+            // semantics) and reduce the warp's best remaining column over lanes 0..7
             const int q = rs8_index(lane);
+            bool lv = false;
 #pragma unroll
             for (int qq = 0; qq < CPW; ++qq)
-                if (lane < 8 && qq == q && live[qq]) n2[warp + NW * qq] = nt;
-        }
-        if (lane == 0) {
+                if (qq == q) lv = live[qq];
+            lv = lv && lane < 8;
+            const int lc = warp + NW * q;
+            double bn = -1.0;
+            int bp = 1 << 30, bl = -1;
+            if (lv) {
+                int p = pos[lc];
+                if (p == j) {
+                    p = pw;
+                    pos[lc] = pw;
+                }
+                n2[lc] = nt;
+                bn = nt;
+                bp = p;
+                bl = lc;
+            }
 #pragma unroll
-            for (int q = 0; q < CPW; ++q) {
-                const int lc = warp + NW * q;
-                if (live[q] && pos[lc] == j) pos[lc] = pw;
+            for (int o = 4; o > 0; o >>= 1) {
+                const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                if (on > bn || (on == bn && op < bp)) {
+                    bn = on;
+                    bp = op;
+                    bl = ol;
+                }
+            }
+            if (lane == 0) {
+                wb_n2[warp] = bn;
+                wb_pos[warp] = bp;
+                wb_lc[warp] = bl;
             }
         }
         __syncthreads();
