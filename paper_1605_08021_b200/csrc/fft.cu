@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
     const int N = G.n0;
     const int T = blockDim.x, tid = threadIdx.x;
     double2* buf = sm1;
-    double* smult = reinterpret_cast<double*>(sm1 + padded(N) + G.tw0n);
+    double* smult = reinterpret_cast<double*>(sm1 + padded(N));
     const int c0 = 2 * blockIdx.x, c1 = c0 + 1;
     const int ncol = IO == IO_OP ? io.f.n : io.n;
     const bool has1 = c1 < ncol;
@@ -159,7 +159,9 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
             for (int i = tid; i < N; i += T) smult[i] = io.f.mult[i];
         }
     }
-    const double2* tw = load_twiddles(sm1 + padded(N), twg, G.p0);
+    // twiddles are read through L1 (read-only path): staging the 20 KB table in shared memory
+    // cost a CTA per SM (measured 10 % slower on configs[1] / [2], profiles/r2i)
+    const double2* tw = twg;
     constexpr int NK = KEEP ? EPT : 1;  // register-resident inputs (KEEP) or re-read in the epilogue
     double u0[NK], u1[NK];
     const double* x0 = io.f.X + (size_t)c0 * N;
@@ -957,7 +959,7 @@ void fft_init(acp_context* ctx) {
         ctx->fthreads = T;
         ctx->fept = ept_for(N, T);
         ACP_REQUIRE(ctx->fept > 0, "1D grid too large for the shared-memory FFT");
-        ctx->fsmem = (size_t)(padded(N) + ctx->plan.twoff[ctx->plan.npass]) * sizeof(double2) + (size_t)N * sizeof(double);
+        ctx->fsmem = (size_t)padded(N) * sizeof(double2) + (size_t)N * sizeof(double);  // twiddles via L1
         ACP_REQUIRE(ctx->fsmem <= 220 * 1024, "1D grid too large for the shared-memory FFT");
     } else {
         // smallest cluster (cs | n0, cs | n1, cs <= 16) whose per-CTA slice has <= 4096 points

@@ -735,6 +735,7 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
             N = j;
             break;
         }
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 5] = clock64();
         // winner's rows j..m-1 from its owner CTA (one DSMEM read per row, by one thread each)
         const double* x = cl.map_shared_rank(pub, ws) + (size_t)buf * m;
         const double x0 = s_x0;
@@ -745,7 +746,7 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
         if (j > 0 && tid == 0) v[j - 1] = 0.0;  // rows < j stay zero (cleared as j advances)
         if (b == 0 && tid == 0) rdiag[j] = rjj;
         __syncthreads();
-        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 5] = clock64();
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 6] = clock64();
         double vr[KR];
 #pragma unroll
         for (int k = 0; k < KR; ++k) {
@@ -838,7 +839,7 @@ __global__ void __launch_bounds__(512, 1) k_qrcp_reg(int m, int Ng, double* __re
             }
         }
         __syncthreads();
-        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 6] = clock64();
+        if (tprof && b == 0 && tid == 0 && j < 512) tprof[8 * j + 7] = clock64();
     }
 #pragma unroll
     for (int q = 0; q < CPW; ++q) {
@@ -1051,7 +1052,7 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
             ACP_CUDA(cudaStreamSynchronize(ctx->stream));
             if (FILE* f = fopen(tpath, "a")) {
                 for (int j = 0; j < 512 && h[8 * j]; ++j) {
-                    for (int k = 0; k < 7; ++k) fprintf(f, "%lld ", h[8 * j + k]);
+                    for (int k = 0; k < 8; ++k) fprintf(f, "%lld ", h[8 * j + k]);
                     fprintf(f, "\n");
                 }
                 fclose(f);
@@ -1091,7 +1092,7 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
             ACP_CUDA(cudaStreamSynchronize(ctx->stream));
             if (FILE* f = fopen(tpath, "a")) {
                 for (int j = 0; j < 512 && h[8 * j]; ++j) {
-                    for (int k = 0; k < 7; ++k) fprintf(f, "%lld ", h[8 * j + k]);
+                    for (int k = 0; k < 8; ++k) fprintf(f, "%lld ", h[8 * j + k]);
                     fprintf(f, "\n");
                 }
                 fclose(f);

@@ -22,8 +22,9 @@ os.environ["ACP_QR_PROFILE"] = out
 torch.cuda.synchronize()
 S, Xi, n = ctx.compress(gs["Psi"], gs["G"], th, nu, id_eps=cfg.id_eps)
 t = np.loadtxt(out)
+t = t[(t > 0).all(axis=1)]  # drop the exit step (unfinished phases)
 d = np.diff(t, axis=1)
 step = np.diff(t[:, 0])
 print("N_mu", n, "steps", len(t))
-print("mean cycles per phase [local argmax+push | syncthreads | publish | cl.sync | winner+v | update]:", d.mean(0).round(0))
+print("mean cycles per phase [local argmax+push | syncthreads | publish | cl.sync | winner+exit test | v from DSMEM | update]:", d.mean(0).round(0))
 print("mean cycles per step:", step.mean().round(0), " -> us per step at 1.9 GHz:", (step.mean() / 1.9e3).round(2))
