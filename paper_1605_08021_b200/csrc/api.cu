@@ -54,6 +54,9 @@ int acp_create(const acp_system* sys, int device, acp_context** out) {
         ACP_CUDA(cudaSetDevice(device));
         ACP_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
         ctx->stream = ctx->own_stream;
+        ACP_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+        ACP_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        ACP_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
         ACP_CUDA(cudaMallocHost(&ctx->pinned, 4096));
         acp::fft_init(ctx);
     } catch (const Error& e) {
@@ -78,6 +81,12 @@ int acp_destroy(acp_context* ctx) {
         if (kv.second.ptr) cudaFree(kv.second.ptr);
     acp::fft_free(ctx);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->stream2) {
+        cudaStreamSynchronize(ctx->stream2);
+        cudaStreamDestroy(ctx->stream2);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return ACP_OK;

@@ -59,6 +59,9 @@ struct acp_context {
     double dV = 0.0, Omega = 0.0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
+    cudaStream_t stream2 = nullptr;       // second PCG group (forked from / joined to `stream`)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int f2_alt = 0;                       // 2D K1 workspace selector while enqueuing on stream2
     std::string err;
     long long launches = 0;
 
@@ -102,7 +105,7 @@ struct acp_context {
             // a cached graph may hold this buffer's old address (and a later allocation may reuse
             // it, so pointer-keyed lookups cannot tell): drop every cached graph on reallocation
             if (b.ptr) {
-                cudaStreamSynchronize(stream);
+                cudaDeviceSynchronize();  // both PCG streams
                 for (auto& kv : graphs)
                     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
                 graphs.clear();
@@ -216,8 +219,9 @@ struct FopArgs {
 };
 // Y = IFFT(mult * FFT(X)) + (diag - shift_j) (.) X, two real columns per complex FFT.
 void fourier_op(acp_context* ctx, const FopArgs& a);
-// Pre-allocate fourier_op's workspace for n columns (call before capturing it into a graph).
-void fourier_reserve(acp_context* ctx, int n);
+// Pre-allocate fourier_op's workspace for n columns (call before capturing it into a graph);
+// alt = 1: the workspace used while ctx->f2_alt is set (the second concurrent PCG group).
+void fourier_reserve(acp_context* ctx, int n, int alt);
 // Fill ctx->d_mult with a multiplier of the given kind (scaled by 1/N); returns it.
 const double* multiplier(acp_context* ctx, MultKind kind, double tau);
 // Real grid functions from Hermitian spectra given as complex coefficients per bin:

@@ -529,40 +529,30 @@ static void launch_nn_ep(acp_context* ctx, int M, int K, int n, const double* A,
     launched(ctx);
 }
 
-void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const double* V, const double* d_shift_c,
-                       int n_c, const double* rhs, int nmu_p, double tol, int max_iter, double tau, double* X,
-                       PcgStats* st) {
-    const int Ng = ctx->Ng;
-    const int n = n_c * nmu_p;
-    if (n == 0) return;
-    double* R = ctx->wsd("pcg_R", (size_t)Ng * n);
-    double* P = ctx->wsd("pcg_P", (size_t)Ng * n);
-    double* Y = ctx->wsd("pcg_Y", (size_t)Ng * n);
-    double* shift = ctx->wsd("pcg_shift", n);
-    double* dots = ctx->wsd("pcg_dots", 2 * (size_t)n);
-    double* C = ctx->wsd("pcg_C", (size_t)n_occ * n);
+// One independent group of columns (a contiguous range of Chebyshev nodes) of the batch: its
+// buffers are column slices of the batch's, so groups never touch each other's data.
+struct PcgGroup {
+    double *R, *P, *Y, *X, *C, *shift, *dots;
     PcgScal s;
-    s.rz = ctx->wsd("pcg_rz", n);
-    s.bb = ctx->wsd("pcg_bb", n);
-    s.alpha = ctx->wsd("pcg_alpha", n);
-    s.beta = ctx->wsd("pcg_beta", n);
-    s.res = ctx->wsd("pcg_res", n);
-    s.active = ctx->wsi("pcg_active", n);
-    s.iters = ctx->wsi("pcg_iters", n);
-    s.dots = dots;
-    int* d_nact = ctx->wsi("pcg_nact", 2);  // [0] active columns, [1] while-loop trips
-    int* h_nact = static_cast<int*>(ctx->pinned);
+    int n;          // columns
+    int* d_nact;    // [0] active columns, [1] while-loop trips
+    int* h_nact;    // pinned host copy
+    bool synced;    // the host already waited for this group (host-driven loop)
+    long long launches_per_trip;
+};
 
-
+// Enqueue the PCG of one group on ctx->stream: r0 = b, z0 = Q M r0, p0 = z0, then the iteration
+// loop (while-node graph).  Returns without waiting unless the host-driven loop is selected.
+static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, const double* V, PcgGroup& G,
+                              int nmu_p, double tol2, double tau, int max_iter) {
+    const int Ng = ctx->Ng;
+    double *R = G.R, *P = G.P, *Y = G.Y, *X = G.X, *C = G.C, *shift = G.shift, *dots = G.dots;
+    PcgScal& s = G.s;
+    const int n = G.n;
+    int* d_nact = G.d_nact;
+    int* h_nact = G.h_nact;
     const int nvalid = nmu_p;  // columns beyond the caller's count are zero RHS -> inactive by bb = 0
-    k_batch_shift<<<cdiv(n, 256), 256, 0, ctx->stream>>>(d_shift_c, n_c, nmu_p, shift);
-    launched(ctx);
-    {
-        size_t tot = (size_t)Ng * n;
-        k_pcg_init<<<cdiv(tot, 256), 256, 0, ctx->stream>>>(Ng, n_c, nmu_p, rhs, R, X);
-        launched(ctx);
-    }
-    const double tol2 = tol * tol;
+    G.synced = false;
 
     auto precond_half = [&](int mode) {
         FopArgs f;
@@ -600,7 +590,6 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
     };
 
-    fourier_reserve(ctx, n);  // before any capture below
     // r0 = b, z0 = Q M r0, p0 = z0
     precond_half(SC_INIT);
 
@@ -712,11 +701,105 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         ACP_CUDA(cudaMemsetAsync(d_chunks, 0, sizeof(int), ctx->stream));
         ACP_CUDA(cudaGraphLaunch(exec, ctx->stream));
         ACP_CUDA(cudaMemcpyAsync(h_nact, d_nact, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        ACP_CUDA(cudaStreamSynchronize(ctx->stream));
-        const int trips = h_nact[1];
-        ctx->launches += ctx->graphs[key].launches * trips;
+        G.launches_per_trip = ctx->graphs[key].launches;
+    } else {
+        G.synced = true;
     }
-    const bool converged = h_nact[0] == 0;
+}
+
+void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const double* V, const double* d_shift_c,
+                       int n_c, const double* rhs, int nmu_p, double tol, int max_iter, double tau, double* X,
+                       PcgStats* st) {
+    const int Ng = ctx->Ng;
+    const int n = n_c * nmu_p;
+    if (n == 0) return;
+    double* R = ctx->wsd("pcg_R", (size_t)Ng * n);
+    double* P = ctx->wsd("pcg_P", (size_t)Ng * n);
+    double* Y = ctx->wsd("pcg_Y", (size_t)Ng * n);
+    double* shift = ctx->wsd("pcg_shift", n);
+    double* dots = ctx->wsd("pcg_dots", 2 * (size_t)n);
+    double* C = ctx->wsd("pcg_C", (size_t)n_occ * n);
+    PcgScal s;
+    s.rz = ctx->wsd("pcg_rz", n);
+    s.bb = ctx->wsd("pcg_bb", n);
+    s.alpha = ctx->wsd("pcg_alpha", n);
+    s.beta = ctx->wsd("pcg_beta", n);
+    s.res = ctx->wsd("pcg_res", n);
+    s.active = ctx->wsi("pcg_active", n);
+    s.iters = ctx->wsi("pcg_iters", n);
+    s.dots = dots;
+    int* d_nact = ctx->wsi("pcg_nact", 4);  // per group: [0] active columns, [1] while-loop trips
+    int* h_nact = static_cast<int*>(ctx->pinned);
+    // Two node groups on two streams: their kernels overlap, filling the latency gaps of each
+    // other's small launches (configs[1]: one K1 launch is a single wave of 464 CTAs).
+    // ACP_PCG_GROUPS=1 runs the whole batch as one group.
+    int ngroups = (n_c >= 2 && ctx->stream2 && !getenv("ACP_PCG_HOSTLOOP")) ? 2 : 1;
+    if (const char* e = getenv("ACP_PCG_GROUPS")) ngroups = std::max(1, std::min(ngroups, atoi(e)));
+
+    k_batch_shift<<<cdiv(n, 256), 256, 0, ctx->stream>>>(d_shift_c, n_c, nmu_p, shift);
+    launched(ctx);
+    {
+        size_t tot = (size_t)Ng * n;
+        k_pcg_init<<<cdiv(tot, 256), 256, 0, ctx->stream>>>(Ng, n_c, nmu_p, rhs, R, X);
+        launched(ctx);
+    }
+    const double tol2 = tol * tol;
+    PcgGroup grp[2];
+    const int nA = ngroups == 2 ? (n_c / 2) * nmu_p : n;
+    fourier_reserve(ctx, nA, 0);  // before any capture below
+    if (ngroups == 2) fourier_reserve(ctx, n - nA, 1);
+    for (int g = 0; g < ngroups; ++g) {
+        const int c0 = g == 0 ? 0 : nA, cn = g == 0 ? nA : n - nA;
+        PcgGroup& G = grp[g];
+        G.R = R + (size_t)c0 * Ng;
+        G.P = P + (size_t)c0 * Ng;
+        G.Y = Y + (size_t)c0 * Ng;
+        G.X = X + (size_t)c0 * Ng;
+        G.C = C + (size_t)c0 * n_occ;
+        G.shift = shift + c0;
+        G.dots = dots + 2 * (size_t)c0;
+        G.s = s;
+        G.s.rz += c0;
+        G.s.bb += c0;
+        G.s.alpha += c0;
+        G.s.beta += c0;
+        G.s.res += c0;
+        G.s.active += c0;
+        G.s.iters += c0;
+        G.s.dots = G.dots;
+        G.n = cn;
+        G.d_nact = d_nact + 2 * g;
+        G.h_nact = h_nact + 2 * g;
+        G.launches_per_trip = 0;
+    }
+    if (ngroups == 1) {
+        pcg_group_enqueue(ctx, Psi, n_occ, V, grp[0], nmu_p, tol2, tau, max_iter);
+        if (!grp[0].synced) ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else {
+        cudaStream_t s0 = ctx->stream, s1 = ctx->stream2;
+        ACP_CUDA(cudaEventRecord(ctx->ev_fork, s0));
+        ACP_CUDA(cudaStreamWaitEvent(s1, ctx->ev_fork, 0));
+        pcg_group_enqueue(ctx, Psi, n_occ, V, grp[0], nmu_p, tol2, tau, max_iter);
+        ctx->stream = s1;
+        ctx->f2_alt = 1;  // the second group's 2D FFT intermediate
+        try {
+            pcg_group_enqueue(ctx, Psi, n_occ, V, grp[1], nmu_p, tol2, tau, max_iter);
+        } catch (...) {
+            ctx->stream = s0;
+            ctx->f2_alt = 0;
+            throw;
+        }
+        ctx->stream = s0;
+        ctx->f2_alt = 0;
+        ACP_CUDA(cudaEventRecord(ctx->ev_join, s1));
+        ACP_CUDA(cudaStreamWaitEvent(s0, ctx->ev_join, 0));
+        ACP_CUDA(cudaStreamSynchronize(s0));
+    }
+    bool converged = true;
+    for (int g = 0; g < ngroups; ++g) {
+        if (!grp[g].synced) ctx->launches += grp[g].launches_per_trip * grp[g].h_nact[1];
+        converged = converged && grp[g].h_nact[0] == 0;
+    }
     if (st) {
         std::vector<int> it(n);
         std::vector<double> res(n), bb(n);
@@ -805,7 +888,7 @@ void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* 
         ACP_CUDA(cudaStreamSynchronize(ctx->stream));
         ctx->graphs[skey] = acp_context::GraphEntry{};
     }
-    fourier_reserve(ctx, n);
+    fourier_reserve(ctx, n, 0);
     // The reps launches are captured into a CUDA graph (cached per shape) and replayed, so the
     // caller's events time device execution back to back, not host launch overhead.
     auto body = [&]() {

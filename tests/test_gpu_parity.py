@@ -414,6 +414,22 @@ def test_apply_chi0_fused_projection_equals_unfused(sysx, monkeypatch):
     assert torch.equal(W1, W2) and i1["total_iter"] == i2["total_iter"]
 
 
+def test_apply_chi0_two_stream_groups_equal_one(sysx, monkeypatch):
+    """The batch split into two node groups on two streams (default) and run as one group
+    (ACP_PCG_GROUPS=1) give bitwise-identical W and iteration counts (per-column arithmetic)."""
+    from paper_1605_08021_b200 import Context
+    s = sysx
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    St, Xt = T(S_o, torch.int32), T(Xi_o.T)
+    W1, i1 = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    monkeypatch.setenv("ACP_PCG_GROUPS", "1")
+    ctx = Context.from_config(s.cfg)
+    W2, i2 = ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    ctx.close()
+    assert torch.equal(W1, W2) and i1["total_iter"] == i2["total_iter"]
+
+
 def test_apply_chi0_empty_shard(sysx):
     """An empty mu-range (a rank with no columns) is a no-op that leaves W untouched."""
     s = sysx
