@@ -54,9 +54,11 @@ int acp_create(const acp_system* sys, int device, acp_context** out) {
         ACP_CUDA(cudaSetDevice(device));
         ACP_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
         ctx->stream = ctx->own_stream;
-        ACP_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
         ACP_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-        ACP_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+        for (int g = 1; g < 4; ++g) {
+            ACP_CUDA(cudaStreamCreateWithFlags(&ctx->gstream[g], cudaStreamNonBlocking));
+            ACP_CUDA(cudaEventCreateWithFlags(&ctx->ev_join[g], cudaEventDisableTiming));
+        }
         ACP_CUDA(cudaMallocHost(&ctx->pinned, 4096));
         acp::fft_init(ctx);
     } catch (const Error& e) {
@@ -81,12 +83,14 @@ int acp_destroy(acp_context* ctx) {
         if (kv.second.ptr) cudaFree(kv.second.ptr);
     acp::fft_free(ctx);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
-    if (ctx->stream2) {
-        cudaStreamSynchronize(ctx->stream2);
-        cudaStreamDestroy(ctx->stream2);
+    for (int g = 1; g < 4; ++g) {
+        if (ctx->gstream[g]) {
+            cudaStreamSynchronize(ctx->gstream[g]);
+            cudaStreamDestroy(ctx->gstream[g]);
+        }
+        if (ctx->ev_join[g]) cudaEventDestroy(ctx->ev_join[g]);
     }
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return ACP_OK;

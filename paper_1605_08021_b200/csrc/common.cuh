@@ -16,6 +16,8 @@
 
 namespace acp {
 
+constexpr int PCG_MAXG = 4;  // concurrent PCG node groups (streams)
+
 struct Error : public std::runtime_error {
     int code;
     Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
@@ -59,9 +61,11 @@ struct acp_context {
     double dV = 0.0, Omega = 0.0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
-    cudaStream_t stream2 = nullptr;       // second PCG group (forked from / joined to `stream`)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    int f2_alt = 0;                       // 2D K1 workspace selector while enqueuing on stream2
+    // PCG node groups 1.. run on gstream[g] (forked from / joined to `stream`)
+    cudaStream_t gstream[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr;
+    cudaEvent_t ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
+    int f2_alt = 0;                       // 2D K1 workspace selector: the group being enqueued
     std::string err;
     long long launches = 0;
 
@@ -220,7 +224,7 @@ struct FopArgs {
 // Y = IFFT(mult * FFT(X)) + (diag - shift_j) (.) X, two real columns per complex FFT.
 void fourier_op(acp_context* ctx, const FopArgs& a);
 // Pre-allocate fourier_op's workspace for n columns (call before capturing it into a graph);
-// alt = 1: the workspace used while ctx->f2_alt is set (the second concurrent PCG group).
+// alt = g: the workspace used while ctx->f2_alt == g (PCG node group g on its own stream).
 void fourier_reserve(acp_context* ctx, int n, int alt);
 // Fill ctx->d_mult with a multiplier of the given kind (scaled by 1/N); returns it.
 const double* multiplier(acp_context* ctx, MultKind kind, double tau);

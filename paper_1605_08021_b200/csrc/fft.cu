@@ -708,11 +708,13 @@ __global__ void k_f2_dots(int n, int nrb, const double* __restrict__ part, const
 
 // Workspace of the three-pass 2D operator for n columns, allocated ahead of a stream capture
 // (allocation is not permitted while capturing).
+static std::string f2_name(const char* base, int alt) { return alt ? base + std::to_string(alt) : std::string(base); }
+
 void fourier_reserve(acp_context* ctx, int n, int alt) {
     if (ctx->dim != 2 || n <= 0) return;
     const int npair = (n + 1) / 2;
-    ctx->ws(alt ? "f2_Z_b" : "f2_Z", (size_t)npair * ctx->n[0] * ctx->n[1] * sizeof(double2));
-    ctx->wsd(alt ? "f2_part_b" : "f2_part", (size_t)npair * (ctx->n[0] / F2_RB) * 4);
+    ctx->ws(f2_name("f2_Z", alt), (size_t)npair * ctx->n[0] * ctx->n[1] * sizeof(double2));
+    ctx->wsd(f2_name("f2_part", alt), (size_t)npair * (ctx->n[0] / F2_RB) * 4);
 }
 
 static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
@@ -729,10 +731,9 @@ static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
     const size_t sc = (size_t)(padded(F2_CB * G.ldc) + G.tw0n) * sizeof(double2);
     if (sr > 200 * 1024 || sc > 200 * 1024) return false;
     const int nrb = n0 / F2_RB, ncb = n1 / F2_CB;
-    // the second PCG group (its own stream, ctx->f2_alt) has its own intermediate
-    double2* Z = static_cast<double2*>(
-        ctx->ws(ctx->f2_alt ? "f2_Z_b" : "f2_Z", (size_t)npair * n0 * n1 * sizeof(double2)));
-    double* part = a.dots ? ctx->wsd(ctx->f2_alt ? "f2_part_b" : "f2_part", (size_t)npair * nrb * 4) : nullptr;
+    // each concurrent PCG group (its own stream, ctx->f2_alt) has its own intermediate
+    double2* Z = static_cast<double2*>(ctx->ws(f2_name("f2_Z", ctx->f2_alt), (size_t)npair * n0 * n1 * sizeof(double2)));
+    double* part = a.dots ? ctx->wsd(f2_name("f2_part", ctx->f2_alt), (size_t)npair * nrb * 4) : nullptr;
     auto ra = er <= 8 ? k_f2_rows_fwd<8> : k_f2_rows_fwd<16>;
     auto cb = ec <= 8 ? k_f2_cols<8> : k_f2_cols<16>;
     auto rc = er <= 8 ? k_f2_rows_inv<8> : k_f2_rows_inv<16>;

@@ -728,13 +728,20 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     s.active = ctx->wsi("pcg_active", n);
     s.iters = ctx->wsi("pcg_iters", n);
     s.dots = dots;
-    int* d_nact = ctx->wsi("pcg_nact", 4);  // per group: [0] active columns, [1] while-loop trips
+    int* d_nact = ctx->wsi("pcg_nact", 2 * PCG_MAXG);  // per group: [0] active columns, [1] trips
     int* h_nact = static_cast<int*>(ctx->pinned);
     // Two node groups on two streams: their kernels overlap, filling the latency gaps of each
     // other's small launches (configs[1]: one K1 launch is a single wave of 464 CTAs).
     // ACP_PCG_GROUPS=1 runs the whole batch as one group.
-    int ngroups = (n_c >= 2 && ctx->stream2 && !getenv("ACP_PCG_HOSTLOOP")) ? 2 : 1;
-    if (const char* e = getenv("ACP_PCG_GROUPS")) ngroups = std::max(1, std::min(ngroups, atoi(e)));
+    // Node groups on separate streams: their kernels overlap, filling the latency gaps of each
+    // other's small launches (configs[1]: one K1 launch is a single wave of 464 CTAs).  Small
+    // batches only (n N_g <= 16M points): configs[1] 12.38 (4 groups) / 12.64 (2) / 13.01 (1)
+    // ms/step; configs[2] gains nothing (270.5 / 271.3 / 272.8).  ACP_PCG_GROUPS overrides (each
+    // 2D group needs its own FFT intermediate).
+    int ngroups = (size_t)n * Ng <= ((size_t)16 << 20) ? std::min(n_c, PCG_MAXG) : 1;
+    if (const char* e = getenv("ACP_PCG_GROUPS")) ngroups = std::max(1, std::min(std::min(n_c, PCG_MAXG), atoi(e)));
+    if (getenv("ACP_PCG_HOSTLOOP")) ngroups = 1;
+    if (ngroups < 1) ngroups = 1;
 
     k_batch_shift<<<cdiv(n, 256), 256, 0, ctx->stream>>>(d_shift_c, n_c, nmu_p, shift);
     launched(ctx);
@@ -744,12 +751,12 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         launched(ctx);
     }
     const double tol2 = tol * tol;
-    PcgGroup grp[2];
-    const int nA = ngroups == 2 ? (n_c / 2) * nmu_p : n;
-    fourier_reserve(ctx, nA, 0);  // before any capture below
-    if (ngroups == 2) fourier_reserve(ctx, n - nA, 1);
+    PcgGroup grp[PCG_MAXG];
+    int gc0[PCG_MAXG + 1];  // group g: nodes [g n_c / G, (g+1) n_c / G)
+    for (int g = 0; g <= ngroups; ++g) gc0[g] = (g * n_c / ngroups) * nmu_p;
+    for (int g = 0; g < ngroups; ++g) fourier_reserve(ctx, gc0[g + 1] - gc0[g], g);  // before any capture
     for (int g = 0; g < ngroups; ++g) {
-        const int c0 = g == 0 ? 0 : nA, cn = g == 0 ? nA : n - nA;
+        const int c0 = gc0[g], cn = gc0[g + 1] - gc0[g];
         PcgGroup& G = grp[g];
         G.R = R + (size_t)c0 * Ng;
         G.P = P + (size_t)c0 * Ng;
@@ -776,14 +783,15 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         pcg_group_enqueue(ctx, Psi, n_occ, V, grp[0], nmu_p, tol2, tau, max_iter);
         if (!grp[0].synced) ACP_CUDA(cudaStreamSynchronize(ctx->stream));
     } else {
-        cudaStream_t s0 = ctx->stream, s1 = ctx->stream2;
+        cudaStream_t s0 = ctx->stream;
         ACP_CUDA(cudaEventRecord(ctx->ev_fork, s0));
-        ACP_CUDA(cudaStreamWaitEvent(s1, ctx->ev_fork, 0));
-        pcg_group_enqueue(ctx, Psi, n_occ, V, grp[0], nmu_p, tol2, tau, max_iter);
-        ctx->stream = s1;
-        ctx->f2_alt = 1;  // the second group's 2D FFT intermediate
+        for (int g = 1; g < ngroups; ++g) ACP_CUDA(cudaStreamWaitEvent(ctx->gstream[g], ctx->ev_fork, 0));
         try {
-            pcg_group_enqueue(ctx, Psi, n_occ, V, grp[1], nmu_p, tol2, tau, max_iter);
+            for (int g = 0; g < ngroups; ++g) {
+                ctx->stream = g == 0 ? s0 : ctx->gstream[g];
+                ctx->f2_alt = g;  // group g's 2D FFT intermediate
+                pcg_group_enqueue(ctx, Psi, n_occ, V, grp[g], nmu_p, tol2, tau, max_iter);
+            }
         } catch (...) {
             ctx->stream = s0;
             ctx->f2_alt = 0;
@@ -791,8 +799,10 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         }
         ctx->stream = s0;
         ctx->f2_alt = 0;
-        ACP_CUDA(cudaEventRecord(ctx->ev_join, s1));
-        ACP_CUDA(cudaStreamWaitEvent(s0, ctx->ev_join, 0));
+        for (int g = 1; g < ngroups; ++g) {
+            ACP_CUDA(cudaEventRecord(ctx->ev_join[g], ctx->gstream[g]));
+            ACP_CUDA(cudaStreamWaitEvent(s0, ctx->ev_join[g], 0));
+        }
         ACP_CUDA(cudaStreamSynchronize(s0));
     }
     bool converged = true;

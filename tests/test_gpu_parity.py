@@ -415,8 +415,8 @@ def test_apply_chi0_fused_projection_equals_unfused(sysx, monkeypatch):
 
 
 def test_apply_chi0_two_stream_groups_equal_one(sysx, monkeypatch):
-    """The batch split into two node groups on two streams (default) and run as one group
-    (ACP_PCG_GROUPS=1) give bitwise-identical W and iteration counts (per-column arithmetic)."""
+    """The batch split into node groups on separate streams (default for small batches) and run
+    as one group (ACP_PCG_GROUPS=1) give bitwise-identical W and iteration counts."""
     from paper_1605_08021_b200 import Context
     s = sysx
     th, nu = s.draws(0, s.G.shape[1])
