@@ -517,13 +517,17 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
     const FftGeom G = geom(ctx);
     const int npair = (ncols + 1) / 2;
     const int T = ctx->fthreads;
-    const size_t smem = ctx->fsmem;
+    size_t smem = ctx->fsmem;
     if (ctx->dim == 1) {
+        // the multiplier-table region is needed only when the symbol comes from a table
+        const bool table = IO == IO_OP && io.f.mult != nullptr && io.f.sym < 0;
+        if (!table) smem = (size_t)padded(G.n0) * sizeof(double2);
         // KEEP (register-resident inputs, <= 160 threads, 4 CTAs/SM) for N <= 1280
-        auto kern = T > 160 ? (ctx->fept <= 8 ? k_fft1d<8, false, IO> : k_fft1d<16, false, IO>)
+        static const bool nokeep = getenv("ACP_FFT_NOKEEP") != nullptr;
+        auto kern = (T > 160 || nokeep) ? (ctx->fept <= 8 ? k_fft1d<8, false, IO> : k_fft1d<16, false, IO>)
                   : ctx->fept <= 2 ? k_fft1d<2, true, IO> : ctx->fept <= 4 ? k_fft1d<4, true, IO>
                   : k_fft1d<8, true, IO>;
-        set_smem_attr((const void*)kern, smem, false);
+        set_smem_attr((const void*)kern, ctx->fsmem, false);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(npair, 1, 1);
         cfg.blockDim = dim3(T, 1, 1);
