@@ -90,6 +90,7 @@ struct acp_context {
     int fnp = 1;                         // 2D: column pairs per cluster for operator launches
     bool pdl = false;                    // launch with programmatic dependent launch (PCG graph)
     int fthreads1 = 0, fept1 = 0;        // 2D: geometry of the one-pair setup transforms
+    int fct = 0;                         // 1D: a compiled-length FFT kernel matches the plan
     size_t fsmem1 = 0;
 
     std::map<std::string, acp::DevBuf> bufs;

@@ -128,7 +128,8 @@ __device__ __forceinline__ double sym_value(const FftGeom& G, int sym, double ta
 // Each thread keeps its input values (i = tid + q T) in registers for the epilogue and
 // prefetches the potential before the second FFT, so no global load sits on the critical path
 // after the initial one.
-template <int EPT, bool KEEP, int IO>
+// NCT != 0: the FFT length is the compile-time constant NCT (fft_ct), else the runtime plan.
+template <int EPT, bool KEEP, int IO, int NCT = 0>
 __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGeom G, const double2* __restrict__ twg,
                                                              IoArgs io) {
     extern __shared__ __align__(16) double2 sm1[];
@@ -194,7 +195,10 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
     cp_async_wait_all_fe();  // twiddles and the multiplier
     __syncthreads();
     K1_TP(1)
-    if (do_fft) fft_inplace<EPT>(buf, N, 1, G.p0, tw);
+    if (do_fft) {
+        if constexpr (NCT != 0) fft_ct<NCT, EPT>(buf, tw);
+        else fft_inplace<EPT>(buf, N, 1, G.p0, tw);
+    }
     K1_TP(2)
     if (IO == IO_HERM) {
         for (int i = tid; i < N; i += T) {
@@ -226,7 +230,8 @@ __global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGe
         }
         __syncthreads();
         K1_TP(3)
-        fft_inplace<EPT>(buf, N, 1, G.p0, tw);
+        if constexpr (NCT != 0) fft_ct<NCT, EPT>(buf, tw);
+        else fft_inplace<EPT>(buf, N, 1, G.p0, tw);
     }
     K1_TP(4)
     const double s0 = a.shift ? a.shift[c0] : 0.0;
@@ -527,6 +532,13 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
         auto kern = (T > 160 || nokeep) ? (ctx->fept <= 8 ? k_fft1d<8, false, IO> : k_fft1d<16, false, IO>)
                   : ctx->fept <= 2 ? k_fft1d<2, true, IO> : ctx->fept <= 4 ? k_fft1d<4, true, IO>
                   : k_fft1d<8, true, IO>;
+        // compiled-length kernels for the configs' grids (hot path only; ACP_FFT_GENERIC=1 off)
+        if (IO == IO_OP && ctx->fct && !nokeep) {
+            if (G.n0 == 1280 && T <= 160 && ctx->fept == 8) kern = k_fft1d<8, true, IO, 1280>;
+            else if (G.n0 == 960 && T <= 160 && ctx->fept == 8) kern = k_fft1d<8, true, IO, 960>;
+            else if (G.n0 == 256 && T <= 160 && ctx->fept == 4) kern = k_fft1d<4, true, IO, 256>;
+            else if (G.n0 == 5120 && T > 160 && ctx->fept == 8) kern = k_fft1d<8, false, IO, 5120>;
+        }
         set_smem_attr((const void*)kern, ctx->fsmem, false);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(npair, 1, 1);
@@ -967,6 +979,16 @@ void fft_init(acp_context* ctx) {
         ctx->fept = ept_for(N, T);
         ACP_REQUIRE(ctx->fept > 0, "1D grid too large for the shared-memory FFT");
         ctx->fsmem = (size_t)padded(N) * sizeof(double2) + (size_t)N * sizeof(double);  // twiddles via L1
+        // compiled-length FFT when the plan's radix schedule equals the compiled one
+        auto same = [&](const int* r, int nr) {
+            if (ctx->plan.npass != nr) return false;
+            for (int q = 0; q < nr; ++q)
+                if (ctx->plan.radix[q] != r[q]) return false;
+            return true;
+        };
+        ctx->fct = !getenv("ACP_FFT_GENERIC") &&
+                   ((N == 1280 && same(CtRadices<1280>::r, 4)) || (N == 5120 && same(CtRadices<5120>::r, 5)) ||
+                    (N == 960 && same(CtRadices<960>::r, 4)) || (N == 256 && same(CtRadices<256>::r, 3)));
         ACP_REQUIRE(ctx->fsmem <= 220 * 1024, "1D grid too large for the shared-memory FFT");
     } else {
         // smallest cluster (cs | n0, cs | n1, cs <= 16) whose per-CTA slice has <= 4096 points

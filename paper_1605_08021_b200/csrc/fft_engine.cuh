@@ -148,6 +148,82 @@ __device__ __forceinline__ void pass_inplace(double2* buf, int L, int ld, int nb
     __syncthreads();
 }
 
+// Compile-time Stockham pass for ONE transform of length L (the 1D kernels): the same data
+// movement and arithmetic as pass_inplace, but every index is a constant expression of the
+// butterfly index j, and strides that are multiples of 8 make the padded index linear in r
+// (P(b + r s) = P(b) + r (s + s/8)), so an element costs an immediate offset instead of a pad
+// computation.
+template <int R, int L, int NS, int EPT>
+__device__ __forceinline__ void pass_ct(double2* buf, const double2* __restrict__ tw) {
+    constexpr int PER = L / R;
+    constexpr int MB = (EPT + R - 1) / R;
+    double2 x[MB][R];
+#pragma unroll
+    for (int b = 0; b < MB; ++b) {
+        const int j = threadIdx.x + b * blockDim.x;
+        if (j < PER) {
+            if constexpr (PER % 8 == 0) {
+                const int pb = P(j);
+#pragma unroll
+                for (int r = 0; r < R; ++r) x[b][r] = buf[pb + r * (PER + PER / 8)];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) x[b][r] = buf[P(j + r * PER)];
+            }
+            if constexpr (NS > 1) {
+                const double2* tk = tw + (j % NS) * (R - 1);
+#pragma unroll
+                for (int r = 1; r < R; ++r) x[b][r] = cmul(x[b][r], tk[r - 1]);
+            }
+            dft<R>(x[b]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < MB; ++b) {
+        const int j = threadIdx.x + b * blockDim.x;
+        if (j < PER) {
+            const int k = j % NS;
+            const int b2 = (j - k) * R + k;
+            if constexpr (NS % 8 == 0) {
+                const int pb = P(b2);
+#pragma unroll
+                for (int r = 0; r < R; ++r) buf[pb + r * (NS + NS / 8)] = x[b][r];
+            } else if constexpr (NS == 1 && R == 8) {
+                const int pb = P(b2);  // b2 = 8 j: the 8 outputs share one pad block
+#pragma unroll
+                for (int r = 0; r < R; ++r) buf[pb + r] = x[b][r];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) buf[P(b2 + r * NS)] = x[b][r];
+            }
+        }
+    }
+    __syncthreads();
+}
+
+template <int EPT, int L, int NS, int OFF, int R, int... Rs>
+__device__ __forceinline__ void fft_ct_passes(double2* buf, const double2* __restrict__ tw) {
+    pass_ct<R, L, NS, EPT>(buf, tw + OFF);
+    if constexpr (sizeof...(Rs) > 0) fft_ct_passes<EPT, L, NS * R, OFF + NS * (R - 1), Rs...>(buf, tw);
+}
+
+// Radix schedules of the compiled lengths -- identical to make_plan's (8s, then 4, 2, 5, 3),
+// which the host checks before selecting a compiled kernel (the twiddle tables follow the plan).
+template <int N> struct CtRadices;
+template <> struct CtRadices<1280> { static constexpr int r[] = {8, 8, 4, 5}; };
+template <> struct CtRadices<5120> { static constexpr int r[] = {8, 8, 8, 2, 5}; };
+template <> struct CtRadices<960> { static constexpr int r[] = {8, 8, 5, 3}; };
+template <> struct CtRadices<256> { static constexpr int r[] = {8, 8, 4}; };
+
+template <int N, int EPT>
+__device__ __forceinline__ void fft_ct(double2* buf, const double2* __restrict__ tw) {
+    if constexpr (N == 1280) fft_ct_passes<EPT, 1280, 1, 0, 8, 8, 4, 5>(buf, tw);
+    else if constexpr (N == 5120) fft_ct_passes<EPT, 5120, 1, 0, 8, 8, 8, 2, 5>(buf, tw);
+    else if constexpr (N == 960) fft_ct_passes<EPT, 960, 1, 0, 8, 8, 5, 3>(buf, tw);
+    else if constexpr (N == 256) fft_ct_passes<EPT, 256, 1, 0, 8, 8, 4>(buf, tw);
+}
+
 // Forward FFT (exp(-i ...)) of nb transforms of length pl.N in place (transform t at buf + t*ld).
 template <int EPT>
 __device__ __forceinline__ void fft_inplace(double2* buf, int ld, int nb, const FftPlan& pl,

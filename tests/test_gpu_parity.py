@@ -108,6 +108,30 @@ def test_fourier_operator_2d_cluster_sizes(cs, np_pairs, monkeypatch):
     ctx.close()
 
 
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("name", ["c0_1d_tiny", "c1_1d_insulator", "c2_1d_semiconductor"])
+def test_fourier_operator_compiled_lengths(name, generic, monkeypatch):
+    """1D K1 at the configs' grid lengths (256, 1280, 5120): the compiled-length FFT kernels
+    (default) and the runtime-plan kernels (ACP_FFT_GENERIC) vs numpy's FFT, odd column count."""
+    from paper_1605_08021_b200 import Context
+    if generic:
+        monkeypatch.setenv("ACP_FFT_GENERIC", "1")
+    cfg = get_config(name)
+    ctx = Context.from_config(cfg)
+    N, L = cfg.grid[0], cfg.cell[0]
+    rng = np.random.default_rng(N)
+    X = rng.standard_normal((5, N))
+    k = 2 * np.pi * np.fft.fftfreq(N, d=L / N)
+    ref = np.real(np.fft.ifft(np.fft.fft(X, axis=1) * (0.5 * k * k)[None], axis=1))
+    Y = ctx.fourier_apply(T(X), 0).cpu().numpy()
+    assert rel(Y, ref) < 1e-12
+    V = rng.standard_normal(N)
+    sh = rng.standard_normal(5)
+    Y2 = ctx.fourier_apply(T(X), 0, diag=T(V), shift=T(sh)).cpu().numpy()
+    assert rel(Y2, ref + (V[None, :] - sh[:, None]) * X) < 1e-12
+    ctx.close()
+
+
 def test_fourier_operator_2d_three_pass():
     """Default 2D K1: row pass, column pass (symbol), row pass + epilogue through the HBM
     intermediate, vs the oracle's operators; odd column counts leave a half-empty last pair."""
