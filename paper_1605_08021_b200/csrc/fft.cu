@@ -600,7 +600,8 @@ __device__ __forceinline__ bool f2_pair_active(const FopArgs& a, int c0) {
     return !a.active || a.active[c0] || (h1 && a.active[c0 + 1]);
 }
 
-template <int EPT>
+// NCT != 0: square grid n0 = n1 = NCT with compile-time FFT indexing (fft_ct).
+template <int EPT, int NCT = 0>
 __global__ void __launch_bounds__(256, 3) k_f2_rows_fwd(FftGeom G, const double2* __restrict__ twg, FopArgs a,
                                                      double2* __restrict__ Z, int pair0) {
     extern __shared__ __align__(16) double2 f2s[];
@@ -616,12 +617,13 @@ __global__ void __launch_bounds__(256, 3) k_f2_rows_fwd(FftGeom G, const double2
     for (int e = threadIdx.x; e < E; e += blockDim.x) buf[P(e)] = make_double2(x0[e], h1 ? x1[e] : 0.0);
     cp_async_wait_all_fe();
     __syncthreads();
-    fft_inplace<EPT>(buf, n1, F2_RB, G.p1, tw);
+    if constexpr (NCT != 0) fft_ct<NCT, EPT, F2_RB, NCT>(buf, tw);
+    else fft_inplace<EPT>(buf, n1, F2_RB, G.p1, tw);
     double2* z = Z + (size_t)blockIdx.y * N + rb;
     for (int e = threadIdx.x; e < E; e += blockDim.x) z[e] = buf[P(e)];
 }
 
-template <int EPT>
+template <int EPT, int NCT = 0>
 __global__ void __launch_bounds__(256, 3) k_f2_cols(FftGeom G, const double2* __restrict__ twg, FopArgs a,
                                                  double2* __restrict__ Z, int pair0) {
     extern __shared__ __align__(16) double2 f2s[];
@@ -638,7 +640,8 @@ __global__ void __launch_bounds__(256, 3) k_f2_cols(FftGeom G, const double2* __
     }
     cp_async_wait_all_fe();
     __syncthreads();
-    fft_inplace<EPT>(buf, ld, F2_CB, G.p0, tw);
+    if constexpr (NCT != 0) fft_ct<NCT, EPT, F2_CB, NCT + 8>(buf, tw);
+    else fft_inplace<EPT>(buf, ld, F2_CB, G.p0, tw);
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
         const int c = e / n0, k0 = e - c * n0;
         const int k1 = k1b + c;
@@ -648,14 +651,15 @@ __global__ void __launch_bounds__(256, 3) k_f2_cols(FftGeom G, const double2* __
         buf[o] = make_double2(m * v.x, -m * v.y);
     }
     __syncthreads();
-    fft_inplace<EPT>(buf, ld, F2_CB, G.p0, tw);
+    if constexpr (NCT != 0) fft_ct<NCT, EPT, F2_CB, NCT + 8>(buf, tw);
+    else fft_inplace<EPT>(buf, ld, F2_CB, G.p0, tw);
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
         const int i0 = e / F2_CB, c = e - i0 * F2_CB;
         z[(size_t)i0 * n1 + c] = buf[P(c * ld + i0)];
     }
 }
 
-template <int EPT>
+template <int EPT, int NCT = 0>
 __global__ void __launch_bounds__(256, 3) k_f2_rows_inv(FftGeom G, const double2* __restrict__ twg, FopArgs a,
                                                      const double2* __restrict__ Z, int pair0,
                                                      double* __restrict__ part) {
@@ -671,7 +675,8 @@ __global__ void __launch_bounds__(256, 3) k_f2_rows_inv(FftGeom G, const double2
     for (int e = threadIdx.x; e < E; e += blockDim.x) buf[P(e)] = z[e];
     cp_async_wait_all_fe();
     __syncthreads();
-    fft_inplace<EPT>(buf, n1, F2_RB, G.p1, tw);
+    if constexpr (NCT != 0) fft_ct<NCT, EPT, F2_RB, NCT>(buf, tw);
+    else fft_inplace<EPT>(buf, n1, F2_RB, G.p1, tw);
     const bool h1 = c1 < a.n;
     const bool act0 = !a.active || a.active[c0];
     const bool act1 = h1 && (!a.active || a.active[c1]);
@@ -753,6 +758,18 @@ static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
     auto ra = er <= 8 ? k_f2_rows_fwd<8> : k_f2_rows_fwd<16>;
     auto cb = ec <= 8 ? k_f2_cols<8> : k_f2_cols<16>;
     auto rc = er <= 8 ? k_f2_rows_inv<8> : k_f2_rows_inv<16>;
+    // compiled-length kernels for the square configs grids (plans checked in fft_init)
+    if (ctx->fct && n0 == n1 && er <= 8 && ec <= 8) {
+        if (n0 == 192) {
+            ra = k_f2_rows_fwd<8, 192>;
+            cb = k_f2_cols<8, 192>;
+            rc = k_f2_rows_inv<8, 192>;
+        } else if (n0 == 256) {
+            ra = k_f2_rows_fwd<8, 256>;
+            cb = k_f2_cols<8, 256>;
+            rc = k_f2_rows_inv<8, 256>;
+        }
+    }
     set_smem_attr((const void*)ra, sr, false);
     set_smem_attr((const void*)cb, sc, false);
     set_smem_attr((const void*)rc, sr, false);
@@ -991,6 +1008,15 @@ void fft_init(acp_context* ctx) {
                     (N == 960 && same(CtRadices<960>::r, 4)) || (N == 256 && same(CtRadices<256>::r, 3)));
         ACP_REQUIRE(ctx->fsmem <= 220 * 1024, "1D grid too large for the shared-memory FFT");
     } else {
+        auto same2 = [&](const FftPlan& pl, const int* r, int nr) {
+            if (pl.npass != nr) return false;
+            for (int q = 0; q < nr; ++q)
+                if (pl.radix[q] != r[q]) return false;
+            return true;
+        };
+        ctx->fct = !getenv("ACP_FFT_GENERIC") && n0 == n1 &&
+                   ((n0 == 192 && same2(ctx->plan, CtRadices<192>::r, 3) && same2(ctx->plan1, CtRadices<192>::r, 3)) ||
+                    (n0 == 256 && same2(ctx->plan, CtRadices<256>::r, 3) && same2(ctx->plan1, CtRadices<256>::r, 3)));
         // smallest cluster (cs | n0, cs | n1, cs <= 16) whose per-CTA slice has <= 4096 points
         auto slice = [&](int c) { return std::max((n0 / c) * n1, (n1 / c) * (n0 + 8)); };
         auto bytes = [&](int c) {

@@ -148,27 +148,32 @@ __device__ __forceinline__ void pass_inplace(double2* buf, int L, int ld, int nb
     __syncthreads();
 }
 
-// Compile-time Stockham pass for ONE transform of length L (the 1D kernels): the same data
-// movement and arithmetic as pass_inplace, but every index is a constant expression of the
-// butterfly index j, and strides that are multiples of 8 make the padded index linear in r
-// (P(b + r s) = P(b) + r (s + s/8)), so an element costs an immediate offset instead of a pad
-// computation.
-template <int R, int L, int NS, int EPT>
+// Compile-time Stockham pass over NB transforms of length L (transform t at buf + t*LD; NB = 1
+// for the 1D kernels): the same data movement and arithmetic as pass_inplace, but every index is
+// a constant expression of the butterfly index, and strides that are multiples of 8 make the
+// padded index linear in r (P(b + r s) = P(b) + r (s + s/8)), so an element costs an immediate
+// offset instead of a pad computation.
+template <int R, int L, int NS, int NB, int LD, int EPT>
 __device__ __forceinline__ void pass_ct(double2* buf, const double2* __restrict__ tw) {
     constexpr int PER = L / R;
+    constexpr int TOTAL = NB * PER;
     constexpr int MB = (EPT + R - 1) / R;
+    constexpr bool LIN_LD = PER % 8 == 0 && (NB == 1 || LD % 8 == 0);
     double2 x[MB][R];
 #pragma unroll
     for (int b = 0; b < MB; ++b) {
-        const int j = threadIdx.x + b * blockDim.x;
-        if (j < PER) {
-            if constexpr (PER % 8 == 0) {
-                const int pb = P(j);
+        const int g = threadIdx.x + b * blockDim.x;
+        if (g < TOTAL) {
+            const int t = NB == 1 ? 0 : g / PER;
+            const int j = g - t * PER;
+            const int base = t * LD + j;
+            if constexpr (LIN_LD) {
+                const int pb = P(base);
 #pragma unroll
                 for (int r = 0; r < R; ++r) x[b][r] = buf[pb + r * (PER + PER / 8)];
             } else {
 #pragma unroll
-                for (int r = 0; r < R; ++r) x[b][r] = buf[P(j + r * PER)];
+                for (int r = 0; r < R; ++r) x[b][r] = buf[P(base + r * PER)];
             }
             if constexpr (NS > 1) {
                 const double2* tk = tw + (j % NS) * (R - 1);
@@ -181,16 +186,18 @@ __device__ __forceinline__ void pass_ct(double2* buf, const double2* __restrict_
     __syncthreads();
 #pragma unroll
     for (int b = 0; b < MB; ++b) {
-        const int j = threadIdx.x + b * blockDim.x;
-        if (j < PER) {
+        const int g = threadIdx.x + b * blockDim.x;
+        if (g < TOTAL) {
+            const int t = NB == 1 ? 0 : g / PER;
+            const int j = g - t * PER;
             const int k = j % NS;
-            const int b2 = (j - k) * R + k;
-            if constexpr (NS % 8 == 0) {
+            const int b2 = t * LD + (j - k) * R + k;
+            if constexpr (NS % 8 == 0 && (NB == 1 || LD % 8 == 0)) {
                 const int pb = P(b2);
 #pragma unroll
                 for (int r = 0; r < R; ++r) buf[pb + r * (NS + NS / 8)] = x[b][r];
-            } else if constexpr (NS == 1 && R == 8) {
-                const int pb = P(b2);  // b2 = 8 j: the 8 outputs share one pad block
+            } else if constexpr (NS == 1 && R == 8 && (NB == 1 || LD % 8 == 0)) {
+                const int pb = P(b2);  // b2 = t LD + 8 j: the 8 outputs share one pad block
 #pragma unroll
                 for (int r = 0; r < R; ++r) buf[pb + r] = x[b][r];
             } else {
@@ -202,10 +209,10 @@ __device__ __forceinline__ void pass_ct(double2* buf, const double2* __restrict_
     __syncthreads();
 }
 
-template <int EPT, int L, int NS, int OFF, int R, int... Rs>
+template <int EPT, int L, int NB, int LD, int NS, int OFF, int R, int... Rs>
 __device__ __forceinline__ void fft_ct_passes(double2* buf, const double2* __restrict__ tw) {
-    pass_ct<R, L, NS, EPT>(buf, tw + OFF);
-    if constexpr (sizeof...(Rs) > 0) fft_ct_passes<EPT, L, NS * R, OFF + NS * (R - 1), Rs...>(buf, tw);
+    pass_ct<R, L, NS, NB, LD, EPT>(buf, tw + OFF);
+    if constexpr (sizeof...(Rs) > 0) fft_ct_passes<EPT, L, NB, LD, NS * R, OFF + NS * (R - 1), Rs...>(buf, tw);
 }
 
 // Radix schedules of the compiled lengths -- identical to make_plan's (8s, then 4, 2, 5, 3),
@@ -215,13 +222,16 @@ template <> struct CtRadices<1280> { static constexpr int r[] = {8, 8, 4, 5}; };
 template <> struct CtRadices<5120> { static constexpr int r[] = {8, 8, 8, 2, 5}; };
 template <> struct CtRadices<960> { static constexpr int r[] = {8, 8, 5, 3}; };
 template <> struct CtRadices<256> { static constexpr int r[] = {8, 8, 4}; };
+template <> struct CtRadices<192> { static constexpr int r[] = {8, 8, 3}; };
 
-template <int N, int EPT>
+// NB transforms of the compiled length N at stride LD (NB = 1: one transform, LD unused).
+template <int N, int EPT, int NB = 1, int LD = 0>
 __device__ __forceinline__ void fft_ct(double2* buf, const double2* __restrict__ tw) {
-    if constexpr (N == 1280) fft_ct_passes<EPT, 1280, 1, 0, 8, 8, 4, 5>(buf, tw);
-    else if constexpr (N == 5120) fft_ct_passes<EPT, 5120, 1, 0, 8, 8, 8, 2, 5>(buf, tw);
-    else if constexpr (N == 960) fft_ct_passes<EPT, 960, 1, 0, 8, 8, 5, 3>(buf, tw);
-    else if constexpr (N == 256) fft_ct_passes<EPT, 256, 1, 0, 8, 8, 4>(buf, tw);
+    if constexpr (N == 1280) fft_ct_passes<EPT, 1280, NB, LD, 1, 0, 8, 8, 4, 5>(buf, tw);
+    else if constexpr (N == 5120) fft_ct_passes<EPT, 5120, NB, LD, 1, 0, 8, 8, 8, 2, 5>(buf, tw);
+    else if constexpr (N == 960) fft_ct_passes<EPT, 960, NB, LD, 1, 0, 8, 8, 5, 3>(buf, tw);
+    else if constexpr (N == 256) fft_ct_passes<EPT, 256, NB, LD, 1, 0, 8, 8, 4>(buf, tw);
+    else if constexpr (N == 192) fft_ct_passes<EPT, 192, NB, LD, 1, 0, 8, 8, 3>(buf, tw);
 }
 
 // Forward FFT (exp(-i ...)) of nb transforms of length pl.N in place (transform t at buf + t*ld).

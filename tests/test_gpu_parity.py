@@ -132,6 +132,29 @@ def test_fourier_operator_compiled_lengths(name, generic, monkeypatch):
     ctx.close()
 
 
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("name", ["c3g_2d_8x8", "c4g_2d_16x16"])
+def test_fourier_operator_2d_compiled_lengths(name, generic, monkeypatch):
+    """2D K1 (three passes) on the configs' square grids 192^2 / 256^2: compiled-length FFT
+    passes (default) and runtime-plan passes (ACP_FFT_GENERIC) vs numpy's fft2."""
+    from paper_1605_08021_b200 import Context
+    if generic:
+        monkeypatch.setenv("ACP_FFT_GENERIC", "1")
+    cfg = get_config(name)
+    ctx = Context.from_config(cfg)
+    n0, n1 = cfg.grid
+    L0, L1 = cfg.cell
+    rng = np.random.default_rng(n0)
+    X = rng.standard_normal((3, n0, n1))
+    k0 = 2 * np.pi * np.fft.fftfreq(n0, d=L0 / n0)
+    k1 = 2 * np.pi * np.fft.fftfreq(n1, d=L1 / n1)
+    k2 = k0[:, None] ** 2 + k1[None, :] ** 2
+    ref = np.real(np.fft.ifft2(np.fft.fft2(X) * (0.5 * k2)[None]))
+    Y = ctx.fourier_apply(T(X.reshape(3, -1)), 0).cpu().numpy().reshape(3, n0, n1)
+    assert rel(Y, ref) < 1e-12
+    ctx.close()
+
+
 def test_fourier_operator_2d_three_pass():
     """Default 2D K1: row pass, column pass (symbol), row pass + epilogue through the HBM
     intermediate, vs the oracle's operators; odd column counts leave a half-empty last pair."""
