@@ -55,7 +55,7 @@ int acp_create(const acp_system* sys, int device, acp_context** out) {
         ACP_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
         ctx->stream = ctx->own_stream;
         ACP_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-        for (int g = 1; g < 4; ++g) {
+        for (int g = 1; g < acp::PCG_MAXG; ++g) {
             ACP_CUDA(cudaStreamCreateWithFlags(&ctx->gstream[g], cudaStreamNonBlocking));
             ACP_CUDA(cudaEventCreateWithFlags(&ctx->ev_join[g], cudaEventDisableTiming));
         }
@@ -83,7 +83,7 @@ int acp_destroy(acp_context* ctx) {
         if (kv.second.ptr) cudaFree(kv.second.ptr);
     acp::fft_free(ctx);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
-    for (int g = 1; g < 4; ++g) {
+    for (int g = 1; g < acp::PCG_MAXG; ++g) {
         if (ctx->gstream[g]) {
             cudaStreamSynchronize(ctx->gstream[g]);
             cudaStreamDestroy(ctx->gstream[g]);

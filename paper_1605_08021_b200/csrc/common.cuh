@@ -16,7 +16,7 @@
 
 namespace acp {
 
-constexpr int PCG_MAXG = 4;  // concurrent PCG node groups (streams)
+constexpr int PCG_MAXG = 8;  // concurrent PCG node groups (streams)
 
 struct Error : public std::runtime_error {
     int code;
@@ -62,9 +62,9 @@ struct acp_context {
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
     // PCG node groups 1.. run on gstream[g] (forked from / joined to `stream`)
-    cudaStream_t gstream[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t gstream[acp::PCG_MAXG] = {};
     cudaEvent_t ev_fork = nullptr;
-    cudaEvent_t ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_join[acp::PCG_MAXG] = {};
     int f2_alt = 0;                       // 2D K1 workspace selector: the group being enqueued
     std::string err;
     long long launches = 0;

@@ -458,6 +458,7 @@ __global__ void k_count_active(const int* __restrict__ active, int n, int* __res
 // Phi_c = Psi B_c with B_c(i, mu) = L(i, c) Psi(r_mu, i) is a genuine GEMM (N_g x N_occ x N_mu):
 // one DMMA GEMM per node whose epilogue accumulates W += 2f X_c (.) Phi_c (nodes in order).
 constexpr int W_MAXC = 32;
+constexpr int PCG_DEFG = 4;  // default group count for small batches (PCG_MAXG with ACP_PCG_GROUPS)
 __global__ void k_w_rhs(int Ng, int n_occ, int nc, int cnt, const double* __restrict__ Psi,
                         const double* __restrict__ L, const int* __restrict__ S, int mu_begin,
                         double* __restrict__ B) {
@@ -738,7 +739,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     // batches only (n N_g <= 16M points): configs[1] 12.38 (4 groups) / 12.64 (2) / 13.01 (1)
     // ms/step; configs[2] gains nothing (270.5 / 271.3 / 272.8).  ACP_PCG_GROUPS overrides (each
     // 2D group needs its own FFT intermediate).
-    int ngroups = (size_t)n * Ng <= ((size_t)16 << 20) ? std::min(n_c, PCG_MAXG) : 1;
+    int ngroups = (size_t)n * Ng <= ((size_t)16 << 20) ? std::min(n_c, PCG_DEFG) : 1;
     if (const char* e = getenv("ACP_PCG_GROUPS")) ngroups = std::max(1, std::min(std::min(n_c, PCG_MAXG), atoi(e)));
     if (getenv("ACP_PCG_HOSTLOOP")) ngroups = 1;
     if (ngroups < 1) ngroups = 1;
