@@ -66,6 +66,12 @@ struct acp_context {
     cudaEvent_t ev_fork = nullptr;
     cudaEvent_t ev_join[acp::PCG_MAXG] = {};
     int f2_alt = 0;                       // 2D K1 workspace selector: the group being enqueued
+    // Deferred checks (acp_dyson): PCG statistics / convergence, LU status and the iteration
+    // differences stay on the device (defer_stats, indexed by defer_iter) and are read once at the
+    // end, so an outer iteration has a single host synchronisation (the QRCP rank N_mu).
+    int defer = 0;
+    int defer_iter = 0;
+    long long* defer_stats = nullptr;  // see DeferStats in pcg.cu
     std::string err;
     long long launches = 0;
 

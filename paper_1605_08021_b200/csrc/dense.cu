@@ -504,8 +504,9 @@ __global__ void __launch_bounds__(512) k_lu_panel_warp(double* __restrict__ AB, 
 void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
     const int ntot = n + nrhs;
     int* piv = ctx->wsi("lu_piv", n);
-    int* st = ctx->wsi("lu_status", 1);
-    ACP_CUDA(cudaMemsetAsync(st, 0, sizeof(int), ctx->stream));
+    // deferred mode (acp_dyson): the status accumulates in the device statistics, read at the end
+    int* st = ctx->defer ? reinterpret_cast<int*>(ctx->defer_stats + 6) : ctx->wsi("lu_status", 1);
+    if (!ctx->defer) ACP_CUDA(cudaMemsetAsync(st, 0, sizeof(int), ctx->stream));
     static bool attr = false;
     if (!attr) {
         ACP_CUDA(cudaFuncSetAttribute(k_lu_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -548,6 +549,7 @@ void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
                     AB + (size_t)r0 * n + r0, n);
     }
     upper_solve_blocked(ctx, AB, n, nrhs);
+    if (ctx->defer) return;
     int* hp = static_cast<int*>(ctx->pinned);
     ACP_CUDA(cudaMemcpyAsync(hp, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ACP_CUDA(cudaStreamSynchronize(ctx->stream));

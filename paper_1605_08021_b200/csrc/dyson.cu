@@ -94,33 +94,81 @@ void dyson(acp_context* ctx, const double* Psi, const double* eps, const double*
     double* W = ctx->wsd("dy_W", (size_t)Ng * nmu_max);
     copy_cols(ctx, Gp, G, (size_t)Ng * n);
     fill(ctx, Uprev, (size_t)Ng * n, 0.0);
+    // Checks deferred to the end (one host synchronisation per outer iteration: N_mu)
+    const int nst = 8 + 2 * o.n_outer;
+    long long* dstats = reinterpret_cast<long long*>(ctx->ws("dy_stats", nst * sizeof(long long)));
+    double* dpart = ctx->wsd("dy_dn_part", (size_t)o.n_outer * 256);
+    ACP_CUDA(cudaMemsetAsync(dstats, 0, nst * sizeof(long long), ctx->stream));
+    std::vector<int> Ns(o.n_outer);
+    struct DeferGuard {
+        acp_context* c;
+        ~DeferGuard() { c->defer = 0; }
+    } guard{ctx};
+    ctx->defer = getenv("ACP_DYSON_SYNC") ? 0 : 1;
+    ctx->defer_stats = dstats;
     long long total_solves = 0, total_it = 0;
     int max_it = 0;
     double max_res = 0.0;
+    std::vector<double> dn_sync(o.n_outer, 0.0), it_sync(o.n_outer, 0.0);
     for (int k = 0; k < o.n_outer; ++k) {
         const int N = compress(ctx, Psi, Gp, n, h_theta + (size_t)k * n, h_nu + (size_t)k * o.r_half, o.r_half,
                                o.id_eps, o.n_mu_fixed, nmu_max, S, Xi);
+        Ns[k] = N;
+        ctx->defer_iter = k;
         PcgStats st;
         apply_chi0(ctx, Psi, eps, V, S, Xi, N, 0, N, o.n_cheb, o.cg_tol, o.max_cg_iter, W, &st);
         smw_update(ctx, G, S, W, N, U, Gp);
-        const double dn = diff_norm(ctx, U, Uprev, (size_t)Ng * n);
-        copy_cols(ctx, Uprev, U, (size_t)Ng * n);
-        total_solves += st.n_solved;
-        total_it += st.total_iter;
-        if (st.max_iter > max_it) max_it = st.max_iter;
-        if (st.max_rel_res > max_res) max_res = st.max_rel_res;
-        if (h_info) {
-            h_info[8 + 3 * k] = N;
-            h_info[8 + 3 * k + 1] = dn;
-            h_info[8 + 3 * k + 2] = (double)st.total_iter;
+        if (ctx->defer) {
+            k_diff_norm2<<<256, 256, 0, ctx->stream>>>((size_t)Ng * n, U, Uprev, dpart + (size_t)k * 256);
+            launched(ctx);
+        } else {
+            dn_sync[k] = diff_norm(ctx, U, Uprev, (size_t)Ng * n);
+            total_solves += st.n_solved;
+            total_it += st.total_iter;
+            if (st.max_iter > max_it) max_it = st.max_iter;
+            if (st.max_rel_res > max_res) max_res = st.max_rel_res;
+            it_sync[k] = (double)st.total_iter;
         }
+        copy_cols(ctx, Uprev, U, (size_t)Ng * n);
     }
-    sync(ctx);
+    std::vector<double> dn(o.n_outer), itk(o.n_outer);
+    if (ctx->defer) {
+        std::vector<long long> hs(nst);
+        std::vector<double> hp((size_t)o.n_outer * 256);
+        ACP_CUDA(cudaMemcpyAsync(hs.data(), dstats, nst * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+        ACP_CUDA(cudaMemcpyAsync(hp.data(), dpart, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        ctx->defer = 0;
+        ctx->launches += hs[3];
+        if (hs[6] != 0) throw Error(ACP_ERR_SINGULAR, "singular SMW core in blocked LU");
+        if (hs[4] != 0)
+            throw Error(ACP_ERR_NOT_CONVERGED,
+                        "Sternheimer PCG did not converge in " + std::to_string(o.max_cg_iter) + " iterations");
+        total_solves = hs[0];
+        total_it = hs[1];
+        max_it = (int)hs[2];
+        max_res = __builtin_bit_cast(double, hs[5]);
+        for (int k = 0; k < o.n_outer; ++k) {
+            double s2 = 0.0;
+            for (int b = 0; b < 256; ++b) s2 += hp[(size_t)k * 256 + b];  // same order as diff_norm
+            dn[k] = std::sqrt(s2);
+            itk[k] = (double)hs[8 + 2 * k];
+        }
+    } else {
+        sync(ctx);
+        dn = dn_sync;
+        itk = it_sync;
+    }
     if (h_info) {
         h_info[0] = (double)total_solves;
         h_info[1] = (double)total_it;
         h_info[2] = max_it;
         h_info[3] = max_res;
+        for (int k = 0; k < o.n_outer; ++k) {
+            h_info[8 + 3 * k] = Ns[k];
+            h_info[8 + 3 * k + 1] = dn[k];
+            h_info[8 + 3 * k + 2] = itk[k];
+        }
     }
 }
 

@@ -708,6 +708,55 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
     }
 }
 
+// Device-side PCG statistics for the deferred mode. Layout of the long long array `st`:
+//   [0] solves, [1] total iterations, [2] max iterations, [3] launches (graph trips x per-trip),
+//   [4] unconverged columns, [5] max relative residual (double bits), [6] LU status,
+//   [8 + 2k] iterations of outer iteration k, [9 + 2k] spare.
+struct PcgLaunchCounts {
+    long long per_trip[PCG_MAXG];
+};
+__global__ void k_pcg_accum_stats(int n, const int* __restrict__ iters, const double* __restrict__ res,
+                                  const double* __restrict__ bb, const int* __restrict__ nact, int ngroups,
+                                  PcgLaunchCounts lc, int k, long long* __restrict__ st) {
+    __shared__ long long r_n[256], r_it[256], r_mx[256];
+    __shared__ double r_res[256];
+    long long cnt = 0, it = 0, mx = 0;
+    double mr = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        if (bb[j] <= 0.0) continue;
+        cnt += 1;
+        it += iters[j];
+        mx = max(mx, (long long)iters[j]);
+        mr = fmax(mr, res[j]);
+    }
+    r_n[threadIdx.x] = cnt;
+    r_it[threadIdx.x] = it;
+    r_mx[threadIdx.x] = mx;
+    r_res[threadIdx.x] = mr;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int t = 1; t < blockDim.x; ++t) {
+            cnt += r_n[t];
+            it += r_it[t];
+            mx = max(mx, r_mx[t]);
+            mr = fmax(mr, r_res[t]);
+        }
+        st[0] += cnt;
+        st[1] += it;
+        st[2] = max(st[2], mx);
+        long long launches = 0, unconv = 0;
+        for (int g = 0; g < ngroups; ++g) {
+            launches += lc.per_trip[g] * nact[2 * g + 1];
+            unconv += nact[2 * g];
+        }
+        st[3] += launches;
+        st[4] += unconv;
+        const double prev = __longlong_as_double(st[5]);
+        st[5] = __double_as_longlong(fmax(prev, mr));
+        st[8 + 2 * k] = it;
+    }
+}
+
 void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const double* V, const double* d_shift_c,
                        int n_c, const double* rhs, int nmu_p, double tol, int max_iter, double tau, double* X,
                        PcgStats* st) {
@@ -782,7 +831,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     }
     if (ngroups == 1) {
         pcg_group_enqueue(ctx, Psi, n_occ, V, grp[0], nmu_p, tol2, tau, max_iter);
-        if (!grp[0].synced) ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (!grp[0].synced && !ctx->defer) ACP_CUDA(cudaStreamSynchronize(ctx->stream));
     } else {
         cudaStream_t s0 = ctx->stream;
         ACP_CUDA(cudaEventRecord(ctx->ev_fork, s0));
@@ -804,7 +853,18 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
             ACP_CUDA(cudaEventRecord(ctx->ev_join[g], ctx->gstream[g]));
             ACP_CUDA(cudaStreamWaitEvent(s0, ctx->ev_join[g], 0));
         }
-        ACP_CUDA(cudaStreamSynchronize(s0));
+        if (!ctx->defer) ACP_CUDA(cudaStreamSynchronize(s0));
+    }
+    if (ctx->defer) {
+        // no host wait: accumulate the statistics on the device (read at the end of acp_dyson)
+        long long lpt[PCG_MAXG] = {};
+        for (int g = 0; g < ngroups; ++g) lpt[g] = grp[g].synced ? 0 : grp[g].launches_per_trip;
+        PcgLaunchCounts lc;
+        for (int g = 0; g < PCG_MAXG; ++g) lc.per_trip[g] = lpt[g];
+        k_pcg_accum_stats<<<1, 256, 0, ctx->stream>>>(n, s.iters, s.res, s.bb, d_nact, ngroups, lc,
+                                                        ctx->defer_iter, ctx->defer_stats);
+        launched(ctx);
+        return;
     }
     bool converged = true;
     for (int g = 0; g < ngroups; ++g) {

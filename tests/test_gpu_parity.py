@@ -382,6 +382,26 @@ def _dyson_parity(s, n_outer=None):
     return res, D_o, lam_o, U_g.cpu().numpy().T, D_g, lam_g, info
 
 
+def test_dyson_deferred_checks_equal_synchronous(sysx, monkeypatch):
+    """acp_dyson keeps PCG statistics, LU status and iteration differences on the device until the
+    end (default) or synchronises after every stage (ACP_DYSON_SYNC): identical U and info."""
+    from paper_1605_08021_b200 import Context
+    s = sysx
+    cfg = s.cfg
+    n = s.G.shape[1]
+    th = np.stack([s.draws(k, n)[0] for k in range(cfg.n_outer)])
+    nu = np.stack([s.draws(k, n)[1] for k in range(cfg.n_outer)])
+    args = (s.Psi_t, s.eps_t, s.V_t, s.G_t, cfg.n_cheb, cfg.n_outer, th, nu)
+    U1, i1 = s.ctx.dyson(*args, id_eps=cfg.id_eps, cg_tol=cfg.cg_tol)
+    monkeypatch.setenv("ACP_DYSON_SYNC", "1")
+    ctx = Context.from_config(cfg)
+    U2, i2 = ctx.dyson(*args, id_eps=cfg.id_eps, cg_tol=cfg.cg_tol)
+    ctx.close()
+    assert torch.equal(U1, U2)
+    for key in i1:
+        assert np.array_equal(np.asarray(i1[key]), np.asarray(i2[key])), key
+
+
 def test_dyson_and_dynamical_matrix(sysx):
     s = sysx
     res, D_o, lam_o, U_g, D_g, lam_g, info = _dyson_parity(s)
