@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(128, 4) k_pcg_update(int M, int K, int n, cons
 }
 
 // Large-K variant (N_occ >= 64): 64 x 64 tiles, multistage cp.async, 256 threads.
-template <class Ep>
+template <class Ep, bool PF = true>
 __global__ void __launch_bounds__(256, 2) k_pcg_update_big(int M, int K, int n, const double* __restrict__ A, int lda,
                                                         const double* __restrict__ B, int ldb, Ep ep) {
     pdl_wait();
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update_big(int M, int K, int n, 
     }
     __syncthreads();
     if (!any) return;
-    nn_tile_big(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, n0, ep);
+    nn_tile_big<Ep, PF>(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, n0, ep);
 }
 
 template <class Ep>
@@ -224,16 +224,22 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
     cfg.attrs = at;
     cfg.numAttrs = ctx->pdl ? 1 : 0;
     if (K >= 64) {
+        // ACP_K3_PF=1: first epilogue half prefetched before the K loop (measured no faster on
+        // configs[2] / [3]: the 2-stage K loop is short; the default loads it after the loop)
+        static const bool nopf = getenv("ACP_K3_PF") == nullptr;
+        auto kern = nopf ? k_pcg_update_big<Ep, false> : k_pcg_update_big<Ep, true>;
         static bool attr = false;
         if (!attr) {
-            ACP_CUDA(cudaFuncSetAttribute(k_pcg_update_big<Ep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            ACP_CUDA(cudaFuncSetAttribute(k_pcg_update_big<Ep, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)nn_big_smem()));
+            ACP_CUDA(cudaFuncSetAttribute(k_pcg_update_big<Ep, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)nn_big_smem()));
             attr = true;
         }
         cfg.gridDim = dim3(cdiv(M, GB_BM), cdiv(n, GB_BN), 1);
         cfg.blockDim = dim3(256, 1, 1);
         cfg.dynamicSmemBytes = nn_big_smem();
-        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_pcg_update_big<Ep>, M, K, n, A, lda, B, ldb, ep));
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, M, K, n, A, lda, B, ldb, ep));
     } else {
         cfg.gridDim = dim3(cdiv(M, NP_BM), cdiv(n, NP_BN), 1);
         cfg.blockDim = dim3(128, 1, 1);
