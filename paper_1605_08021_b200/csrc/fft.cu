@@ -594,6 +594,10 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
 //               partials of a column in row-block order (fixed order, deterministic).
 // Same transform and inverse-by-conjugation as k_fft2d; different rounding order.
 constexpr int F2_RB = 8, F2_CB = 8;  // 8 x n values per CTA: <= 256 threads, 3 CTAs/SM
+// Z is stored in 8 x 8 tiles (tile (i0/8, k1/8) at ((i0/8) n1/8 + k1/8) * 64, row-major inside),
+// so a row block (passes A, C) is one contiguous range and a column block (pass B) is n0/8
+// contiguous 1 KB tiles instead of n0 strided 128-byte segments.
+static_assert(F2_RB == 8 && F2_CB == 8, "the tiled intermediate assumes 8-row / 8-column blocks");
 
 __device__ __forceinline__ bool f2_pair_active(const FopArgs& a, int c0) {
     const bool h1 = c0 + 1 < a.n;
@@ -619,29 +623,35 @@ __global__ void __launch_bounds__(256, 3) k_f2_rows_fwd(FftGeom G, const double2
     __syncthreads();
     if constexpr (NCT != 0) fft_ct<NCT, EPT, F2_RB, NCT>(buf, tw);
     else fft_inplace<EPT>(buf, n1, F2_RB, G.p1, tw);
-    double2* z = Z + (size_t)blockIdx.y * N + rb;
-    for (int e = threadIdx.x; e < E; e += blockDim.x) z[e] = buf[P(e)];
+    double2* z = Z + (size_t)blockIdx.y * N + rb;  // this row block: E contiguous values (8 x 8 tiles)
+    for (int o = threadIdx.x; o < E; o += blockDim.x) {
+        const int r = (o >> 3) & 7, k1 = ((o >> 6) << 3) | (o & 7);
+        z[o] = buf[P(r * n1 + k1)];
+    }
 }
 
-template <int EPT, int NCT = 0, int CB = F2_CB>
-__global__ void __launch_bounds__(CB == 8 ? 256 : 512, CB == 8 ? 3 : 1) k_f2_cols(FftGeom G, const double2* __restrict__ twg, FopArgs a,
+template <int EPT, int NCT = 0>
+__global__ void __launch_bounds__(256, 3) k_f2_cols(FftGeom G, const double2* __restrict__ twg, FopArgs a,
                                                  double2* __restrict__ Z, int pair0) {
     extern __shared__ __align__(16) double2 f2s[];
     const int pr = pair0 + blockIdx.y, c0 = 2 * pr;
     if (!f2_pair_active(a, c0)) return;
-    const int n0 = G.n0, n1 = G.n1, ld = G.ldc, E = CB * n0;
+    const int n0 = G.n0, n1 = G.n1, ld = G.ldc, E = F2_CB * n0;
     double2* buf = f2s;
-    const double2* tw = load_twiddles(f2s + padded(CB * ld), twg, G.p0);
-    const int k1b = blockIdx.x * CB;
-    double2* z = Z + (size_t)blockIdx.y * n0 * n1 + k1b;
+    const double2* tw = load_twiddles(f2s + padded(F2_CB * ld), twg, G.p0);
+    const int k1b = blockIdx.x * F2_CB;
+    // column block k1b / 8: tiles (ib, k1b / 8) for ib = 0 .. n0/8 - 1, 64 contiguous values each
+    double2* z = Z + (size_t)blockIdx.y * n0 * n1 + (size_t)blockIdx.x * 64;
+    const int tstride = (n1 / 8) * 64;
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        const int i0 = e / CB, c = e - i0 * CB;
-        buf[P(c * ld + i0)] = z[(size_t)i0 * n1 + c];
+        const int ib = e >> 6, w = e & 63;
+        const int i0 = (ib << 3) | (w >> 3), c = w & 7;
+        buf[P(c * ld + i0)] = z[(size_t)ib * tstride + w];
     }
     cp_async_wait_all_fe();
     __syncthreads();
-    if constexpr (NCT != 0) fft_ct<NCT, EPT, CB, NCT + 8>(buf, tw);
-    else fft_inplace<EPT>(buf, ld, CB, G.p0, tw);
+    if constexpr (NCT != 0) fft_ct<NCT, EPT, F2_CB, NCT + 8>(buf, tw);
+    else fft_inplace<EPT>(buf, ld, F2_CB, G.p0, tw);
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
         const int c = e / n0, k0 = e - c * n0;
         const int k1 = k1b + c;
@@ -651,11 +661,12 @@ __global__ void __launch_bounds__(CB == 8 ? 256 : 512, CB == 8 ? 3 : 1) k_f2_col
         buf[o] = make_double2(m * v.x, -m * v.y);
     }
     __syncthreads();
-    if constexpr (NCT != 0) fft_ct<NCT, EPT, CB, NCT + 8>(buf, tw);
-    else fft_inplace<EPT>(buf, ld, CB, G.p0, tw);
+    if constexpr (NCT != 0) fft_ct<NCT, EPT, F2_CB, NCT + 8>(buf, tw);
+    else fft_inplace<EPT>(buf, ld, F2_CB, G.p0, tw);
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        const int i0 = e / CB, c = e - i0 * CB;
-        z[(size_t)i0 * n1 + c] = buf[P(c * ld + i0)];
+        const int ib = e >> 6, w = e & 63;
+        const int i0 = (ib << 3) | (w >> 3), c = w & 7;
+        z[(size_t)ib * tstride + w] = buf[P(c * ld + i0)];
     }
 }
 
@@ -671,8 +682,11 @@ __global__ void __launch_bounds__(256, 3) k_f2_rows_inv(FftGeom G, const double2
     double2* buf = f2s;
     const double2* tw = load_twiddles(f2s + padded(E), twg, G.p1);
     const size_t rb = (size_t)blockIdx.x * E;
-    const double2* z = Z + (size_t)blockIdx.y * N + rb;
-    for (int e = threadIdx.x; e < E; e += blockDim.x) buf[P(e)] = z[e];
+    const double2* z = Z + (size_t)blockIdx.y * N + rb;  // this row block (8 x 8 tiles)
+    for (int o = threadIdx.x; o < E; o += blockDim.x) {
+        const int r = (o >> 3) & 7, k1 = ((o >> 6) << 3) | (o & 7);
+        buf[P(r * n1 + k1)] = z[o];
+    }
     cp_async_wait_all_fe();
     __syncthreads();
     if constexpr (NCT != 0) fft_ct<NCT, EPT, F2_RB, NCT>(buf, tw);
@@ -741,34 +755,32 @@ void fourier_reserve(acp_context* ctx, int n, int alt) {
 static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
     const FftGeom G = geom(ctx);
     const int n0 = G.n0, n1 = G.n1;
-    static const int cb16 = getenv("ACP_F2_CB16") ? 1 : 0;  // 16-column tiles (256-byte row segments)
-    const int CBv = cb16 ? 16 : F2_CB;
-    if (getenv("ACP_FFT2D_CLUSTER") || n0 % F2_RB || n1 % CBv) return false;
+    if (getenv("ACP_FFT2D_CLUSTER") || n0 % F2_RB || n1 % F2_CB) return false;
     if (a.mult == nullptr && a.sym < 0) return false;  // no transform: the cluster kernel's epilogue only
     const int npair = (a.n + 1) / 2;
     const int Tr = std::min(256, std::max(64, (F2_RB * n1 / 8 + 31) / 32 * 32));
-    const int Tc = std::min(cb16 ? 512 : 256, std::max(64, (CBv * n0 / 8 + 31) / 32 * 32));
-    const int er = (F2_RB * n1 + Tr - 1) / Tr, ec = (CBv * n0 + Tc - 1) / Tc;
+    const int Tc = std::min(256, std::max(64, (F2_CB * n0 / 8 + 31) / 32 * 32));
+    const int er = (F2_RB * n1 + Tr - 1) / Tr, ec = (F2_CB * n0 + Tc - 1) / Tc;
     if (er > 16 || ec > 16) return false;
     const size_t sr = (size_t)(padded(F2_RB * n1) + G.tw1n) * sizeof(double2);
-    const size_t sc = (size_t)(padded(CBv * G.ldc) + G.tw0n) * sizeof(double2);
+    const size_t sc = (size_t)(padded(F2_CB * G.ldc) + G.tw0n) * sizeof(double2);
     if (sr > 200 * 1024 || sc > 200 * 1024) return false;
-    const int nrb = n0 / F2_RB, ncb = n1 / CBv;
+    const int nrb = n0 / F2_RB, ncb = n1 / F2_CB;
     // each concurrent PCG group (its own stream, ctx->f2_alt) has its own intermediate
     double2* Z = static_cast<double2*>(ctx->ws(f2_name("f2_Z", ctx->f2_alt), (size_t)npair * n0 * n1 * sizeof(double2)));
     double* part = a.dots ? ctx->wsd(f2_name("f2_part", ctx->f2_alt), (size_t)npair * nrb * 4) : nullptr;
     auto ra = er <= 8 ? k_f2_rows_fwd<8> : k_f2_rows_fwd<16>;
-    auto cb = cb16 ? (ec <= 8 ? k_f2_cols<8, 0, 16> : k_f2_cols<16, 0, 16>) : (ec <= 8 ? k_f2_cols<8> : k_f2_cols<16>);
+    auto cb = ec <= 8 ? k_f2_cols<8> : k_f2_cols<16>;
     auto rc = er <= 8 ? k_f2_rows_inv<8> : k_f2_rows_inv<16>;
     // compiled-length kernels for the square configs grids (plans checked in fft_init)
     if (ctx->fct && n0 == n1 && er <= 8 && ec <= 8) {
         if (n0 == 192) {
             ra = k_f2_rows_fwd<8, 192>;
-            cb = cb16 ? k_f2_cols<8, 192, 16> : k_f2_cols<8, 192>;
+            cb = k_f2_cols<8, 192>;
             rc = k_f2_rows_inv<8, 192>;
         } else if (n0 == 256) {
             ra = k_f2_rows_fwd<8, 256>;
-            cb = cb16 ? k_f2_cols<8, 256, 16> : k_f2_cols<8, 256>;
+            cb = k_f2_cols<8, 256>;
             rc = k_f2_rows_inv<8, 256>;
         }
     }
