@@ -128,6 +128,75 @@ template <int KR, class ColP>
 __device__ __forceinline__ void qr_update_cols_warp(ColP colp, int warp, int nc, int c0, int cw, int j, int m,
                                                     double alpha, double tau, const double* __restrict__ v,
                                                     const int* __restrict__ dn, double* __restrict__ n2) {
+    // two columns per warp and iteration (lc, lc + nwarp): two independent load batches in flight
+    const int nwarp = blockDim.x >> 5, lane = threadIdx.x & 31;
+    for (int lc0 = warp; lc0 < nc; lc0 += 2 * nwarp) {
+        const int lc1 = lc0 + nwarp;
+        const bool has1 = lc1 < nc;
+        const bool piv0 = c0 + lc0 == cw, piv1 = has1 && c0 + lc1 == cw;
+        const bool live0 = !piv0 && !dn[lc0];
+        const bool live1 = has1 && !piv1 && !dn[lc1];
+        double* ca = colp(lc0);
+        double* cb = colp(has1 ? lc1 : lc0);
+        double ya[KR], yb[KR];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const int i = lane + 32 * k;
+            const bool in = i >= j && i < m;
+            ya[k] = (live0 && in) ? ca[i] : 0.0;
+            yb[k] = (live1 && in) ? cb[i] : 0.0;
+        }
+        double da = 0.0, db = 0.0;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const int i = lane + 32 * k;
+            if (i >= j && i < m) {
+                const double vi = v[i];
+                da += vi * ya[k];
+                db += vi * yb[k];
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            da += __shfl_xor_sync(0xffffffffu, da, o);
+            db += __shfl_xor_sync(0xffffffffu, db, o);
+        }
+        const double fa = tau * da, fb = tau * db;
+        double na = 0.0, nb = 0.0;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const int i = lane + 32 * k;
+            if (i >= j && i < m) {
+                const double vi = v[i];
+                const double ua = ya[k] - fa * vi, ub = yb[k] - fb * vi;
+                if (live0) ca[i] = ua;
+                if (live1) cb[i] = ub;
+                if (i > j) {
+                    na += ua * ua;
+                    nb += ub * ub;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            na += __shfl_xor_sync(0xffffffffu, na, o);
+            nb += __shfl_xor_sync(0xffffffffu, nb, o);
+        }
+        if (lane == 0) {
+            if (live0) n2[lc0] = na;
+            if (live1) n2[lc1] = nb;
+        }
+        if (piv0)
+            for (int i = j + lane; i < m; i += 32) ca[i] = (i == j) ? alpha : 0.0;
+        if (piv1)
+            for (int i = j + lane; i < m; i += 32) cb[i] = (i == j) ? alpha : 0.0;
+    }
+}
+
+template <int KR, class ColP>
+__device__ __forceinline__ void qr_update_cols_warp1(ColP colp, int warp, int nc, int c0, int cw, int j, int m,
+                                                     double alpha, double tau, const double* __restrict__ v,
+                                                     const int* __restrict__ dn, double* __restrict__ n2) {
     const int nwarp = blockDim.x >> 5, lane = threadIdx.x & 31;
     for (int lc = warp; lc < nc; lc += nwarp) {
         const bool piv = c0 + lc == cw;
@@ -339,7 +408,10 @@ __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* 
         __syncthreads();
         // ---- trailing update of the remaining owned columns (16 threads per column)
         if (KR > 0)
-            qr_update_cols_warp<(KR > 0 ? KR : 1)>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
+            if constexpr (KR == 32)  // two columns per warp (243 registers); KR = 64: one
+                qr_update_cols_warp<32>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
+            else
+                qr_update_cols_warp1<(KR > 0 ? KR : 1)>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
         else
             qr_update_cols(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
         __syncthreads();

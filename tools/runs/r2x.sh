@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+T=r2x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1 || { tail -20 gpurun_out/${T}_build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "qrcp or compress" > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc $?"; tail -1 gpurun_out/${T}_pytest.log
+for C in c3g_2d_8x8 c2_1d_semiconductor; do
+timeout 1500 python bench.py --config $C --steps 2 --warmup 3 --skip-cpu > gpurun_out/${T}_bench_$C.log 2>&1; echo "bench $C rc $? $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/${T}_bench_$C.log | head -1)"
+done
