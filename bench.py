@@ -225,7 +225,9 @@ def run_acp(args, cfg):
     d2h = 8 * (n * n + n)
     e2e_ms = 0.0
     e2e_steps = max(1, min(args.steps, 3))
-    for _ in range(e2e_steps):
+    # one untimed pass first: the device input buffers are new allocations, so the PCG graphs
+    # (keyed by their pointers) are captured here rather than inside the timed passes
+    for it in range(e2e_steps + 1):
         with torch.cuda.stream(stream):
             flush.zero_()
         barrier()
@@ -244,7 +246,8 @@ def run_acp(args, cfg):
         D2, lam2 = ctx.dynamical_matrix(R, dev_in["rho"], dev_in["G"], U)   # D, lambda land in host memory
         e1.record(stream)
         barrier()
-        e2e_ms += e0.elapsed_time(e1)
+        if it > 0:
+            e2e_ms += e0.elapsed_time(e1)
     e2e_ms /= e2e_steps
     e2e_value = (solves / args.steps) / (e2e_ms / 1e3)
 
