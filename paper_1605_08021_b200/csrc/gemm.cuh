@@ -435,12 +435,12 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     for (int e = rank * 128 + tid; e < BM * TC_BN; e += CS * 128) {
         const int row = e % BM, col = e / BM;
         // all CS remote loads in flight together (one DSMEM latency), then summed in rank order
-        double part[8];
+        double part[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) part[q] = q < CS ? cluster.map_shared_rank(Cs, q)[row * LDC + col] : 0.0;
+        for (int q = 0; q < 16; ++q) part[q] = q < CS ? cluster.map_shared_rank(Cs, q)[row * LDC + col] : 0.0;
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s += part[q];
+        for (int q = 0; q < 16; ++q) s += part[q];
         const int gm = m0 + row, gn = n0 + col;
         if (gm < m && gn < n) C[(size_t)gn * ldc + gm] = alpha * s;
     }
@@ -448,16 +448,28 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     cluster.sync();
 }
 
+// K split of the cluster projection: CS <= 8 ranks of kchunk rows (~160 per rank).  ACP_K2_SHORTK=1
+// instead gives short K (<= 16 x 128) one memory latency per rank (kchunk <= TC_ST * TC_BK, up
+// to 16 ranks): measured slower on configs[1] (K2 17.5 vs 13.3 us; non-portable cluster sizes).
+inline void tn_split(int K, int& CS, int& kchunk) {
+    static const bool shortk = getenv("ACP_K2_SHORTK") != nullptr;
+    const int ring = TC_ST * TC_BK;
+    if (shortk && K <= 16 * ring) {
+        CS = std::max(1, cdiv(K, ring));
+    } else {
+        CS = std::min(8, std::max(1, cdiv(K, 160)));
+    }
+    kchunk = cdiv(cdiv(K, CS), TC_BK) * TC_BK;
+    CS = cdiv(K, kchunk);
+}
+
 // Host launcher: returns false if the operand layout does not allow 16-byte cp.async.
 template <class Hook>
 bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, const double* A, int lda, const double* B,
                        int ldb, double* C, int ldc, Hook hook) {
     if ((K & 1) || (lda & 1) || (ldb & 1) || (((uintptr_t)A | (uintptr_t)B) & 15)) return false;
-    int CS = cdiv(K, 160);
-    if (CS > 8) CS = 8;
-    if (CS < 1) CS = 1;
-    int kchunk = cdiv(cdiv(K, CS), TC_BK) * TC_BK;
-    CS = cdiv(K, kchunk);
+    int CS, kchunk;
+    tn_split(K, CS, kchunk);
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(128, 1, 1);
     cfg.stream = ctx->stream;
@@ -477,6 +489,7 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
         if (!attr32) {
             ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)tn_cluster_smem<32>()));
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             attr32 = true;
         }
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
@@ -487,6 +500,7 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
         if (!attr64) {
             ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<64, Hook>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)tn_cluster_smem<64>()));
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<64, Hook>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             attr64 = true;
         }
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<64, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));

@@ -335,12 +335,12 @@ __global__ void __launch_bounds__(PU_T, 2) k_proj_update(int K, int m, int n, co
     //    flight together, as k_tn_cluster) into its Cf; rank 0 runs the CG scalar hook
     for (int e = rank * PU_T + tid; e < PU_BM * PU_BN; e += CS * PU_T) {
         const int row = e / PU_BN, col = e % PU_BN;
-        double part[8];
+        double part[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) part[q] = q < CS ? cluster.map_shared_rank(Cs, q)[row * LDC + col] : 0.0;
+        for (int q = 0; q < 16; ++q) part[q] = q < CS ? cluster.map_shared_rank(Cs, q)[row * LDC + col] : 0.0;
         double sum = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) sum += part[q];
+        for (int q = 0; q < 16; ++q) sum += part[q];
         Cf[row * LDC + col] = alpha * sum;
     }
     if (rank == 0 && tid < PU_BN && n0 + tid < n) hook(n0 + tid);
@@ -409,15 +409,15 @@ static bool launch_proj_update(acp_context* ctx, int K, int m, int n, double alp
     // serial cluster barriers per tile and 8x fewer CTAs for the update)
     if (m > PU_BM || (K & 1) || (((uintptr_t)Psi | (uintptr_t)Y) & 15) || !getenv("ACP_PCG_FUSED")) return false;
     // the same K split as launch_tn_cluster (identical partial sums)
-    int CS = std::min(8, std::max(1, cdiv(K, 160)));
-    int kchunk = cdiv(cdiv(K, CS), TC_BK) * TC_BK;
+    int CS, kchunk;
+    tn_split(K, CS, kchunk);
     if (kchunk > PU_KMAX) return false;
-    CS = cdiv(K, kchunk);
     const size_t smem = pu_smem(kchunk);
     static bool attr = false;
     if (!attr) {
         ACP_CUDA(cudaFuncSetAttribute(k_proj_update<Hook, Ep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)pu_smem(PU_KMAX)));
+        ACP_CUDA(cudaFuncSetAttribute(k_proj_update<Hook, Ep>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
