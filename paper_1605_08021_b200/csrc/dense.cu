@@ -59,7 +59,7 @@ __device__ __forceinline__ void block_argmax_abs(double val, int idx, double* sv
 // B are independent).  ~4 block barriers per panel instead of ~3 per column.
 constexpr int LU_NB = 32;
 __global__ void __launch_bounds__(1024) k_lu_solve(double* __restrict__ Ag, int n, double* __restrict__ Bg, int nrhs,
-                                                   int use_smem, int* __restrict__ status) {
+                                                   int use_smem, int* __restrict__ status, int accumulate) {
     // use_smem: 0 = both in global memory, 1 = A in shared memory, 2 = A and B in shared memory
     extern __shared__ double lsm[];
     __shared__ int s_piv[LU_NB];
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(1024) k_lu_solve(double* __restrict__ Ag, int 
     __syncthreads();
     if (use_smem >= 2)
         for (long long e = tid; e < (long long)n * nrhs; e += nt) Bg[e] = B[e];
-    if (tid == 0) *status = 0;
+    if (tid == 0 && !accumulate) *status = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -557,7 +557,8 @@ void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
 }
 
 void lu_solve(acp_context* ctx, double* A, int n, double* B, int nrhs) {
-    int* st = ctx->wsi("lu_status", 1);
+    // deferred mode (acp_dyson): the status accumulates in the device statistics
+    int* st = ctx->defer ? reinterpret_cast<int*>(ctx->defer_stats + 6) : ctx->wsi("lu_status", 1);
     const size_t abytes = (size_t)n * n * sizeof(double), bbytes = (size_t)n * nrhs * sizeof(double);
     const int use_smem = abytes + bbytes <= 224 * 1024 ? 2 : abytes <= 224 * 1024 ? 1 : 0;
     const size_t bytes = use_smem == 2 ? abytes + bbytes : use_smem == 1 ? abytes : 0;
@@ -566,8 +567,9 @@ void lu_solve(acp_context* ctx, double* A, int n, double* B, int nrhs) {
         ACP_CUDA(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
         attr = true;
     }
-    k_lu_solve<<<1, 1024, bytes, ctx->stream>>>(A, n, B, nrhs, use_smem, st);
+    k_lu_solve<<<1, 1024, bytes, ctx->stream>>>(A, n, B, nrhs, use_smem, st, ctx->defer);
     launched(ctx);
+    if (ctx->defer) return;
     int* hp = static_cast<int*>(ctx->pinned);
     ACP_CUDA(cudaMemcpyAsync(hp, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ACP_CUDA(cudaStreamSynchronize(ctx->stream));
