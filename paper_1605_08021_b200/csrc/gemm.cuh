@@ -182,7 +182,7 @@ constexpr int GB_BM = 64, GB_BN = 64, GB_BK = 32, GB_ST = 3, GB_LDA = GB_BM + 4,
 
 constexpr size_t nn_big_smem() { return (size_t)GB_ST * (GB_BK * GB_LDA + GB_BN * GB_LDB) * sizeof(double); }
 
-template <class Ep, bool PF = false>
+template <class Ep, int EPI = 0>
 __device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* __restrict__ A, int lda,
                                             const double* __restrict__ B, int ldb, int m0, int n0, const Ep& ep) {
     extern __shared__ __align__(16) double gsm[];
@@ -225,8 +225,9 @@ __device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* _
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    // PF: the first epilogue half's operands (independent of the product) are loaded before the
-    // K loop; measured no faster for the PCG update (ACP_K3_PF), so off by default
+    // Epilogue order EPI: 0 = each half loaded then stored after the K loop (one half live),
+    // 1 = both halves loaded after the K loop, 2 = the first half loaded before the K loop (its
+    // operands do not depend on the product).  Selected per call site (ACP_K3_EPI for the update).
     typename Ep::Regs regs0[2][2][2];
     auto load_half0 = [&]() {
 #pragma unroll
@@ -240,7 +241,7 @@ __device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* _
                     if (row < M && col < n) ep.load(row, col, regs0[i][j][e]);
                 }
     };
-    if constexpr (PF) load_half0();
+    if constexpr (EPI == 2) load_half0();
 #pragma unroll
     for (int st = 0; st < GB_ST - 1; ++st) {
         if (st < nk) load_stage(st, st * GB_BK);
@@ -269,7 +270,35 @@ __device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* _
         __syncthreads();
     }
     cp_async_wait<0>();
-    if constexpr (!PF) load_half0();
+    if constexpr (EPI == 0) {
+        // one epilogue half live at a time (load, then store) keeps the registers in budget
+#pragma unroll
+        for (int ih = 0; ih < 4; ih += 2) {
+            typename Ep::Regs regs[2][2][2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int row = m0 + wm * 32 + (ih + i) * 8 + g;
+                        const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
+                        if (row < M && col < n) ep.load(row, col, regs[i][j][e]);
+                    }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int row = m0 + wm * 32 + (ih + i) * 8 + g;
+                        const int col = n0 + wn * 16 + j * 8 + 2 * t + e;
+                        if (row < M && col < n) ep.store(row, col, acc[ih + i][j][e], regs[i][j][e]);
+                    }
+        }
+        return;
+    }
+    if constexpr (EPI == 1) load_half0();
     typename Ep::Regs regs1[2][2][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)

@@ -177,8 +177,14 @@ struct EpBeta {
     }
 };
 
+// Resident CTAs per SM requested from ptxas: enough that configs[1]'s 1160 tiles fit one wave
+// where the epilogue registers allow it (EpBeta keeps 2 operands per element, EpAlpha 4).
+template <class Ep> struct K3Occ { static constexpr int v = 4; };
+template <> struct K3Occ<EpBeta> { static constexpr int v = 8; };
+template <> struct K3Occ<EpAlpha> { static constexpr int v = 6; };
+
 template <class Ep>
-__global__ void __launch_bounds__(128, 4) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
+__global__ void __launch_bounds__(128, K3Occ<Ep>::v) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
                                                        const double* __restrict__ B, int ldb, Ep ep) {
     pdl_wait();
     pdl_trigger();
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(128, 4) k_pcg_update(int M, int K, int n, cons
 }
 
 // Large-K variant (N_occ >= 64): 64 x 64 tiles, multistage cp.async, 256 threads.
-template <class Ep, bool PF = true>
+template <class Ep, int EPI = 0>
 __global__ void __launch_bounds__(256, 2) k_pcg_update_big(int M, int K, int n, const double* __restrict__ A, int lda,
                                                         const double* __restrict__ B, int ldb, Ep ep) {
     pdl_wait();
@@ -210,7 +216,7 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update_big(int M, int K, int n, 
     }
     __syncthreads();
     if (!any) return;
-    nn_tile_big<Ep, PF>(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, n0, ep);
+    nn_tile_big<Ep, EPI>(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, n0, ep);
 }
 
 template <class Ep>
@@ -224,16 +230,15 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
     cfg.attrs = at;
     cfg.numAttrs = ctx->pdl ? 1 : 0;
     if (K >= 64) {
-        // ACP_K3_PF=1: first epilogue half prefetched before the K loop (measured no faster on
-        // configs[2] / [3]: the 2-stage K loop is short; the default loads it after the loop)
-        static const bool nopf = getenv("ACP_K3_PF") == nullptr;
-        auto kern = nopf ? k_pcg_update_big<Ep, false> : k_pcg_update_big<Ep, true>;
+        // epilogue order (nn_tile_big), same-box A/B: configs[3] 836.8 / 824.9 / 828.2 ms and
+        // configs[2] 252.0 / 251.0 / 252.8 ms per step for EPI 0 / 1 / 2 -> 1 (ACP_K3_EPI overrides)
+        static const int epi = getenv("ACP_K3_EPI") ? atoi(getenv("ACP_K3_EPI")) : 1;
+        auto kern = epi == 1 ? k_pcg_update_big<Ep, 1> : epi == 2 ? k_pcg_update_big<Ep, 2> : k_pcg_update_big<Ep, 0>;
         static bool attr = false;
         if (!attr) {
-            ACP_CUDA(cudaFuncSetAttribute(k_pcg_update_big<Ep, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)nn_big_smem()));
-            ACP_CUDA(cudaFuncSetAttribute(k_pcg_update_big<Ep, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)nn_big_smem()));
+            for (const void* f : {(const void*)k_pcg_update_big<Ep, 0>, (const void*)k_pcg_update_big<Ep, 1>,
+                                  (const void*)k_pcg_update_big<Ep, 2>})
+                ACP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nn_big_smem()));
             attr = true;
         }
         cfg.gridDim = dim3(cdiv(M, GB_BM), cdiv(n, GB_BN), 1);
