@@ -497,6 +497,32 @@ struct EpW {
     }
 };
 
+// Node-parallel W (small problems): T_c = 2f X_c (.) (Psi B_c) for all nodes at once (one CTA per
+// tile and node), then W = sum_c T_c in node order -- the same additions in the same order as the
+// node-sequential epilogue (0 + t_0 + t_1 + ...), so W is bitwise identical.
+struct EpWTerm {
+    const double* X;
+    double* T;  // [c][col][row], ld Ng, cnt columns per node
+    int Ng, nmu_p, cnt;
+    double pref;
+    struct Regs {
+        double x;
+    };
+    __device__ __forceinline__ void load(int r, int col, Regs& g) const {
+        g.x = X[(size_t)(blockIdx.z * nmu_p + col) * Ng + r];
+    }
+    __device__ __forceinline__ void store(int r, int col, double acc, const Regs& g) const {
+        T[((size_t)blockIdx.z * cnt + col) * Ng + r] = pref * (g.x * acc);
+    }
+};
+__global__ void k_w_sum(size_t per, int n_cheb, const double* __restrict__ T, double* __restrict__ W) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= per) return;
+    double w = 0.0;
+    for (int c = 0; c < n_cheb; ++c) w = w + T[(size_t)c * per + i];
+    W[i] = w;
+}
+
 template <class Ep>
 __global__ void __launch_bounds__(128) k_nn_ep(int M, int K, int n, const double* __restrict__ A, int lda,
                                                const double* __restrict__ B, int ldb, Ep ep) {
@@ -507,6 +533,11 @@ __global__ void __launch_bounds__(256, 2) k_nn_ep_big(int M, int K, int n, const
                                                       const double* __restrict__ B, int ldb, Ep ep) {
     nn_tile_big(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, blockIdx.y * GB_BN, ep);
 }
+__global__ void __launch_bounds__(128) k_w_terms(int M, int K, int n, const double* __restrict__ A,
+                                                const double* __restrict__ B, EpWTerm ep) {
+    nn_tile_pf(M, K, n, A, M, B + (size_t)blockIdx.z * n * K, K, blockIdx.x * NP_BM, blockIdx.y * NP_BN, ep);
+}
+
 // All nodes in ONE launch: each CTA owns a W tile and runs the N_c tile GEMMs in node order,
 // accumulating into its W tile (the same thread owns the same element in every pass).
 template <bool BIG>
@@ -937,6 +968,17 @@ void apply_chi0(acp_context* ctx, const double* Psi, const double* eps, const do
             ep.first = c == 0;
             launch_nn_ep(ctx, Ng, n_occ, cnt, Psi, Ng, B + (size_t)c * cnt * n_occ, n_occ, ep);
         }
+    } else if (n_occ < 64 && (size_t)n_cheb * cnt * Ng * sizeof(double) <= ((size_t)256 << 20) &&
+               !getenv("ACP_W_SEQ")) {
+        // small problems (configs[1]): all nodes in parallel, then the ordered sum
+        double* T = ctx->wsd("chi_Wterms", (size_t)n_cheb * cnt * Ng);
+        EpWTerm et{X, T, Ng, nmu_p, cnt, 2.0 * ctx->sys.occ};
+        k_w_terms<<<dim3(cdiv(Ng, NP_BM), cdiv(cnt, NP_BN), n_cheb), 128, 0, ctx->stream>>>(Ng, n_occ, cnt, Psi, B,
+                                                                                           et);
+        launched(ctx);
+        const size_t per = (size_t)cnt * Ng;
+        k_w_sum<<<cdiv((long long)per, 256), 256, 0, ctx->stream>>>(per, n_cheb, T, W + (size_t)mu_begin * Ng);
+        launched(ctx);
     } else if (n_occ >= 64) {
         static bool attr = false;
         if (!attr) {

@@ -497,6 +497,22 @@ def test_apply_chi0_two_stream_groups_equal_one(sysx, monkeypatch):
     assert torch.equal(W1, W2) and i1["total_iter"] == i2["total_iter"]
 
 
+def test_apply_chi0_node_parallel_W_equals_sequential(sysx, monkeypatch):
+    """W built node-parallel + ordered sum (default for small problems) and node-sequential in one
+    kernel (ACP_W_SEQ=1): the same additions in the same order, bitwise-identical W."""
+    from paper_1605_08021_b200 import Context
+    s = sysx
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    St, Xt = T(S_o, torch.int32), T(Xi_o.T)
+    W1, _ = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    monkeypatch.setenv("ACP_W_SEQ", "1")
+    ctx = Context.from_config(s.cfg)
+    W2, _ = ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    ctx.close()
+    assert torch.equal(W1, W2)
+
+
 def test_apply_chi0_empty_shard(sysx):
     """An empty mu-range (a rank with no columns) is a no-op that leaves W untouched."""
     s = sysx
