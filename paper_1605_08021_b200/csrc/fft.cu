@@ -533,6 +533,7 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
                   : ctx->fept <= 2 ? k_fft1d<2, true, IO> : ctx->fept <= 4 ? k_fft1d<4, true, IO>
                   : k_fft1d<8, true, IO>;
         // compiled-length kernels for the configs' grids (hot path only; ACP_FFT_GENERIC=1 off)
+        if (IO == IO_OP && ctx->fct && nokeep && G.n0 == 1280 && ctx->fept == 8) kern = k_fft1d<8, false, IO, 1280>;
         if (IO == IO_OP && ctx->fct && !nokeep) {
             if (G.n0 == 1280 && T <= 160 && ctx->fept == 8) kern = k_fft1d<8, true, IO, 1280>;
             else if (G.n0 == 960 && T <= 160 && ctx->fept == 8) kern = k_fft1d<8, true, IO, 960>;
