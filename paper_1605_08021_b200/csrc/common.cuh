@@ -199,6 +199,15 @@ cudaGraphExec_t graph_cached(acp_context* ctx, const std::string& key, F&& body)
     ctx->launches = before;
     return e;
 }
+// Bound the graph cache (each new shape / pointer set adds entries): called where no cached
+// executable is held by the caller; waits for the device before destroying.
+inline void graph_cache_trim(acp_context* ctx, size_t max_entries = 128) {
+    if (ctx->graphs.size() <= max_entries) return;
+    cudaDeviceSynchronize();
+    for (auto& kv : ctx->graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    ctx->graphs.clear();
+}
 inline void graph_launch(acp_context* ctx, const std::string& key, cudaGraphExec_t e) {
     ACP_CUDA(cudaGraphLaunch(e, ctx->stream));
     ctx->launches += ctx->graphs[key].launches;

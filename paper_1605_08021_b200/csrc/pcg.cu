@@ -805,6 +805,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     const int Ng = ctx->Ng;
     const int n = n_c * nmu_p;
     if (n == 0) return;
+    graph_cache_trim(ctx);
     double* R = ctx->wsd("pcg_R", (size_t)Ng * n);
     double* P = ctx->wsd("pcg_P", (size_t)Ng * n);
     double* Y = ctx->wsd("pcg_Y", (size_t)Ng * n);
