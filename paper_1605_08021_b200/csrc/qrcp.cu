@@ -237,6 +237,67 @@ __device__ __forceinline__ void qr_update_cols_warp1(ColP colp, int warp, int nc
     }
 }
 
+// Long columns (m > 2048, configs[4]: m = 4096): one warp per column in chunks of 32 KR rows --
+// pass 1 accumulates v.c chunk by chunk (KR loads in flight per lane), pass 2 re-reads each chunk,
+// updates, stores and accumulates the new norm.  Two reads + one write per element, like the
+// 16-lane version, but with enough loads in flight to run at HBM bandwidth.
+template <int KR, class ColP>
+__device__ __forceinline__ void qr_update_cols_chunked(ColP colp, int warp, int nc, int c0, int cw, int j, int m,
+                                                       double alpha, double tau, const double* __restrict__ v,
+                                                       const int* __restrict__ dn, double* __restrict__ n2) {
+    const int nwarp = blockDim.x >> 5, lane = threadIdx.x & 31;
+    const int r_begin = j & ~31;
+    for (int lc = warp; lc < nc; lc += nwarp) {
+        const bool piv = c0 + lc == cw;
+        const bool live = !piv && !dn[lc];
+        double* c = colp(lc);
+        if (live) {
+            double d = 0.0;
+            for (int r0 = r_begin; r0 < m; r0 += 32 * KR) {
+                double y[KR];
+#pragma unroll
+                for (int k = 0; k < KR; ++k) {
+                    const int i = r0 + lane + 32 * k;
+                    y[k] = (i >= j && i < m) ? c[i] : 0.0;
+                }
+                asm volatile("" ::: "memory");  // issue all KR loads before their first use
+#pragma unroll
+                for (int k = 0; k < KR; ++k) {
+                    const int i = r0 + lane + 32 * k;
+                    if (i >= j && i < m) d += v[i] * y[k];
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            const double f = tau * d;
+            double nn = 0.0;
+            for (int r0 = r_begin; r0 < m; r0 += 32 * KR) {
+                double y[KR];
+#pragma unroll
+                for (int k = 0; k < KR; ++k) {
+                    const int i = r0 + lane + 32 * k;
+                    y[k] = (i >= j && i < m) ? c[i] : 0.0;
+                }
+                asm volatile("" ::: "memory");  // issue all KR loads before their first use
+#pragma unroll
+                for (int k = 0; k < KR; ++k) {
+                    const int i = r0 + lane + 32 * k;
+                    if (i >= j && i < m) {
+                        const double yy = y[k] - f * v[i];
+                        c[i] = yy;
+                        if (i > j) nn += yy * yy;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+            if (lane == 0) n2[lc] = nn;
+        } else if (piv) {
+            for (int i = j + lane; i < m; i += 32) c[i] = (i == j) ? alpha : 0.0;
+        }
+    }
+}
+
 template <bool SMEM, int KR>
 __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* __restrict__ Ag, int kmax, double eps,
                                                          int fixed, QrSlot* __restrict__ slots,
@@ -407,11 +468,12 @@ __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* 
         }
         __syncthreads();
         // ---- trailing update of the remaining owned columns (16 threads per column)
-        if (KR > 0)
-            if constexpr (KR == 32)  // two columns per warp (243 registers); KR = 64: one
-                qr_update_cols_warp<32>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
-            else
-                qr_update_cols_warp1<(KR > 0 ? KR : 1)>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
+        if constexpr (KR == 32)  // two columns per warp (243 registers)
+            qr_update_cols_warp<32>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
+        else if constexpr (KR == 64)
+            qr_update_cols_warp1<64>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
+        else if constexpr (KR == 1)  // m > 2048: warp per column, 1024-row chunks
+            qr_update_cols_chunked<32>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
         else
             qr_update_cols(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
         __syncthreads();
@@ -1184,8 +1246,10 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
         void* args[] = {(void*)&m, (void*)&Ng, (void*)&A, (void*)&kmax, (void*)&id_eps, (void*)&n_fixed,
                         (void*)&slots, (void*)&cand, (void*)&perm, (void*)&rdiag, (void*)&d_nmu};
         // global-memory columns: one warp per column, rows in registers, when m <= 2048
-        const int kr = (use_smem || getenv("ACP_QRCP_GRID16")) ? 0 : m <= 1024 ? 32 : m <= 2048 ? 64 : 0;
+        int kr = (use_smem || getenv("ACP_QRCP_GRID16")) ? 0 : m <= 1024 ? 32 : m <= 2048 ? 64 : 1;
+        if (!use_smem && getenv("ACP_QRCP_CHUNKED")) kr = 1;  // test knob: the m > 2048 update
         const void* fn = use_smem ? (const void*)k_qrcp_persistent<true, 0>
+                         : kr == 1 ? (const void*)k_qrcp_persistent<false, 1>
                          : kr == 32 ? (const void*)k_qrcp_persistent<false, 32>
                          : kr == 64 ? (const void*)k_qrcp_persistent<false, 64>
                                     : (const void*)k_qrcp_persistent<false, 0>;

@@ -304,7 +304,8 @@ def test_compress_pivots_bit_exact(sysx):
 
 
 @pytest.mark.parametrize("knob", ["ACP_QRCP_GRID", "ACP_QRCP_SMEM", "ACP_QRCP_GRID+ACP_QRCP_NOSMEM",
-                                  "ACP_QRCP_GRID+ACP_QRCP_NOSMEM+ACP_QRCP_GRID16"])
+                                  "ACP_QRCP_GRID+ACP_QRCP_NOSMEM+ACP_QRCP_GRID16",
+                                  "ACP_QRCP_GRID+ACP_QRCP_NOSMEM+ACP_QRCP_CHUNKED"])
 def test_compress_alternative_qrcp_kernels_agree(sysx, monkeypatch, knob):
     """The QRCP kernels -- register-resident cluster (default for small problems), shared-memory
     cluster (ACP_QRCP_SMEM) and grid-wide persistent (ACP_QRCP_GRID; columns in shared memory, or
