@@ -298,6 +298,88 @@ __device__ __forceinline__ void qr_update_cols_chunked(ColP colp, int warp, int 
     }
 }
 
+// Two columns per warp variant of the chunked update (independent load streams interleave).
+template <int KR, class ColP>
+__device__ __forceinline__ void qr_update_cols_chunked2(ColP colp, int warp, int nc, int c0, int cw, int j, int m,
+                                                        double alpha, double tau, const double* __restrict__ v,
+                                                        const int* __restrict__ dn, double* __restrict__ n2) {
+    const int nwarp = blockDim.x >> 5, lane = threadIdx.x & 31;
+    const int r_begin = j & ~31;
+    for (int lc0 = warp; lc0 < nc; lc0 += 2 * nwarp) {
+        const int lc1 = lc0 + nwarp;
+        const bool has1 = lc1 < nc;
+        const bool piv0 = c0 + lc0 == cw, piv1 = has1 && c0 + lc1 == cw;
+        const bool live0 = !piv0 && !dn[lc0];
+        const bool live1 = has1 && !piv1 && !dn[lc1];
+        double* ca = colp(lc0);
+        double* cb = colp(has1 ? lc1 : lc0);
+        double da = 0.0, db = 0.0;
+        for (int r0 = r_begin; r0 < m; r0 += 32 * KR) {
+            double ya[KR], yb[KR];
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int i = r0 + lane + 32 * k;
+                const bool in = i >= j && i < m;
+                ya[k] = (live0 && in) ? ca[i] : 0.0;
+                yb[k] = (live1 && in) ? cb[i] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int i = r0 + lane + 32 * k;
+                if (i >= j && i < m) {
+                    const double vi = v[i];
+                    da += vi * ya[k];
+                    db += vi * yb[k];
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            da += __shfl_xor_sync(0xffffffffu, da, o);
+            db += __shfl_xor_sync(0xffffffffu, db, o);
+        }
+        const double fa = tau * da, fb = tau * db;
+        double na = 0.0, nb = 0.0;
+        for (int r0 = r_begin; r0 < m; r0 += 32 * KR) {
+            double ya[KR], yb[KR];
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int i = r0 + lane + 32 * k;
+                const bool in = i >= j && i < m;
+                ya[k] = (live0 && in) ? ca[i] : 0.0;
+                yb[k] = (live1 && in) ? cb[i] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int i = r0 + lane + 32 * k;
+                if (i >= j && i < m) {
+                    const double vi = v[i];
+                    const double ua = ya[k] - fa * vi, ub = yb[k] - fb * vi;
+                    if (live0) ca[i] = ua;
+                    if (live1) cb[i] = ub;
+                    if (i > j) {
+                        na += ua * ua;
+                        nb += ub * ub;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            na += __shfl_xor_sync(0xffffffffu, na, o);
+            nb += __shfl_xor_sync(0xffffffffu, nb, o);
+        }
+        if (lane == 0) {
+            if (live0) n2[lc0] = na;
+            if (live1) n2[lc1] = nb;
+        }
+        if (piv0)
+            for (int i = j + lane; i < m; i += 32) ca[i] = (i == j) ? alpha : 0.0;
+        if (piv1)
+            for (int i = j + lane; i < m; i += 32) cb[i] = (i == j) ? alpha : 0.0;
+    }
+}
+
 template <bool SMEM, int KR>
 __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* __restrict__ Ag, int kmax, double eps,
                                                          int fixed, QrSlot* __restrict__ slots,
@@ -474,6 +556,8 @@ __global__ void __launch_bounds__(256) k_qrcp_persistent(int m, int Ng, double* 
             qr_update_cols_warp1<64>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
         else if constexpr (KR == 1)  // m > 2048: warp per column, 1024-row chunks
             qr_update_cols_chunked<32>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
+        else if constexpr (KR == 2)  // m > 2048: two columns per warp, 512-row chunks
+            qr_update_cols_chunked2<16>(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
         else
             qr_update_cols(colp, warp, nc, c0, cw, j, m, alpha, tau, v, dn, n2);
         __syncthreads();
@@ -1247,9 +1331,11 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
                         (void*)&slots, (void*)&cand, (void*)&perm, (void*)&rdiag, (void*)&d_nmu};
         // global-memory columns: one warp per column, rows in registers, when m <= 2048
         int kr = (use_smem || getenv("ACP_QRCP_GRID16")) ? 0 : m <= 1024 ? 32 : m <= 2048 ? 64 : 1;
-        if (!use_smem && getenv("ACP_QRCP_CHUNKED")) kr = 1;  // test knob: the m > 2048 update
+        if (kr == 1 && !getenv("ACP_QRCP_CHUNK1")) kr = 2;      // two columns per warp
+        if (!use_smem && getenv("ACP_QRCP_CHUNKED")) kr = getenv("ACP_QRCP_CHUNK1") ? 1 : 2;  // test knob
         const void* fn = use_smem ? (const void*)k_qrcp_persistent<true, 0>
                          : kr == 1 ? (const void*)k_qrcp_persistent<false, 1>
+                         : kr == 2 ? (const void*)k_qrcp_persistent<false, 2>
                          : kr == 32 ? (const void*)k_qrcp_persistent<false, 32>
                          : kr == 64 ? (const void*)k_qrcp_persistent<false, 64>
                                     : (const void*)k_qrcp_persistent<false, 0>;
