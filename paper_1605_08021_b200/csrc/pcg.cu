@@ -640,11 +640,12 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
     // `chunk` CG iterations + k_count_active, which sets the loop condition (columns still active
     // and fewer than max_iter iterations done) -- no host round trip until every column has
     // converged.  Cached per shapes/pointers; the chunk counter is reset before each launch.
-    const int chunk = 4;
+    static const int chunk_env = getenv("ACP_PCG_CHUNK") ? atoi(getenv("ACP_PCG_CHUNK")) : 0;
+    const int chunk = chunk_env > 0 ? chunk_env : 4;  // CG iterations per while-node trip
     const int max_chunks = (max_iter + chunk - 1) / chunk;
     int* d_chunks = d_nact + 1;
     char key[512];
-    snprintf(key, sizeof(key), "pcgw:%d:%d:%d:%d:%d:%d:%.17g:%.17g:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p", Ng, n,
+    snprintf(key, sizeof(key), "pcgw%d:%d:%d:%d:%d:%d:%d:%.17g:%.17g:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p:%p", chunk, Ng, n,
              n_occ, nmu_p, nvalid, max_chunks, tol2, tau, (void*)Psi, (void*)V, (void*)R, (void*)P, (void*)Y,
              (void*)X, (void*)C, (void*)shift, (void*)dots, (void*)s.rz, (void*)s.active, (void*)d_nact);
     // ACP_PCG_HOSTLOOP=1: the same body as a plain graph replayed from the host (ncu cannot
