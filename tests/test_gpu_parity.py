@@ -337,6 +337,20 @@ def test_apply_chi0_matches_direct_solves(sysx):
     assert rel(W_g.cpu().numpy().T, W_o) < 1e-9
 
 
+@pytest.mark.parametrize("n_cheb", [1, 3, 5])
+def test_apply_chi0_node_counts(n_cheb):
+    """N_c = 1, 3, 5 (one node group, uneven node groups over the streams, more groups than the
+    default) against the oracle's direct compressed solves."""
+    s = system("tiny4")
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    W_o = oacp.compressed_W(s.m, s.H, s.gs.Psi, s.gs.eps[: s.cfg.n_occ], S_o, Xi_o, n_cheb)
+    W_g, info = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, T(S_o, torch.int32), T(Xi_o.T), n_cheb,
+                                 cg_tol=s.cfg.cg_tol)
+    assert info["n_solved"] == n_cheb * len(S_o)
+    assert rel(W_g.cpu().numpy().T, W_o) < 1e-9
+
+
 def test_apply_chi0_sharding_is_bitwise(sysx):
     """RHS sharding across GPUs (even shard sizes) reproduces the unsharded W bit for bit."""
     s = sysx
