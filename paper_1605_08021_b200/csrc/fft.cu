@@ -129,8 +129,8 @@ __device__ __forceinline__ double sym_value(const FftGeom& G, int sym, double ta
 // prefetches the potential before the second FFT, so no global load sits on the critical path
 // after the initial one.
 // NCT != 0: the FFT length is the compile-time constant NCT (fft_ct), else the runtime plan.
-template <int EPT, bool KEEP, int IO, int NCT = 0>
-__global__ void __launch_bounds__(KEEP ? 160 : 1024, KEEP ? 4 : 1) k_fft1d(FftGeom G, const double2* __restrict__ twg,
+template <int EPT, bool KEEP, int IO, int NCT = 0, int NKT = 1024, int NKB = 1>
+__global__ void __launch_bounds__(KEEP ? 160 : NKT, KEEP ? 4 : NKB) k_fft1d(FftGeom G, const double2* __restrict__ twg,
                                                              IoArgs io) {
     extern __shared__ __align__(16) double2 sm1[];
     __shared__ double red[132];
@@ -538,7 +538,10 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
             if (G.n0 == 1280 && T <= 160 && ctx->fept == 8) kern = k_fft1d<8, true, IO, 1280>;
             else if (G.n0 == 960 && T <= 160 && ctx->fept == 8) kern = k_fft1d<8, true, IO, 960>;
             else if (G.n0 == 256 && T <= 160 && ctx->fept == 4) kern = k_fft1d<4, true, IO, 256>;
-            else if (G.n0 == 5120 && T > 160 && ctx->fept == 8) kern = k_fft1d<8, false, IO, 5120>;
+            else if (G.n0 == 5120 && T > 160 && ctx->fept == 8)
+                // 2 CTAs/SM (<= 48 registers): K1 400 vs 474 us, configs[2] 241 vs 251 ms/step
+                kern = (T == 640 && !getenv("ACP_FFT_1CTA")) ? k_fft1d<8, false, IO, 5120, 640, 2>
+                                                             : k_fft1d<8, false, IO, 5120>;
         }
         set_smem_attr((const void*)kern, ctx->fsmem, false);
         cudaLaunchConfig_t cfg = {};
