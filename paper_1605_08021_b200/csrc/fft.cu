@@ -609,8 +609,8 @@ __device__ __forceinline__ bool f2_pair_active(const FopArgs& a, int c0) {
 }
 
 // NCT != 0: square grid n0 = n1 = NCT with compile-time FFT indexing (fft_ct).
-template <int EPT, int NCT = 0>
-__global__ void __launch_bounds__(256, 3) k_f2_rows_fwd(FftGeom G, const double2* __restrict__ twg, FopArgs a,
+template <int EPT, int NCT = 0, int TB = 256, int MB = 3>
+__global__ void __launch_bounds__(TB, MB) k_f2_rows_fwd(FftGeom G, const double2* __restrict__ twg, FopArgs a,
                                                      double2* __restrict__ Z, int pair0) {
     extern __shared__ __align__(16) double2 f2s[];
     const int pr = pair0 + blockIdx.y, c0 = 2 * pr;
@@ -634,8 +634,8 @@ __global__ void __launch_bounds__(256, 3) k_f2_rows_fwd(FftGeom G, const double2
     }
 }
 
-template <int EPT, int NCT = 0>
-__global__ void __launch_bounds__(256, 3) k_f2_cols(FftGeom G, const double2* __restrict__ twg, FopArgs a,
+template <int EPT, int NCT = 0, int TB = 256, int MB = 3>
+__global__ void __launch_bounds__(TB, MB) k_f2_cols(FftGeom G, const double2* __restrict__ twg, FopArgs a,
                                                  double2* __restrict__ Z, int pair0) {
     extern __shared__ __align__(16) double2 f2s[];
     const int pr = pair0 + blockIdx.y, c0 = 2 * pr;
@@ -674,8 +674,8 @@ __global__ void __launch_bounds__(256, 3) k_f2_cols(FftGeom G, const double2* __
     }
 }
 
-template <int EPT, int NCT = 0>
-__global__ void __launch_bounds__(256, 3) k_f2_rows_inv(FftGeom G, const double2* __restrict__ twg, FopArgs a,
+template <int EPT, int NCT = 0, int TB = 256, int MB = 3>
+__global__ void __launch_bounds__(TB, MB) k_f2_rows_inv(FftGeom G, const double2* __restrict__ twg, FopArgs a,
                                                      const double2* __restrict__ Z, int pair0,
                                                      double* __restrict__ part) {
     extern __shared__ __align__(16) double2 f2s[];
@@ -779,13 +779,43 @@ static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
     // compiled-length kernels for the square configs grids (plans checked in fft_init)
     if (ctx->fct && n0 == n1 && er <= 8 && ec <= 8) {
         if (n0 == 192) {
-            ra = k_f2_rows_fwd<8, 192>;
-            cb = k_f2_cols<8, 192>;
-            rc = k_f2_rows_inv<8, 192>;
+            // 192 threads per CTA bounded to 6 CTAs/SM (<= 56 registers, no spill): configs[3]
+            // 762 / 787 / 825 ms/step at 6 / 5 / 3 CTAs/SM (ACP_F2_OCC=3|5|6|7 selects)
+            static const int occ = getenv("ACP_F2_OCC") ? atoi(getenv("ACP_F2_OCC")) : 6;
+            if (occ == 7) {
+                ra = k_f2_rows_fwd<8, 192, 192, 7>;
+                cb = k_f2_cols<8, 192, 192, 7>;
+                rc = k_f2_rows_inv<8, 192, 192, 7>;
+            } else if (occ == 6) {
+                ra = k_f2_rows_fwd<8, 192, 192, 6>;
+                cb = k_f2_cols<8, 192, 192, 6>;
+                rc = k_f2_rows_inv<8, 192, 192, 6>;
+            } else if (occ == 5) {
+                ra = k_f2_rows_fwd<8, 192, 192, 5>;
+                cb = k_f2_cols<8, 192, 192, 5>;
+                rc = k_f2_rows_inv<8, 192, 192, 5>;
+            } else {
+                ra = k_f2_rows_fwd<8, 192>;
+                cb = k_f2_cols<8, 192>;
+                rc = k_f2_rows_inv<8, 192>;
+            }
         } else if (n0 == 256) {
-            ra = k_f2_rows_fwd<8, 256>;
-            cb = k_f2_cols<8, 256>;
-            rc = k_f2_rows_inv<8, 256>;
+            // 256 threads bounded to 5 CTAs/SM (<= 48 registers, small spills): K1 4.06 / 4.51 / 5.31
+            // ms at 4096 columns for 5 / 4 / 3 CTAs/SM (ACP_F2_OCC256 selects)
+            static const int occ = getenv("ACP_F2_OCC256") ? atoi(getenv("ACP_F2_OCC256")) : 5;
+            if (occ == 5) {
+                ra = k_f2_rows_fwd<8, 256, 256, 5>;
+                cb = k_f2_cols<8, 256, 256, 5>;
+                rc = k_f2_rows_inv<8, 256, 256, 5>;
+            } else if (occ == 4) {
+                ra = k_f2_rows_fwd<8, 256, 256, 4>;
+                cb = k_f2_cols<8, 256, 256, 4>;
+                rc = k_f2_rows_inv<8, 256, 256, 4>;
+            } else {
+                ra = k_f2_rows_fwd<8, 256>;
+                cb = k_f2_cols<8, 256>;
+                rc = k_f2_rows_inv<8, 256>;
+            }
         }
     }
     set_smem_attr((const void*)ra, sr, false);

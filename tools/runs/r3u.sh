@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+T=r3u
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1 || { tail -20 gpurun_out/${T}_build.log; exit 1; }
+for O in 6 7 6 7; do
+ACP_F2_OCC=$O timeout 1500 python bench.py --config c3g_2d_8x8 --steps 2 --warmup 2 --skip-cpu > gpurun_out/${T}_bench.log 2>&1; echo "c3g occ=$O rc $? $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/${T}_bench.log | head -1)"
+done
+for O in 4 5 4 5; do
+echo "c4g occ256=$O $(ACP_F2_OCC256=$O timeout 300 python tools/k1_sweep.py c4g_2d_16x16 4096 2>&1 | tail -1)"
+done
