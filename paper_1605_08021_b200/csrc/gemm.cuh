@@ -180,14 +180,15 @@ __device__ __forceinline__ void nn_tile_pf(int M, int K, int n, const double* __
 // a GB_ST-stage cp.async ring of 32-deep K slices, then the two-phase epilogue.
 constexpr int GB_BM = 64, GB_BN = 64, GB_BK = 32, GB_ST = 3, GB_LDA = GB_BM + 4, GB_LDB = GB_BK + 4;
 
-constexpr size_t nn_big_smem() { return (size_t)GB_ST * (GB_BK * GB_LDA + GB_BN * GB_LDB) * sizeof(double); }
+template <int ST = GB_ST>
+constexpr size_t nn_big_smem() { return (size_t)ST * (GB_BK * GB_LDA + GB_BN * GB_LDB) * sizeof(double); }
 
-template <class Ep, int EPI = 0>
+template <class Ep, int EPI = 0, int ST = GB_ST>
 __device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* __restrict__ A, int lda,
                                             const double* __restrict__ B, int ldb, int m0, int n0, const Ep& ep) {
     extern __shared__ __align__(16) double gsm[];
-    double* As = gsm;                              // [GB_ST][GB_BK][GB_LDA]  (k-major: A(m, k) at [k][m])
-    double* Bs = gsm + GB_ST * GB_BK * GB_LDA;     // [GB_ST][GB_BN][GB_LDB]  (B(k, n) at [n][k])
+    double* As = gsm;                              // [ST][GB_BK][GB_LDA]  (k-major: A(m, k) at [k][m])
+    double* Bs = gsm + ST * GB_BK * GB_LDA;     // [ST][GB_BN][GB_LDB]  (B(k, n) at [n][k])
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp & 1, wn = warp >> 1;
@@ -243,18 +244,18 @@ __device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* _
     };
     if constexpr (EPI == 2) load_half0();
 #pragma unroll
-    for (int st = 0; st < GB_ST - 1; ++st) {
+    for (int st = 0; st < ST - 1; ++st) {
         if (st < nk) load_stage(st, st * GB_BK);
         cp_async_commit();
     }
     for (int it = 0; it < nk; ++it) {
-        const int nxt = it + GB_ST - 1;
-        if (nxt < nk) load_stage(nxt % GB_ST, nxt * GB_BK);
+        const int nxt = it + ST - 1;
+        if (nxt < nk) load_stage(nxt % ST, nxt * GB_BK);
         cp_async_commit();
-        cp_async_wait<GB_ST - 1>();
+        cp_async_wait<ST - 1>();
         __syncthreads();
-        const double* as = As + (it % GB_ST) * GB_BK * GB_LDA;
-        const double* bs = Bs + (it % GB_ST) * GB_BN * GB_LDB;
+        const double* as = As + (it % ST) * GB_BK * GB_LDA;
+        const double* bs = Bs + (it % ST) * GB_BN * GB_LDB;
 #pragma unroll
         for (int ks = 0; ks < GB_BK; ks += 4) {
             double af[4], bf[2];

@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(128, K3Occ<Ep>::v) k_pcg_update(int M, int K, 
 }
 
 // Large-K variant (N_occ >= 64): 64 x 64 tiles, multistage cp.async, 256 threads.
-template <class Ep, int EPI = 0>
-__global__ void __launch_bounds__(256, 2) k_pcg_update_big(int M, int K, int n, const double* __restrict__ A, int lda,
+template <class Ep, int EPI = 0, int ST = GB_ST, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_pcg_update_big(int M, int K, int n, const double* __restrict__ A, int lda,
                                                         const double* __restrict__ B, int ldb, Ep ep) {
     pdl_wait();
     pdl_trigger();
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update_big(int M, int K, int n, 
     }
     __syncthreads();
     if (!any) return;
-    nn_tile_big<Ep, EPI>(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, n0, ep);
+    nn_tile_big<Ep, EPI, ST>(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, n0, ep);
 }
 
 template <class Ep>
@@ -234,16 +234,23 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
         // configs[2] 252.0 / 251.0 / 252.8 ms per step for EPI 0 / 1 / 2 -> 1 (ACP_K3_EPI overrides)
         static const int epi = getenv("ACP_K3_EPI") ? atoi(getenv("ACP_K3_EPI")) : 1;
         auto kern = epi == 1 ? k_pcg_update_big<Ep, 1> : epi == 2 ? k_pcg_update_big<Ep, 2> : k_pcg_update_big<Ep, 0>;
+        size_t smem = nn_big_smem();
+        // ACP_K3_ST2=1: 2-stage ring (72 KB) and 3 CTAs/SM for short K (<= 128)
+        static const bool st2 = getenv("ACP_K3_ST2") != nullptr;
+        if (st2 && K <= 128 && epi == 1) {
+            kern = k_pcg_update_big<Ep, 1, 2, 3>;
+            smem = nn_big_smem<2>();
+        }
         static bool attr = false;
         if (!attr) {
             for (const void* f : {(const void*)k_pcg_update_big<Ep, 0>, (const void*)k_pcg_update_big<Ep, 1>,
-                                  (const void*)k_pcg_update_big<Ep, 2>})
+                                  (const void*)k_pcg_update_big<Ep, 2>, (const void*)k_pcg_update_big<Ep, 1, 2, 3>})
                 ACP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nn_big_smem()));
             attr = true;
         }
         cfg.gridDim = dim3(cdiv(M, GB_BM), cdiv(n, GB_BN), 1);
         cfg.blockDim = dim3(256, 1, 1);
-        cfg.dynamicSmemBytes = nn_big_smem();
+        cfg.dynamicSmemBytes = smem;
         ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, M, K, n, A, lda, B, ldb, ep));
     } else {
         cfg.gridDim = dim3(cdiv(M, NP_BM), cdiv(n, NP_BN), 1);
