@@ -349,12 +349,12 @@ struct NoHook {
     __device__ __forceinline__ bool tile_active(int, int) const { return true; }
 };
 
-template <int BM>
+template <int BM, int ST = TC_ST>
 constexpr size_t tn_cluster_smem() {
-    return (size_t)TC_ST * (BM + TC_BN) * (TC_BK + TC_PAD) * sizeof(double);
+    return (size_t)ST * (BM + TC_BN) * (TC_BK + TC_PAD) * sizeof(double);
 }
 
-template <int BM, class Hook>
+template <int BM, class Hook, int ST = TC_ST>
 __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const double* __restrict__ A, int lda,
                                                     const double* __restrict__ B, int ldb, int kchunk, double alpha,
                                                     double* __restrict__ C, int ldc, Hook hook) {
@@ -362,8 +362,8 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) double tsm[];
     constexpr int LD = TC_BK + TC_PAD;
-    double* As = tsm;                         // [TC_ST][BM][LD]
-    double* Bs = tsm + TC_ST * BM * LD;       // [TC_ST][BN][LD]
+    double* As = tsm;                         // [ST][BM][LD]
+    double* Bs = tsm + ST * BM * LD;       // [ST][BN][LD]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp & 1, wn = warp >> 1;
@@ -419,21 +419,21 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
 #pragma unroll
         for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    // TC_ST-stage ring: TC_ST - 1 stages in flight ahead of the one being multiplied (for the
+    // ST-stage ring: ST - 1 stages in flight ahead of the one being multiplied (for the
     // 1D configs the whole K chunk, <= 160 rows, is requested at once: one memory latency)
 #pragma unroll
-    for (int st = 0; st < TC_ST - 1; ++st) {
+    for (int st = 0; st < ST - 1; ++st) {
         if (st < nk) load_stage(st, kb + st * TC_BK);
         cp_async_commit();
     }
     for (int it = 0; it < nk; ++it) {
-        const int nxt = it + TC_ST - 1;
-        if (nxt < nk) load_stage(nxt % TC_ST, kb + nxt * TC_BK);
+        const int nxt = it + ST - 1;
+        if (nxt < nk) load_stage(nxt % ST, kb + nxt * TC_BK);
         cp_async_commit();
-        cp_async_wait<TC_ST - 1>();
+        cp_async_wait<ST - 1>();
         __syncthreads();
-        const double* as = As + (it % TC_ST) * BM * LD;
-        const double* bs = Bs + (it % TC_ST) * TC_BN * LD;
+        const double* as = As + (it % ST) * BM * LD;
+        const double* bs = Bs + (it % ST) * TC_BN * LD;
 #pragma unroll
         for (int ks = 0; ks < TC_BK; ks += 4) {
             double af[TI], bf[2];
@@ -512,7 +512,32 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = ctx->pdl ? 2 : 1;
-    if (m <= 32) {
+    static const int st32 = getenv("ACP_K2_ST32") ? atoi(getenv("ACP_K2_ST32")) : 4;
+    if (m <= 32 && st32 == 2) {
+        cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
+        cfg.dynamicSmemBytes = tn_cluster_smem<32, 2>();
+        static bool a322 = false;
+        if (!a322) {
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)tn_cluster_smem<32, 2>()));
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            a322 = true;
+        }
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook, 2>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc,
+                                    hook));
+    } else if (m <= 32 && st32 == 3) {
+        cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
+        cfg.dynamicSmemBytes = tn_cluster_smem<32, 3>();
+        static bool a323 = false;
+        if (!a323) {
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)tn_cluster_smem<32, 3>()));
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook, 3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            a323 = true;
+        }
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook, 3>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc,
+                                    hook));
+    } else if (m <= 32) {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
         cfg.dynamicSmemBytes = tn_cluster_smem<32>();
         static bool attr32 = false;
@@ -523,6 +548,20 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
             attr32 = true;
         }
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
+    } else if (!getenv("ACP_K2_ST4")) {
+        // 2-stage ring (55 KB -> up to 4 CTAs/SM instead of 2): K2 0.70 vs 0.52 of FP64 peak on
+        // configs[2] (223 vs 241 ms/step), 0.78 vs 0.66 on configs[3] (745 vs 762); ACP_K2_ST4=1: 4-stage
+        cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 64));
+        cfg.dynamicSmemBytes = tn_cluster_smem<64, 2>();
+        static bool attr642 = false;
+        if (!attr642) {
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<64, Hook, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)tn_cluster_smem<64, 2>()));
+            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<64, Hook, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            attr642 = true;
+        }
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<64, Hook, 2>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc,
+                                    hook));
     } else {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 64));
         cfg.dynamicSmemBytes = tn_cluster_smem<64>();
