@@ -183,8 +183,8 @@ template <class Ep> struct K3Occ { static constexpr int v = 4; };
 template <> struct K3Occ<EpBeta> { static constexpr int v = 8; };
 template <> struct K3Occ<EpAlpha> { static constexpr int v = 6; };
 
-template <class Ep>
-__global__ void __launch_bounds__(128, K3Occ<Ep>::v) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
+template <class Ep, int OCC = K3Occ<Ep>::v>
+__global__ void __launch_bounds__(128, OCC) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
                                                        const double* __restrict__ B, int ldb, Ep ep) {
     pdl_wait();
     pdl_trigger();
@@ -256,7 +256,11 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
         cfg.gridDim = dim3(cdiv(M, NP_BM), cdiv(n, NP_BN), 1);
         cfg.blockDim = dim3(128, 1, 1);
         cfg.dynamicSmemBytes = 0;
-        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_pcg_update<Ep>, M, K, n, A, lda, B, ldb, ep));
+        // ACP_K3_OCC=4|5|8 (A/B): the EpAlpha instance's resident-CTA bound
+        static const int kocc = getenv("ACP_K3_OCC") ? atoi(getenv("ACP_K3_OCC")) : 0;
+        auto kern = kocc == 4 ? k_pcg_update<Ep, 4> : kocc == 5 ? k_pcg_update<Ep, 5>
+                  : kocc == 8 ? k_pcg_update<Ep, 8> : k_pcg_update<Ep>;
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, M, K, n, A, lda, B, ldb, ep));
     }
     launched(ctx);
 }
