@@ -155,3 +155,105 @@ def test_2d_model_basics():
     G = m.G_matrix()
     assert G.shape == (576, 8)
     assert np.abs(G.sum(axis=0) * m.dV).max() < 1e-10
+
+
+# ---------------------------------------------------------------- 2D branch (configs[3], [4] shape)
+def _model_2d(**kw):
+    from workloads.configs import small_config_2d
+    cfg = small_config_2d(grid=(24, 24), **kw)
+    return cfg, atom_positions(cfg)
+
+
+def test_2d_g_columns_are_fd_derivatives_of_V():
+    """Both columns g_{I,x}, g_{I,y} of every atom against central differences of
+    V_ion in R_{I,a}; a transposed axis or a wrong k-component fails by O(1)."""
+    cfg, R = _model_2d()
+    m = Model(cfg, R)
+    G = m.G_matrix()
+    h = 1e-4
+    for I in range(m.NA):
+        for a in range(2):
+            Rp, Rm = R.copy(), R.copy()
+            Rp[I, a] += h
+            Rm[I, a] -= h
+            fd = (Model(cfg, Rp).v_ion() - Model(cfg, Rm).v_ion()) / (2 * h)
+            col = G[:, 2 * I + a]
+            assert np.abs(fd - col).max() < 1e-7 * np.abs(col).max()
+            assert abs(m.integrate(col)) < 1e-12 * np.abs(col).max() * m.Omega
+
+
+def test_2d_d2V_all_entries_fd():
+    """d2V_I/dR_a dR_b for a, b in {x, y} (incl. the a != b cross terms) against central
+    differences of g_{I,b} in R_{I,a}; the 2x2 block is symmetric."""
+    cfg, R = _model_2d()
+    m = Model(cfg, R)
+    h = 1e-4
+    I = 2
+    H2 = m.d2V(I)
+    for a in range(2):
+        Rp, Rm = R.copy(), R.copy()
+        Rp[I, a] += h
+        Rm[I, a] -= h
+        dG = (Model(cfg, Rp).G_matrix() - Model(cfg, Rm).G_matrix()) / (2 * h)
+        for b in range(2):
+            fd = dG[:, 2 * I + b]
+            assert np.abs(fd - H2[:, a, b]).max() < 1e-7 * np.abs(H2).max(), (a, b)
+    assert np.array_equal(H2[:, 0, 1], H2[:, 1, 0])
+    # the cross term is not identically zero for a generic position (else the check is vacuous)
+    assert np.abs(H2[:, 0, 1]).max() > 1e-2 * np.abs(H2).max()
+
+
+def test_2d_eii_gradient_and_hessian_fd():
+    """E_II (reading R4) in 2D: gradient vs central differences of the energy, the full Hessian
+    (x/y and cross-atom blocks) vs central differences of the gradient, translation invariance."""
+    cfg, R = _model_2d()
+    m = Model(cfg, R)
+    g = m.e_ii_gradient()
+    Hs = m.e_ii_hessian()
+    for I in range(m.NA):
+        for a in range(2):
+            Rp, Rm = R.copy(), R.copy()
+            Rp[I, a] += 1e-2
+            Rm[I, a] -= 1e-2
+            fdg = (Model(cfg, Rp).e_ii() - Model(cfg, Rm).e_ii()) / 2e-2
+            assert abs(fdg - g[I, a]) < 1e-5 * np.abs(g).max()
+            Rp, Rm = R.copy(), R.copy()
+            Rp[I, a] += 1e-4
+            Rm[I, a] -= 1e-4
+            fdH = (Model(cfg, Rp).e_ii_gradient() - Model(cfg, Rm).e_ii_gradient()).reshape(-1) / 2e-4
+            assert np.abs(fdH - Hs[2 * I + a, :]).max() < 1e-6 * np.abs(Hs).max()
+    assert np.abs(Hs - Hs.T).max() < 1e-12 * np.abs(Hs).max()
+    # translation invariance in x and in y separately: sum over J of the (I a, J b) block is 0
+    for b in range(2):
+        assert np.abs(Hs[:, b::2].sum(axis=1)).max() < 1e-11 * np.abs(Hs).max()
+    assert np.abs(g.sum(axis=0)).max() < 1e-11 * np.abs(g).max()
+
+
+def test_2d_eii_pair_closed_form_gaussians():
+    """Two 2D Gaussians through the Yukawa symbol 4pi/(eps0(|k|^2+kappa^2)): in the
+    plane this is the kernel (2/eps0) K_0(kappa r) (the 2D Green's function of -Delta + kappa^2
+    times 4 pi / eps0), so E_12 = Z^2 (2/eps0) E[K_0(kappa |X|)], X ~ N(d, 2 sigma^2 I_2).  A
+    large cell makes the periodic images negligible; the expectation is a 2D quadrature."""
+    from scipy.special import k0
+    from workloads.configs import small_config_2d
+    cfg = small_config_2d(n_side=2, spacing=30.0, kappa=0.4, sigma=1.0, grid=(256, 256), jitter=0.0)
+    R = np.array([[20.0, 25.0], [22.9, 26.3]])
+    m = Model(cfg, R)
+    d = R[1] - R[0]
+    s2 = 2 * cfg.sigma ** 2
+    # polar quadrature centred on the kernel's log singularity at X = 0, radial variable r = u^2
+    # (the integrand ~ u^3 log u is then smooth enough for Gauss-Legendre), uniform in angle
+    nu_, nt = 600, 512
+    xu, wu = np.polynomial.legendre.leggauss(nu_)
+    umax = np.sqrt(np.hypot(*d) + 10.0 * np.sqrt(s2))
+    u = 0.5 * umax * (xu + 1)
+    wu = 0.5 * umax * wu
+    r = u * u
+    th = 2 * np.pi * np.arange(nt) / nt
+    X = r[:, None] * np.cos(th)[None, :]
+    Y = r[:, None] * np.sin(th)[None, :]
+    dens = np.exp(-((X - d[0]) ** 2 + (Y - d[1]) ** 2) / (2 * s2)) / (2 * np.pi * s2)
+    val = k0(cfg.kappa * r)[:, None]
+    ex = float(np.sum((wu * 2 * u * r)[:, None] * dens * val) * (2 * np.pi / nt))
+    ref = cfg.Z ** 2 * (2.0 / cfg.eps0) * ex
+    assert abs(m.e_ii() - ref) < 1e-9 * abs(ref), (m.e_ii(), ref)

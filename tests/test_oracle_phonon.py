@@ -61,3 +61,53 @@ def test_periodic_lattice_acoustic_mode():
     lam, om, _ = phonon.phonon_modes(phonon.dynamical_matrix(m, gs.rho, G, U))
     assert np.sum(np.abs(lam) < 1e-9 * np.abs(lam).max()) == 1
     assert lam[1] > 1e-6 * np.abs(lam).max()
+
+
+# ---------------------------------------------------------------- 2D (configs[3], [4] shape)
+@pytest.fixture(scope="module")
+def system_2d():
+    from workloads.configs import small_config_2d
+    cfg = small_config_2d(grid=(24, 24))
+    R = atom_positions(cfg)
+    m = Model(cfg, R)
+    gs = scf(m, tol=1e-13)
+    H = m.hamiltonian_dense(gs.V)
+    G = m.G_matrix()
+    C0 = rs.chi0_adler_wiser_matrix(m, H, cfg.n_occ)
+    U = rs.dyson_dense(m, C0, G)
+    D, parts = phonon.dynamical_matrix(m, gs.rho, G, U, parts=True)
+    return cfg, R, m, gs, G, C0, D, parts
+
+
+def test_2d_dfpt_matches_frozen_phonon(system_2d):
+    """2D Eq. SecDeriv/chiterm vs central differences of the 2D forces
+    (frozen phonon): pins the x/y column order of G, the 2D d2V block (incl. the
+    x-y cross terms), the 2D E_II Hessian and the 2f prefactor together."""
+    cfg, R, m, gs, G, C0, D, parts = system_2d
+    Dfd = phonon.fd_dynamical_matrix(cfg, R, delta=1e-3, gs0=gs)
+    err = np.abs(Dfd - D).max() / np.abs(D).max()
+    assert err < 2e-6, err
+    # the off-diagonal x-y blocks carry weight (a dropped cross term would show)
+    xy = np.abs(D[0::2, 1::2]).max() / np.abs(D).max()
+    assert xy > 1e-3
+    # wrong prefactor 2 instead of 2f = 4 (reading R2) is far outside the band
+    Dw = phonon.dynamical_matrix(m, gs.rho, G, rs.dyson_dense(m, 0.5 * C0, G))
+    assert np.abs(Dfd - Dw).max() / np.abs(D).max() > 1e-2
+    # so is a local term with the x-y cross entries dropped
+    D_chi, D_loc, D_ii = parts
+    D_loc_diag = D_loc.copy()
+    D_loc_diag[0::2, 1::2] = 0.0
+    D_loc_diag[1::2, 0::2] = 0.0
+    Dd = 0.5 * ((D_chi + D_loc_diag + D_ii) + (D_chi + D_loc_diag + D_ii).T)
+    if np.abs(D_loc[0::2, 1::2]).max() > 1e-4 * np.abs(D).max():
+        assert np.abs(Dfd - Dd).max() / np.abs(D).max() > 10 * err
+
+
+def test_2d_sum_rule_and_symmetry(system_2d):
+    """Acoustic sum rule in x and in y (a rigid translation along either axis costs nothing)."""
+    D = system_2d[6]
+    assert np.abs(D - D.T).max() == 0.0
+    for b in range(2):
+        assert np.abs(D[:, b::2].sum(axis=1)).max() < 1e-8 * np.abs(D).max()
+    lam = np.linalg.eigvalsh(D)
+    assert np.sum(np.abs(lam) < 1e-7 * np.abs(lam).max()) == 2   # two acoustic modes in 2D
