@@ -73,6 +73,47 @@ def sketch_matrix(Psi: np.ndarray, Gt: np.ndarray) -> np.ndarray:
     return M
 
 
+# Large sketch matrices (configs[3], [4]: up to 4096 x 65536) are processed in row blocks on a
+# thread pool -- numpy releases the GIL inside these ufuncs / BLAS calls.  Same arithmetic as the
+# one-line forms used for small matrices (sum of squares per column; A <- A - 2 v (v^T A)), only
+# the summation order of the column norms differs (rounding).
+_BIG = 1 << 24
+_ROWS = 64
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        import concurrent.futures
+        import os
+        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=os.cpu_count() or 1)
+    return _POOL
+
+
+_POOL = None
+
+
+def _col_norms2(sub: np.ndarray) -> np.ndarray:
+    if sub.size < _BIG:
+        return np.einsum("ij,ij->j", sub, sub)
+    blocks = range(0, sub.shape[0], _ROWS)
+    parts = list(_pool().map(lambda i: np.einsum("ij,ij->j", sub[i:i + _ROWS], sub[i:i + _ROWS]), blocks))
+    return np.sum(parts, axis=0)
+
+
+def _householder_update(sub: np.ndarray, v: np.ndarray) -> None:
+    """sub <- (I - 2 v v^T) sub for a unit vector v."""
+    if sub.size < _BIG:
+        sub -= 2.0 * np.outer(v, v @ sub)
+        return
+    blocks = range(0, sub.shape[0], _ROWS)
+    w = np.sum(list(_pool().map(lambda i: v[i:i + _ROWS] @ sub[i:i + _ROWS], blocks)), axis=0)
+
+    def upd(i):
+        sub[i:i + _ROWS] -= np.outer(2.0 * v[i:i + _ROWS], w)
+    list(_pool().map(upd, blocks))
+
+
 @dataclasses.dataclass
 class QRCP:
     perm: np.ndarray     # column permutation (Pi~), perm[j] = original column at position j
@@ -98,7 +139,7 @@ def qrcp(A: np.ndarray, eps: float, k_max: int | None = None, n_fixed: int | Non
     n_mu = kmax
     for j in range(kmax):
         sub = A[j:, j:]
-        norms2 = np.einsum("ij,ij->j", sub, sub)
+        norms2 = _col_norms2(sub)
         p = j + int(np.argmax(norms2))
         rjj = float(np.sqrt(norms2[p - j]))
         if r11 is None:
@@ -116,7 +157,7 @@ def qrcp(A: np.ndarray, eps: float, k_max: int | None = None, n_fixed: int | Non
         vn = np.linalg.norm(v)
         if vn > 0:
             v /= vn
-            A[j:, j:] -= 2.0 * np.outer(v, v @ A[j:, j:])
+            _householder_update(sub, v)
         A[j + 1:, j] = 0.0
         rdiag.append(rjj)
     R = np.triu(A[:n_mu, :])
@@ -147,10 +188,12 @@ def compress(model: Model, Psi: np.ndarray, Gp: np.ndarray, theta, nu, eps: floa
 
 
 def compressed_W(model: Model, H: np.ndarray, Psi: np.ndarray, eps_occ: np.ndarray,
-                 S: np.ndarray, Xi: np.ndarray, Nc: int, return_zeta: bool = False):
+                 S: np.ndarray, Xi: np.ndarray, Nc: int, return_zeta: bool = False, solve=None):
     """Alg. 3 steps 2-3: solve Eq. eqncompressU directly, build W by Eq. eqnW.
 
     W_mu = 2 f sum_i psi_i (.) ( sum_c zeta~_{c mu} l_c(eps_i) ) psi_i(r_mu).
+    solve(shift, rhs) -> zeta replaces the dense solve (H unused then): the MINRES of
+    oracle.iterative for grids too large for dense matrices.
     """
     nodes = chebyshev_nodes(eps_occ[0], eps_occ[-1], Nc)
     Lw = lagrange_weights(nodes, eps_occ)            # (N_occ, Nc)
@@ -158,8 +201,11 @@ def compressed_W(model: Model, H: np.ndarray, Psi: np.ndarray, eps_occ: np.ndarr
     W = np.zeros_like(Xi)
     zetas = []
     for c in range(Nc):
-        A = projected_operator(model, H, Psi, nodes[c])
-        Z = np.linalg.solve(A, rhs)                  # zeta~_{c mu}, all mu
+        if solve is None:
+            A = projected_operator(model, H, Psi, nodes[c])
+            Z = np.linalg.solve(A, rhs)              # zeta~_{c mu}, all mu
+        else:
+            Z = solve(nodes[c], rhs)
         if return_zeta:
             zetas.append(Z)
         Phi_c = Psi @ (Lw[:, c:c + 1] * Psi[S, :].T)  # sum_i psi_i l_c(eps_i) psi_i(r_mu)
@@ -193,10 +239,13 @@ def smw_update(model: Model, G: np.ndarray, W: np.ndarray, S: np.ndarray):
 
 def acp_dyson(model: Model, H: np.ndarray, Psi: np.ndarray, eps_occ: np.ndarray,
               G: np.ndarray, Nc: int, n_outer: int, id_eps: float,
-              draws: Callable[[int, int], tuple], n_fixed: int | None = None) -> ACPResult:
+              draws: Callable[[int, int], tuple], n_fixed: int | None = None, solve=None,
+              keep=True, log=None, on_outer=None) -> ACPResult:
     """Alg. 4 with a fixed number of outer iterations.
 
     draws(k, n_cols) -> (theta, nu): the SRFT randomness of outer iteration k.
+    solve: see compressed_W.  keep=False drops the per-iteration W / Y (memory at full size);
+    on_outer(k, S, W, Y) sees them before they are dropped.
     """
     Gp = G.copy()                      # v U~^0 = v B = G
     U_prev = np.zeros_like(G)
@@ -204,13 +253,20 @@ def acp_dyson(model: Model, H: np.ndarray, Psi: np.ndarray, eps_occ: np.ndarray,
     for k in range(n_outer):
         theta, nu = draws(k, G.shape[1])
         S, Xi, qr = compress(model, Psi, Gp, theta, nu, id_eps, n_fixed=n_fixed)
-        W = compressed_W(model, H, Psi, eps_occ, S, Xi, Nc)
+        if log:
+            log(f"outer {k}: N_mu = {len(S)}")
+        W = compressed_W(model, H, Psi, eps_occ, S, Xi, Nc, solve=solve)
+        del Xi
         U, Gp, Y = smw_update(model, G, W, S)
+        if on_outer:
+            on_outer(k, S, W, Y)
         res.diff.append(float(np.linalg.norm(U - U_prev)))
         res.n_mu.append(len(S))
         res.S.append(S)
-        res.W.append(W)
+        res.W.append(W if keep else None)
         res.Y.append(Y)
+        if log:
+            log(f"outer {k}: W done, ||U^k - U^k-1|| = {res.diff[-1]:.3e}")
         U_prev = U
     res.U = U_prev
     return res

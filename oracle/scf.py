@@ -47,8 +47,12 @@ def density(model: Model, Psi: np.ndarray) -> np.ndarray:
 
 def scf(model: Model, tol: float = 1e-12, max_iter: int = 400, n_extra: int = 4,
         rho0: np.ndarray | None = None, history: int = 12, beta: float = 0.5,
-        kerker_k0: float = 0.5, verbose: bool = False) -> GroundState:
-    """Self-consistent field iteration to ||rho_out - rho_in|| / ||rho_in|| <= tol."""
+        kerker_k0: float = 0.5, verbose: bool = False, eigensolver=None) -> GroundState:
+    """Self-consistent field iteration to ||rho_out - rho_in|| / ||rho_in|| <= tol.
+
+    eigensolver(model, V, nb, X0, scf_res) -> (eps, Psi) replaces the dense diagonalisation (the
+    matrix-free LOBPCG of oracle.iterative); X0 = the previous orbitals or None,
+    scf_res = the previous SCF residual (inf at first), which sets how tightly it must solve."""
     m = model.pseudocharge()
     if rho0 is None:
         rho = np.clip(-m, 0.0, None)
@@ -67,7 +71,10 @@ def scf(model: Model, tol: float = 1e-12, max_iter: int = 400, n_extra: int = 4,
     err = np.inf
     for it in range(1, max_iter + 1):
         V = model.yukawa(rho + m)
-        eps, Psi = eigenpairs(model, V, nb)
+        if eigensolver is None:
+            eps, Psi = eigenpairs(model, V, nb)
+        else:
+            eps, Psi = eigensolver(model, V, nb, None if it == 1 else Psi * np.sqrt(model.dV), err)
         rho_out = density(model, Psi[:, : model.n_occ])
         res = rho_out - rho
         err = float(np.linalg.norm(res) / np.linalg.norm(rho))

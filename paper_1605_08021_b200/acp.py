@@ -102,6 +102,31 @@ def _ptr(t: Optional[torch.Tensor]):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _chk(name: str, t, device: int, dtype=torch.float64, shape=None, min_numel=None):
+    """Validate a device argument before its pointer crosses the C ABI: CUDA, contiguous, on the
+    context's device, the expected dtype and shape (None entries = any extent)."""
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise AcpError(f"{name}: expected a CUDA tensor")
+    if t.device.index != device:
+        raise AcpError(f"{name}: tensor on cuda:{t.device.index}, context on cuda:{device}")
+    if t.dtype != dtype:
+        raise AcpError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise AcpError(f"{name}: expected a contiguous tensor")
+    if shape is not None:
+        if t.dim() != len(shape) or any(e is not None and e != d for e, d in zip(shape, t.shape)):
+            raise AcpError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if min_numel is not None and t.numel() < min_numel:
+        raise AcpError(f"{name}: expected at least {min_numel} elements, got {t.numel()}")
+
+
+def _i32(S: torch.Tensor) -> torch.Tensor:
+    """Pivot indices as the int32 array the C ABI takes (the oracle hands out int64)."""
+    return S.to(torch.int32).contiguous()
+
+
 def _host(a, dtype=np.float64):
     a = np.ascontiguousarray(a, dtype=dtype)
     return a, a.ctypes.data_as(_dp if dtype == np.float64 else _ip)
@@ -188,9 +213,13 @@ class Context:
     # -- 2. compression --------------------------------------------------
     def compress(self, Psi, Gp, theta, nu, id_eps=1e-3, n_mu_fixed=0, n_mu_max=None):
         self._pre()
+        _chk("Psi", Psi, self.device, shape=(self.n_occ, self.Ng))
+        _chk("Gp", Gp, self.device, shape=(None, self.Ng))
         n_cols = Gp.shape[0]
         th, thp = _host(theta)
         nuh, nup = _host(nu, np.int32)
+        if th.size != n_cols:
+            raise AcpError(f"theta: expected {n_cols} draws, got {th.size}")
         r_half = len(nuh)
         if n_mu_max is None:
             n_mu_max = min(self.n_occ * 2 * r_half, self.Ng)
@@ -206,12 +235,19 @@ class Context:
     def apply_chi0(self, Psi, eps, V, S, Xi, n_cheb, cg_tol=1e-11, max_iter=2000, mu_range=None, W=None):
         self._pre()
         n_mu = Xi.shape[0]
+        S = _i32(S)
         mb, me = (0, n_mu) if mu_range is None else mu_range
         if W is None:
             W = torch.zeros(n_mu, self.Ng, dtype=torch.float64, device=Psi.device)
+        _chk("Psi", Psi, self.device, shape=(self.n_occ, self.Ng))
+        _chk("eps", eps, self.device, min_numel=self.n_occ)
+        _chk("V", V, self.device, shape=(self.Ng,))
+        _chk("S", S, self.device, dtype=torch.int32, shape=(n_mu,))
+        _chk("Xi", Xi, self.device, shape=(n_mu, self.Ng))
+        _chk("W", W, self.device, shape=(n_mu, self.Ng))
         info = np.zeros(4)
         eps_occ = eps[: self.n_occ].contiguous()
-        self._check(_lib.acp_apply_chi0(self._h, _ptr(Psi), _ptr(eps_occ), _ptr(V), _ptr(S.contiguous()),
+        self._check(_lib.acp_apply_chi0(self._h, _ptr(Psi), _ptr(eps_occ), _ptr(V), _ptr(S),
                                         _ptr(Xi), n_mu, mb, me, n_cheb, cg_tol, max_iter, _ptr(W),
                                         info.ctypes.data_as(_dp)), "acp_apply_chi0")
         return W, dict(max_iter=int(info[0]), total_iter=int(info[1]), max_rel_res=float(info[2]),
@@ -221,8 +257,19 @@ class Context:
     def dyson(self, Psi, eps, V, G, n_cheb, n_outer, theta, nu, id_eps=1e-3, n_mu_fixed=0, cg_tol=1e-11,
               max_cg_iter=2000, U=None):
         self._pre()
-        theta = np.ascontiguousarray(theta, dtype=np.float64).reshape(n_outer, -1)
-        nu = np.ascontiguousarray(nu, dtype=np.int32).reshape(n_outer, -1)
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+        if theta.size != n_outer * self.n_pert:
+            raise AcpError(f"theta: expected n_outer x dN_A = {n_outer * self.n_pert} draws, got {theta.size}")
+        theta = theta.reshape(n_outer, -1)
+        nu = np.ascontiguousarray(nu, dtype=np.int32)
+        if nu.size % n_outer:
+            raise AcpError(f"nu: {nu.size} frequencies do not split into {n_outer} outer iterations")
+        nu = nu.reshape(n_outer, -1)
+        _chk("Psi", Psi, self.device, shape=(self.n_occ, self.Ng))
+        _chk("eps", eps, self.device, min_numel=self.n_occ)
+        _chk("V", V, self.device, shape=(self.Ng,))
+        _chk("G", G, self.device, shape=(self.n_pert, self.Ng))
+        _chk("U", U, self.device, shape=(self.n_pert, self.Ng))
         r_half = nu.shape[1]
         o = acp_dyson_opts(n_cheb, n_outer, r_half, id_eps, n_mu_fixed, cg_tol, max_cg_iter)
         if U is None:
@@ -240,17 +287,28 @@ class Context:
     def smw_update(self, G, S, W, U=None, Gp=None):
         """Eq. dyson4: returns (U, Gp) with U = W Y, Gp = G + (K W) Y."""
         self._pre()
+        S = _i32(S)
+        _chk("G", G, self.device, shape=(self.n_pert, self.Ng))
+        _chk("W", W, self.device, shape=(None, self.Ng))
+        _chk("S", S, self.device, dtype=torch.int32, shape=(W.shape[0],))
+        _chk("U", U, self.device, shape=(self.n_pert, self.Ng))
+        _chk("Gp", Gp, self.device, shape=(self.n_pert, self.Ng))
         if U is None:
             U = self._empty(self.n_pert, self.Ng)
         if Gp is None:
             Gp = self._empty(self.n_pert, self.Ng)
-        self._check(_lib.acp_smw_update(self._h, _ptr(G), _ptr(S.contiguous()), _ptr(W), W.shape[0], _ptr(U),
+        self._check(_lib.acp_smw_update(self._h, _ptr(G), _ptr(S), _ptr(W), W.shape[0], _ptr(U),
                                         _ptr(Gp)), "acp_smw_update")
         return U, Gp
 
     # -- 5. dynamical matrix --------------------------------------------
     def dynamical_matrix(self, R, rho, G, U, masses=None):
         self._pre()
+        _chk("rho", rho, self.device, shape=(self.Ng,))
+        _chk("G", G, self.device, shape=(self.n_pert, self.Ng))
+        _chk("U", U, self.device, shape=(self.n_pert, self.Ng))
+        if np.asarray(R).size != self.n_pert:
+            raise AcpError(f"R: expected N_A x d = {self.n_pert} coordinates")
         Rh, Rp = _host(R)
         n = self.n_pert
         D = np.zeros((n, n))
@@ -277,6 +335,9 @@ class Context:
     # -- building blocks ------------------------------------------------
     def fourier_apply(self, X, which: int, tau: float = 0.0, diag=None, shift=None):
         self._pre()
+        _chk("X", X, self.device, shape=(None, self.Ng))
+        _chk("diag", diag, self.device, shape=(self.Ng,))
+        _chk("shift", shift, self.device, shape=(X.shape[0],))
         Y = torch.empty_like(X)
         self._check(_lib.acp_fourier_apply(self._h, _ptr(X), X.shape[0], which, tau, _ptr(diag), _ptr(shift),
                                            _ptr(Y)), "acp_fourier_apply")

@@ -1,8 +1,30 @@
 // api.cu -- extern "C" entry points of include/acp_b200.h.  Argument checking,
 // device selection and error translation only; all arithmetic lives in the kernels.
+#include <mutex>
+#include <map>
 #include "common.cuh"
 
 #include <cmath>
+
+namespace acp {
+void func_attr(const void* fn, size_t smem, bool nonportable_cluster) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, std::pair<size_t, bool>> done;
+    int dev = 0;
+    ACP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    auto& d = done[{dev, fn}];
+    if (d.first < smem) {
+        ACP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        d.first = smem;
+    }
+    if (nonportable_cluster && !d.second) {
+        ACP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        d.second = true;
+    }
+}
+}  // namespace acp
+
 
 using acp::Error;
 

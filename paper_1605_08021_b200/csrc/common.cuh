@@ -169,6 +169,11 @@ inline void launched_at(acp_context* ctx, const char* file, int line, int n = 1)
     }
 }
 
+// Raise a kernel's dynamic shared-memory limit to >= smem bytes (and allow non-portable cluster
+// sizes) on the CURRENT device.  Function attributes belong to a device context, so the record
+// of what was set is keyed by (device, kernel); it is mutex-protected (api.cu).
+void func_attr(const void* fn, size_t smem, bool nonportable_cluster = false);
+
 inline void sync(acp_context* ctx) { ACP_CUDA(cudaStreamSynchronize(ctx->stream)); }
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }

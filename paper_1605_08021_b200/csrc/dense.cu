@@ -507,25 +507,15 @@ void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
     // deferred mode (acp_dyson): the status accumulates in the device statistics, read at the end
     int* st = ctx->defer ? reinterpret_cast<int*>(ctx->defer_stats + 6) : ctx->wsi("lu_status", 1);
     if (!ctx->defer) ACP_CUDA(cudaMemsetAsync(st, 0, sizeof(int), ctx->stream));
-    static bool attr = false;
-    if (!attr) {
-        ACP_CUDA(cudaFuncSetAttribute(k_lu_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    func_attr((const void*)k_lu_panel, 200 * 1024);
     for (int p0 = 0; p0 < n; p0 += 32) {
         const int pw = std::min(32, n - p0);
         const int R = n - p0;
         const size_t pbytes = (size_t)R * pw * sizeof(double);
         const int use_smem = pbytes <= 200 * 1024;
         if (R <= 512 && getenv("ACP_LU_WARP_PANEL")) {  // opt-in: measured no faster end to end
-            static bool wattr = false;
-            if (!wattr) {
-                for (const void* f : {(const void*)k_lu_panel_warp<8>, (const void*)k_lu_panel_warp<16>,
-                                      (const void*)k_lu_panel_warp<32>})
-                    ACP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  32 * 513 * (int)sizeof(double)));
-                wattr = true;
-            }
+            for (const void* f : {(const void*)k_lu_panel_warp<8>, (const void*)k_lu_panel_warp<16>, (const void*)k_lu_panel_warp<32>})
+                func_attr(f, 32 * 513 * (int)sizeof(double));
             const size_t ls = (size_t)32 * (R + 1) * sizeof(double);
             if (R <= 128)
                 k_lu_panel_warp<8><<<1, 32 * cdiv(R, 8), ls, ctx->stream>>>(AB, n, p0, pw, piv, st);
@@ -562,11 +552,7 @@ void lu_solve(acp_context* ctx, double* A, int n, double* B, int nrhs) {
     const size_t abytes = (size_t)n * n * sizeof(double), bbytes = (size_t)n * nrhs * sizeof(double);
     const int use_smem = abytes + bbytes <= 224 * 1024 ? 2 : abytes <= 224 * 1024 ? 1 : 0;
     const size_t bytes = use_smem == 2 ? abytes + bbytes : use_smem == 1 ? abytes : 0;
-    static bool attr = false;
-    if (!attr) {
-        ACP_CUDA(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
-        attr = true;
-    }
+    func_attr((const void*)k_lu_solve, 224 * 1024);
     k_lu_solve<<<1, 1024, bytes, ctx->stream>>>(A, n, B, nrhs, use_smem, st, ctx->defer);
     launched(ctx);
     if (ctx->defer) return;
@@ -961,17 +947,13 @@ static void sym_eigvals_tridiag(acp_context* ctx, double* A, int n, double* w) {
     double* p = ctx->wsd("eig_p", n);
     const size_t small = ((size_t)2 * n + 32 + (size_t)n * n) * sizeof(double);
     if (small <= 200 * 1024) {
-        static bool attr = false;
-        if (!attr) {
-            ACP_CUDA(cudaFuncSetAttribute(k_tridiag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr = true;
-        }
+        func_attr((const void*)k_tridiag<false>, 200 * 1024);
         const int nt = std::min(1024, std::max(128, cdiv(n, 32) * 32 * 4));
         k_tridiag<false><<<1, nt, small, ctx->stream>>>(A, n, p, d, e);
     } else {
         const size_t smem = ((size_t)2 * n + 32) * sizeof(double);
         const void* fn = (const void*)k_tridiag<true>;
-        if (smem > 48 * 1024) ACP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (smem > 48 * 1024) func_attr(fn, smem);
         int occ = 0;
         ACP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
         int dev = 0, sms = 0;
@@ -987,11 +969,7 @@ static void sym_eigvals_tridiag(acp_context* ctx, double* A, int n, double* w) {
     const size_t ms = (size_t)2 * n * sizeof(double);
     ACP_REQUIRE(ms <= 200 * 1024, "eigenvalue search: n too large");
     if (ms > 48 * 1024) {
-        static bool a2 = false;
-        if (!a2) {
-            ACP_CUDA(cudaFuncSetAttribute(k_tri_multisect, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            a2 = true;
-        }
+        func_attr((const void*)k_tri_multisect, 200 * 1024);
     }
     k_tri_multisect<<<cdiv(n, 8), 256, ms, ctx->stream>>>(n, d, e, w);
     launched(ctx);
@@ -1014,11 +992,7 @@ void sym_eig(acp_context* ctx, double* A, int n, double* w, double* V) {
     double* rot = ctx->wsd("eig_rot", 4 * (size_t)(n / 2 + 2));
     const size_t bytes = (size_t)n * n * sizeof(double);
     const int use_smem = bytes <= 200 * 1024;
-    static bool attr = false;
-    if (!attr) {
-        ACP_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    func_attr((const void*)k_jacobi, 200 * 1024);
     // one warp per rotation pair (n/2 pairs) is enough; fewer threads make each barrier cheaper
     const int jt = std::min(1024, std::max(64, ((n + 1) / 2) * 32));
     k_jacobi<<<1, jt, use_smem ? bytes : 0, ctx->stream>>>(A, n, Vt, w, order, rot, 40, use_smem);

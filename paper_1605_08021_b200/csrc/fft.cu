@@ -505,16 +505,9 @@ __global__ void __launch_bounds__(1024) k_fft2d(FftGeom G, const double2* __rest
 }
 
 // ============================================================================ launchers
-// cudaFuncSetAttribute once per kernel instance and size (a host call per launch would make the
-// un-graphed launches host-bound).
-static void set_smem_attr(const void* kern, size_t smem, bool cluster16) {
-    static std::map<const void*, size_t> done;  // per kernel instance (device attributes are per process)
-    size_t& d = done[kern];
-    if (d >= smem) return;
-    ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (cluster16) ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    d = smem;
-}
+// shared-memory / cluster-size attributes once per (device, kernel instance) and size (a host call
+// per launch would make the un-graphed launches host-bound)
+static void set_smem_attr(const void* kern, size_t smem, bool cluster16) { func_attr(kern, smem, cluster16); }
 
 template <int IO>
 static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {

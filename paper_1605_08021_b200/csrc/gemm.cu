@@ -129,12 +129,7 @@ void gemm_nn(acp_context* ctx, int M, int K, int n, double alpha, const double* 
     if (M <= 0 || n <= 0) return;
     EpAxpby ep{alpha, beta, C, ldc};
     if (K >= 64) {  // genuine GEMM (SMW products at large N_mu): 64 x 64 multistage tiles
-        static bool attr = false;
-        if (!attr) {
-            ACP_CUDA(cudaFuncSetAttribute(k_gemm_nn_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)nn_big_smem()));
-            attr = true;
-        }
+        func_attr((const void*)k_gemm_nn_big, (int)nn_big_smem());
         k_gemm_nn_big<<<dim3(cdiv(M, GB_BM), cdiv(n, GB_BN)), 256, nn_big_smem(), ctx->stream>>>(M, K, n, A, lda, B,
                                                                                                  ldb, ep);
         launched(ctx);

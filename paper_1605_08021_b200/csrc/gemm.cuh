@@ -516,62 +516,32 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
     if (m <= 32 && st32 == 2) {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
         cfg.dynamicSmemBytes = tn_cluster_smem<32, 2>();
-        static bool a322 = false;
-        if (!a322) {
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)tn_cluster_smem<32, 2>()));
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            a322 = true;
-        }
+        func_attr((const void*)k_tn_cluster<32, Hook, 2>, (int)tn_cluster_smem<32, 2>(), true);
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook, 2>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc,
                                     hook));
     } else if (m <= 32 && st32 == 3) {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
         cfg.dynamicSmemBytes = tn_cluster_smem<32, 3>();
-        static bool a323 = false;
-        if (!a323) {
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)tn_cluster_smem<32, 3>()));
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook, 3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            a323 = true;
-        }
+        func_attr((const void*)k_tn_cluster<32, Hook, 3>, (int)tn_cluster_smem<32, 3>(), true);
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook, 3>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc,
                                     hook));
     } else if (m <= 32) {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
         cfg.dynamicSmemBytes = tn_cluster_smem<32>();
-        static bool attr32 = false;
-        if (!attr32) {
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)tn_cluster_smem<32>()));
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<32, Hook>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            attr32 = true;
-        }
+        func_attr((const void*)k_tn_cluster<32, Hook>, (int)tn_cluster_smem<32>(), true);
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
     } else if (!getenv("ACP_K2_ST4")) {
         // 2-stage ring (55 KB -> up to 4 CTAs/SM instead of 2): K2 0.70 vs 0.52 of FP64 peak on
         // configs[2] (223 vs 241 ms/step), 0.78 vs 0.66 on configs[3] (745 vs 762); ACP_K2_ST4=1: 4-stage
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 64));
         cfg.dynamicSmemBytes = tn_cluster_smem<64, 2>();
-        static bool attr642 = false;
-        if (!attr642) {
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<64, Hook, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)tn_cluster_smem<64, 2>()));
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<64, Hook, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            attr642 = true;
-        }
+        func_attr((const void*)k_tn_cluster<64, Hook, 2>, (int)tn_cluster_smem<64, 2>(), true);
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<64, Hook, 2>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc,
                                     hook));
     } else {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 64));
         cfg.dynamicSmemBytes = tn_cluster_smem<64>();
-        static bool attr64 = false;
-        if (!attr64) {
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<64, Hook>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)tn_cluster_smem<64>()));
-            ACP_CUDA(cudaFuncSetAttribute(k_tn_cluster<64, Hook>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            attr64 = true;
-        }
+        func_attr((const void*)k_tn_cluster<64, Hook>, (int)tn_cluster_smem<64>(), true);
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<64, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
     }
     launched(ctx);

@@ -241,13 +241,8 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
             kern = k_pcg_update_big<Ep, 1, 2, 3>;
             smem = nn_big_smem<2>();
         }
-        static bool attr = false;
-        if (!attr) {
-            for (const void* f : {(const void*)k_pcg_update_big<Ep, 0>, (const void*)k_pcg_update_big<Ep, 1>,
-                                  (const void*)k_pcg_update_big<Ep, 2>, (const void*)k_pcg_update_big<Ep, 1, 2, 3>})
-                ACP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nn_big_smem()));
-            attr = true;
-        }
+        for (const void* f : {(const void*)k_pcg_update_big<Ep, 0>, (const void*)k_pcg_update_big<Ep, 1>, (const void*)k_pcg_update_big<Ep, 2>, (const void*)k_pcg_update_big<Ep, 1, 2, 3>})
+            func_attr(f, (int)nn_big_smem());
         cfg.gridDim = dim3(cdiv(M, GB_BM), cdiv(n, GB_BN), 1);
         cfg.blockDim = dim3(256, 1, 1);
         cfg.dynamicSmemBytes = smem;
@@ -429,13 +424,7 @@ static bool launch_proj_update(acp_context* ctx, int K, int m, int n, double alp
     tn_split(K, CS, kchunk);
     if (kchunk > PU_KMAX) return false;
     const size_t smem = pu_smem(kchunk);
-    static bool attr = false;
-    if (!attr) {
-        ACP_CUDA(cudaFuncSetAttribute(k_proj_update<Hook, Ep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)pu_smem(PU_KMAX)));
-        ACP_CUDA(cudaFuncSetAttribute(k_proj_update<Hook, Ep>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
-    }
+    func_attr((const void*)k_proj_update<Hook, Ep>, (int)pu_smem(PU_KMAX), true);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CS, cdiv(n, PU_BN), 1);
     cfg.blockDim = dim3(PU_T, 1, 1);
@@ -569,12 +558,7 @@ template <class Ep>
 static void launch_nn_ep(acp_context* ctx, int M, int K, int n, const double* A, int lda, const double* B, int ldb,
                          const Ep& ep) {
     if (K >= 64) {
-        static bool attr = false;
-        if (!attr) {
-            ACP_CUDA(cudaFuncSetAttribute(k_nn_ep_big<Ep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)nn_big_smem()));
-            attr = true;
-        }
+        func_attr((const void*)k_nn_ep_big<Ep>, (int)nn_big_smem());
         k_nn_ep_big<Ep><<<dim3(cdiv(M, GB_BM), cdiv(n, GB_BN)), 256, nn_big_smem(), ctx->stream>>>(M, K, n, A, lda, B,
                                                                                                    ldb, ep);
     } else {
@@ -993,12 +977,7 @@ void apply_chi0(acp_context* ctx, const double* Psi, const double* eps, const do
         k_w_sum<<<cdiv((long long)per, 256), 256, 0, ctx->stream>>>(per, n_cheb, T, W + (size_t)mu_begin * Ng);
         launched(ctx);
     } else if (n_occ >= 64) {
-        static bool attr = false;
-        if (!attr) {
-            ACP_CUDA(cudaFuncSetAttribute(k_w_nodes<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)nn_big_smem()));
-            attr = true;
-        }
+        func_attr((const void*)k_w_nodes<true>, (int)nn_big_smem());
         k_w_nodes<true><<<dim3(cdiv(Ng, GB_BM), cdiv(cnt, GB_BN)), 256, nn_big_smem(), ctx->stream>>>(
             Ng, n_occ, cnt, n_cheb, Psi, B, ep);
         launched(ctx);

@@ -1143,7 +1143,7 @@ static void trsm_cols(acp_context* ctx, int m, int Ng, int N, const double* A, c
         ACP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
         const int blocks = std::min(sms, cdiv(warps, 32));
         auto launch = [&](auto kern) {
-            ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            func_attr((const void*)kern, 200 * 1024);
             kern<<<blocks, 1024, smem, ctx->stream>>>(m, Ng, N, A, perm, T);
         };
         if (N <= 64) launch(k_trsm_smem<2>);
@@ -1199,7 +1199,7 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
     double* A = ctx->wsd("qr_A", (size_t)m * Ng);
     {
         size_t smem = 32 * (size_t)(n_occ + r) * sizeof(double);
-        ACP_CUDA(cudaFuncSetAttribute(k_kron_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        func_attr((const void*)k_kron_rows, smem);
         k_kron_rows<<<cdiv(Ng, 32), 256, smem, ctx->stream>>>(Ng, n_occ, r, Psi, Gt, A);
         launched(ctx);
     }
@@ -1241,8 +1241,7 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
         auto kern = rkind == 1 ? k_qrcp_reg<8, 2> : k_qrcp_reg<5, 8>;
         const int cpb = cdiv(Ng, rcs);
         const size_t rsm = (3 * (size_t)m + cpb) * sizeof(double) + 2 * (size_t)cpb * sizeof(int);
-        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        func_attr((const void*)kern, rsm, true);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(rcs, 1, 1);
         cfg.blockDim = dim3(512, 1, 1);
@@ -1282,8 +1281,7 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
         // register-resident kernel already launched
     } else if (csq > 0) {
         auto kern = m <= 64 ? k_qrcp_cluster<2> : m <= 128 ? k_qrcp_cluster<4> : k_qrcp_cluster<8>;
-        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        ACP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        func_attr((const void*)kern, 200 * 1024, true);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(csq, 1, 1);
         cfg.blockDim = dim3(1024, 1, 1);
@@ -1339,7 +1337,7 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
                          : kr == 32 ? (const void*)k_qrcp_persistent<false, 32>
                          : kr == 64 ? (const void*)k_qrcp_persistent<false, 64>
                                     : (const void*)k_qrcp_persistent<false, 0>;
-        ACP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        func_attr(fn, smem);
         int occ = 0;
         ACP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
         ACP_REQUIRE(occ >= 1 && G <= occ * dev_sms, "QRCP: cooperative grid does not fit");
