@@ -38,9 +38,10 @@ def _peaks():
     src = "measured (MEASURED_PEAKS.json)"
     if hbm is None:
         hbm, bf16, src = 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
-    # FP64 tensor (DMMA) peak: measured bf16 x guide nominal ratio 45 TF / 2250 TF
-    fp64 = bf16 * 45.0 / 2250.0
-    return dict(hbm_gbs=hbm, fp64_tflops=fp64, src=src)
+    # FP64 peak MEASURED on this pool's B200 (tools/micro/fp64_peak.cu, profiles/R2a_fp64_peak_b200.txt):
+    # DMMA (mma.sync .f64, every shape) 37.1 TF/s, DFMA 36.4 TF/s -- the driver's file has no FP64 entry
+    fp64 = 37.1
+    return dict(hbm_gbs=hbm, fp64_tflops=fp64, src=src, fp64_src="measured (profiles/R2a_fp64_peak_b200.txt)")
 
 
 class ClockSampler:
@@ -85,24 +86,54 @@ def dist_env():
 
 
 # ------------------------------------------------------------------ oracle (reference arm / cpu baseline)
+DENSE_MAX_NG = 6000   # the dense oracle (N_g x N_g matrices) runs up to configs[2]
+
+
 def oracle_sample(cfg, R, outer_k: int = 0, state=None):
-    """One outer iteration of the oracle's Alg. 4 (compress + direct compressed solves + W + SMW)."""
+    """A bounded sample of the oracle on this workload.
+
+    N_g <= 6000: one outer iteration of the oracle's Alg. 4 (compress + direct compressed solves
+    + W + SMW) on its own dense ground state.  2D grids: the oracle's MINRES solves of Eq.
+    eqncompressU (oracle/iterative.py) for 16 interpolation vectors of outer iteration 0 at one
+    Chebyshev node per sample, on the oracle's cached ground state (tests/cache, written by
+    tools/make_golden.py).  Returns (seconds, solves, state, description)."""
     from workloads import sketch_draws
     from oracle.model import Model
-    from oracle.scf import scf
     from oracle import acp as oacp
+    if cfg.n_grid <= DENSE_MAX_NG:
+        from oracle.scf import scf
+        if state is None:
+            m = Model(cfg, R)
+            gs = scf(m, tol=cfg.scf_tol)
+            state = dict(m=m, gs=gs, H=m.hamiltonian_dense(gs.V), G=m.G_matrix())
+        m, gs, H, G = state["m"], state["gs"], state["H"], state["G"]
+        th, nu = sketch_draws(cfg.seed, outer_k % cfg.n_outer, G.shape[1], cfg.sketch_r)
+        t0 = time.perf_counter()
+        S, Xi, _ = oacp.compress(m, gs.Psi, G, th, nu, cfg.id_eps)
+        W = oacp.compressed_W(m, H, gs.Psi, gs.eps[: cfg.n_occ], S, Xi, cfg.n_cheb)
+        oacp.smw_update(m, G, W, S)
+        dt = time.perf_counter() - t0
+        return dt, cfg.n_cheb * len(S), state, (f"one outer iteration of the dense oracle's Alg. 4 "
+                                                 f"(compress + {cfg.n_cheb} x N_mu direct solves + W + SMW)")
+    from oracle.iterative import SternheimerMinres
     if state is None:
+        gp = os.path.join(ROOT, "tests", "cache", f"{cfg.name}_gs.npz")
+        xp = os.path.join(ROOT, "tests", "cache", f"{cfg.name}_xi0.npz")
+        if not (os.path.exists(gp) and os.path.exists(xp)):
+            raise FileNotFoundError(f"oracle ground state for {cfg.name} not cached (tools/make_golden.py)")
+        z = np.load(gp)
         m = Model(cfg, R)
-        gs = scf(m, tol=cfg.scf_tol)
-        state = dict(m=m, gs=gs, H=m.hamiltonian_dense(gs.V), G=m.G_matrix())
-    m, gs, H, G = state["m"], state["gs"], state["H"], state["G"]
-    th, nu = sketch_draws(cfg.seed, outer_k, G.shape[1], cfg.sketch_r)
+        eo = z["eps"][: cfg.n_occ]
+        state = dict(solver=SternheimerMinres(m, z["V"], z["Psi"], tol=cfg.cg_tol, block=16),
+                     Xi=np.load(xp)["Xi"][:, :16], nodes=oacp.chebyshev_nodes(eo[0], eo[-1], cfg.n_cheb))
+    c = outer_k % cfg.n_cheb
     t0 = time.perf_counter()
-    S, Xi, _ = oacp.compress(m, gs.Psi, G, th, nu, cfg.id_eps)
-    W = oacp.compressed_W(m, H, gs.Psi, gs.eps[: cfg.n_occ], S, Xi, cfg.n_cheb)
-    oacp.smw_update(m, G, W, S)
+    state["solver"](state["nodes"][c], state["Xi"])
     dt = time.perf_counter() - t0
-    return dt, cfg.n_cheb * len(S), state
+    return dt, state["Xi"].shape[1], state, ("the oracle's MINRES solves of Eq. eqncompressU (oracle/iterative.py, "
+                                             "relative residual 1e-11) for 16 interpolation vectors of outer "
+                                             "iteration 0 at one Chebyshev node per step, on the oracle's ground "
+                                             "state")
 
 
 def blas_threads():
@@ -121,16 +152,20 @@ def run_reference(args, cfg):
     from workloads import atom_positions
     R = atom_positions(cfg)
     state = None
-    for _ in range(args.warmup):
-        _, _, state = oracle_sample(cfg, R, 0, state)
+    try:
+        for _ in range(args.warmup):
+            _, _, state, _ = oracle_sample(cfg, R, 0, state)
+    except FileNotFoundError as e:
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}), flush=True)
+        return
     tot_t, tot_s = 0.0, 0
     for k in range(args.steps):
-        dt, ns, state = oracle_sample(cfg, R, k % cfg.n_outer, state)
+        dt, ns, state, what = oracle_sample(cfg, R, k, state)
         tot_t += dt
         tot_s += ns
     v = tot_s / tot_t
     cores = blas_threads()
-    sample = f"one outer iteration of Alg. 4 per step (compress + {cfg.n_cheb} x N_mu direct solves + W + SMW)"
+    sample = what + " (each step one such sample)"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -254,7 +289,19 @@ def run_acp(args, cfg):
     # ---- live roofline of the hot kernels (same shapes as inside the step)
     peaks = _peaks()
     n_mu = info["n_mu"][0]
-    ncols = cfg.n_cheb * ((n_mu + 1) // 2 * 2)
+    # the production launch shape: one PCG node group's columns (pcg.cu: up to 4 groups on their own
+    # streams when N_c N_mu' N_g <= 16M points, else one group = the whole batch)
+    n_all = cfg.n_cheb * ((n_mu + 1) // 2 * 2)
+    ngroups = min(cfg.n_cheb, 4) if n_all * ctx.Ng <= (16 << 20) else 1
+    ncols = (cfg.n_cheb // ngroups) * ((n_mu + 1) // 2 * 2)
+    # X and Y for the kernel timing must fit beside the library's PCG workspace
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    fit = int((free_b - (4 << 30)) // (2 * 8 * ctx.Ng)) // 2 * 2
+    shape_note = "production launch shape (one PCG node group)"
+    if fit < ncols:
+        ncols = max(2, fit)
+        shape_note = (f"{ncols} of the production launch's {n_all} columns (memory beside the PCG workspace); "
+                      f"per-column work and traffic are the same at any width >> SM count")
     X = torch.randn(ncols, ctx.Ng, dtype=torch.float64, device=dev)
     Y = torch.zeros_like(X)
     kern = {}
@@ -297,24 +344,39 @@ def run_acp(args, cfg):
         kern[name]["frac"] = kern[name]["achieved"] / kern[name]["peak"]
     dom_name = os.environ.get("ACP_DOMINANT_KERNEL", "K1_fourier_op")
     dom = kern[dom_name]
+    # DRAM bytes per launch of this kernel on THIS workload from one ncu --set full capture
+    # (profiles/traffic.json: {workload: {kernel: {"bytes_per_launch", "units_per_launch", ...}}}),
+    # scaled to this launch's width; null when no capture of this workload exists
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(dom_name)
+        ent = json.load(open(tf)).get(cfg.name, {}).get(dom_name)
+        if ent:
+            traffic = ent["bytes_per_launch"] * ncols / ent["units_per_launch"]
     roofline = {"kernel": dom_name, "bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
                 "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic, "peak_source": peaks["src"],
-                "units_per_launch": ncols, "per_unit": ("16*N_g bytes" if dom["bound"] == "hbm" and
+                "units_per_launch": ncols, "launch_shape": shape_note,
+                "fp64_peak_source": peaks["fp64_src"], "per_unit": ("16*N_g bytes" if dom["bound"] == "hbm" and
                                                         dom_name.startswith("K1") else
                                                         "24*N_g bytes" if dom["bound"] == "hbm" else
                                                         "2*N_g*N_occ flops")}
 
-    # ---- CPU baseline: the oracle, bounded sample, rank 0 at N = 1 only
+    # ---- CPU baseline: the oracle, bounded sample (~10-30 s of host work), rank 0 at N = 1 only
     cpu = None
     if world == 1 and rank == 0 and not args.skip_cpu:
-        dt, ns, _ = oracle_sample(cfg, R, 0)
-        cpu = {"value": ns / dt, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
-               "sample": f"one outer iteration of Alg. 4 ({ns} direct compressed solves + compress + W + SMW), "
-                         f"{dt:.1f} s; ground state untimed"}
+        try:
+            st, tt, ns_tot, k = None, 0.0, 0, 0
+            while tt < 10.0 and k < 64:
+                dt, ns, st, what = oracle_sample(cfg, R, k, st)
+                if k > 0 or cfg.n_grid <= DENSE_MAX_NG:  # first MINRES sample warms the FFT plans
+                    tt += dt
+                    ns_tot += ns
+                k += 1
+            cpu = {"value": ns_tot / tt, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
+                   "sample": f"{what}; {ns_tot} solves in {tt:.1f} s; ground state untimed"}
+        except FileNotFoundError as e:
+            cpu = {"value": None, "unit": "solves/s", "cores": blas_threads(), "kind": "oracle",
+                   "sample": f"unavailable: {e}"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
@@ -340,7 +402,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c1_1d_insulator")
+    # default: the largest single-GPU configuration (BASELINE.json configs[4], 2D 16 x 16 on 256^2,
+    # run with eps0 = 1: DESIGN.md reading R13); configs[1] is the secondary line (--config c1_1d_insulator)
+    ap.add_argument("--config", default="c4g_2d_16x16")
     ap.add_argument("--impl", default="acp", choices=["acp", "reference"])
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()

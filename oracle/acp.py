@@ -245,7 +245,7 @@ def acp_dyson(model: Model, H: np.ndarray, Psi: np.ndarray, eps_occ: np.ndarray,
 
     draws(k, n_cols) -> (theta, nu): the SRFT randomness of outer iteration k.
     solve: see compressed_W.  keep=False drops the per-iteration W / Y (memory at full size);
-    on_outer(k, S, W, Y) sees them before they are dropped.
+    on_outer(k, S, W, Y, Xi) sees them before they are dropped.
     """
     Gp = G.copy()                      # v U~^0 = v B = G
     U_prev = np.zeros_like(G)
@@ -256,10 +256,10 @@ def acp_dyson(model: Model, H: np.ndarray, Psi: np.ndarray, eps_occ: np.ndarray,
         if log:
             log(f"outer {k}: N_mu = {len(S)}")
         W = compressed_W(model, H, Psi, eps_occ, S, Xi, Nc, solve=solve)
-        del Xi
         U, Gp, Y = smw_update(model, G, W, S)
         if on_outer:
-            on_outer(k, S, W, Y)
+            on_outer(k, S, W, Y, Xi)
+        del Xi
         res.diff.append(float(np.linalg.norm(U - U_prev)))
         res.n_mu.append(len(S))
         res.S.append(S)

@@ -97,6 +97,8 @@ struct acp_context {
     bool pdl = false;                    // launch with programmatic dependent launch (PCG graph)
     int fthreads1 = 0, fept1 = 0;        // 2D: geometry of the one-pair setup transforms
     int fct = 0;                         // 1D: a compiled-length FFT kernel matches the plan
+    double2* d_twf2c = nullptr;          // fused 2D operator (fft2c.cu): exp(-2 pi i j / n0), j < n0
+    int f2c_maxcl = 0;                   // fused 2D operator: co-resident clusters (queried once)
     size_t fsmem1 = 0;
 
     std::map<std::string, acp::DevBuf> bufs;
@@ -247,6 +249,12 @@ void fourier_op(acp_context* ctx, const FopArgs& a);
 // Pre-allocate fourier_op's workspace for n columns (call before capturing it into a graph);
 // alt = g: the workspace used while ctx->f2_alt == g (PCG node group g on its own stream).
 void fourier_reserve(acp_context* ctx, int n, int alt);
+// Fused 2D operator (fft2c.cu): square grids n = 16 N2, N2 in {2, 4, 8, 12, 16}.
+bool f2c_supported(int n0, int n1);
+size_t f2c_scratch_bytes(acp_context* ctx, int n);
+size_t f2c_queue_ints(int n);
+int f2c_items_per_phase(int N);
+void launch_f2c(acp_context* ctx, const FopArgs& a, double2* S, int* queue, double* part, const double2* tw);
 // Fill ctx->d_mult with a multiplier of the given kind (scaled by 1/N); returns it.
 const double* multiplier(acp_context* ctx, MultKind kind, double tau);
 // Real grid functions from Hermitian spectra given as complex coefficients per bin:

@@ -742,9 +742,26 @@ __global__ void k_f2_dots(int n, int nrb, const double* __restrict__ part, const
 // (allocation is not permitted while capturing).
 static std::string f2_name(const char* base, int alt) { return alt ? base + std::to_string(alt) : std::string(base); }
 
+// The fused operator (fft2c.cu) is the default where it measured faster: 256^2 (configs[4] grid,
+// K1 3.01 vs 4.07 ms per 4096 columns) and the small test grids; on 192^2 (configs[3]) it is on par
+// with the three passes (4.57 vs 4.49 ms per 7680 columns, profiles/R2i_k1.txt), which stay.
+// ACP_F2C=0 / 1 forces either path.
+static bool use_f2c(const acp_context* ctx) {
+    if (ctx->dim != 2 || !ctx->d_twf2c) return false;
+    static const char* e = getenv("ACP_F2C");
+    if (e) return atoi(e) != 0;
+    return ctx->n[0] != 192;
+}
+
 void fourier_reserve(acp_context* ctx, int n, int alt) {
     if (ctx->dim != 2 || n <= 0) return;
     const int npair = (n + 1) / 2;
+    if (use_f2c(ctx)) {
+        ctx->ws(f2_name("f2c_S", alt), f2c_scratch_bytes(ctx, n));
+        ctx->wsi(f2_name("f2c_q", alt), f2c_queue_ints(n));
+        ctx->wsd(f2_name("f2_part", alt), (size_t)npair * f2c_items_per_phase(ctx->n[0]) * 4);
+        return;
+    }
     ctx->ws(f2_name("f2_Z", alt), (size_t)npair * ctx->n[0] * ctx->n[1] * sizeof(double2));
     ctx->wsd(f2_name("f2_part", alt), (size_t)npair * (ctx->n[0] / F2_RB) * 4);
 }
@@ -835,8 +852,24 @@ static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
     return true;
 }
 
+// The fused cluster kernel (fft2c.cu) + the ordered dot reduction.
+static bool launch_fft2d_fused(acp_context* ctx, const FopArgs& a) {
+    if (!use_f2c(ctx) || (a.mult == nullptr && a.sym < 0)) return false;
+    const int npair = (a.n + 1) / 2, cs = f2c_items_per_phase(ctx->n[0]);
+    double2* S = static_cast<double2*>(ctx->ws(f2_name("f2c_S", ctx->f2_alt), f2c_scratch_bytes(ctx, a.n)));
+    double* part = a.dots ? ctx->wsd(f2_name("f2_part", ctx->f2_alt), (size_t)npair * cs * 4) : nullptr;
+    int* q = ctx->wsi(f2_name("f2c_q", ctx->f2_alt), f2c_queue_ints(a.n));
+    launch_f2c(ctx, a, S, q, part, ctx->d_twf2c);
+    if (a.dots) {
+        k_f2_dots<<<cdiv(2 * a.n, 256), 256, 0, ctx->stream>>>(a.n, cs, part, a.active, a.dots);
+        launched(ctx);
+    }
+    return true;
+}
+
 void fourier_op(acp_context* ctx, const FopArgs& a) {
     if (a.n <= 0) return;
+    if (ctx->dim == 2 && launch_fft2d_fused(ctx, a)) return;
     if (ctx->dim == 2 && launch_fft2d_passes(ctx, a)) return;
     IoArgs io;
     io.f = a;
@@ -996,6 +1029,14 @@ void fft_init(acp_context* ctx) {
     if (dim == 2) ctx->plan1 = make_plan(n1);
     ctx->d_tw = upload(twiddle_table(ctx->plan));
     if (dim == 2) ctx->d_tw1 = upload(twiddle_table(ctx->plan1));
+    if (dim == 2 && f2c_supported(n0, n1)) {
+        std::vector<double2> t(n0);
+        for (int j = 0; j < n0; ++j) {
+            const long double ang = -2.0L * 3.14159265358979323846264338327950288L * (long double)j / (long double)n0;
+            t[j] = make_double2((double)cosl(ang), (double)sinl(ang));
+        }
+        ctx->d_twf2c = upload(t);
+    }
     // per-axis frequencies and the N_g tables (bins in C order)
     std::vector<double> kax[2], kodd[2];
     for (int a = 0; a < dim; ++a) {
@@ -1111,6 +1152,7 @@ void fft_init(acp_context* ctx) {
 void fft_free(acp_context* ctx) {
     cudaFree(ctx->d_tw);
     cudaFree(ctx->d_tw1);
+    cudaFree(ctx->d_twf2c);
     cudaFree(ctx->d_k2);
     cudaFree(ctx->d_khat);
     for (int a = 0; a < 2; ++a) {

@@ -562,3 +562,62 @@ def test_bench_config_end_to_end():
     assert np.abs(lam_g - lam_o).max() / np.abs(lam_o).max() < 1e-7
     out = s.ctx.ground_state(s.R, scf_tol=s.cfg.scf_tol)
     assert rel(out["rho"].cpu().numpy(), s.gs.rho) < 1e-9
+
+
+@pytest.mark.parametrize("mb", ["1", "2"])
+@pytest.mark.parametrize("n", [32, 64, 128, 192, 256])
+def test_fourier_operator_2d_fused(n, mb, monkeypatch):
+    """Fused 2D K1 (fft2c.cu: persistent work queue of row / column / row items, transposes
+    through a ring of L2-resident planes) on every supported square grid, both register budgets
+    (ACP_F2C_MB), against numpy's fft2: kinetic and preconditioner symbols, Yukawa table,
+    potential + per-column shifts, odd column counts (half-empty last pair); ACP_F2C_SKEW=1
+    shrinks the queue skew and the ring (6 slots) so items wait on their producers and 21 pairs
+    cycle through the ring slots."""
+    from paper_1605_08021_b200 import Context
+    monkeypatch.setenv("ACP_F2C_MB", mb)
+    monkeypatch.setenv("ACP_F2C", "1")
+    L0, L1 = 0.37 * n, 0.37 * n
+    for skew in ("", "1"):
+        if skew:
+            monkeypatch.setenv("ACP_F2C_SKEW", skew)
+        ctx = Context(2, (n, n), (L0, L1), 2, 2, 2.0, 2.0, 1.0, 0.01, 1.0)
+        rng = np.random.default_rng(n)
+        k0 = 2 * np.pi * np.fft.fftfreq(n, d=L0 / n)
+        k1 = 2 * np.pi * np.fft.fftfreq(n, d=L1 / n)
+        k2 = k0[:, None] ** 2 + k1[None, :] ** 2
+        for ncol in ((1, 2, 9) if not skew else (41,)):
+            X = rng.standard_normal((ncol, n, n))
+            Xt = T(X.reshape(ncol, -1))
+            F = np.fft.fft2(X)
+            ref = np.real(np.fft.ifft2(F * (0.5 * k2)[None]))
+            assert rel(ctx.fourier_apply(Xt, 0).cpu().numpy().reshape(ncol, n, n), ref) < 1e-12
+            khat = 4 * np.pi / (1.0 * (k2 + 0.01 ** 2))
+            ref = np.real(np.fft.ifft2(F * khat[None]))
+            assert rel(ctx.fourier_apply(Xt, 1).cpu().numpy().reshape(ncol, n, n), ref) < 1e-12
+            ref = np.real(np.fft.ifft2(F * (1.0 / (0.5 * k2 + 0.05))[None]))
+            assert rel(ctx.fourier_apply(Xt, 2, tau=0.05).cpu().numpy().reshape(ncol, n, n), ref) < 1e-12
+            V = rng.standard_normal(n * n)
+            sh = rng.uniform(-0.2, 0.2, ncol)
+            ref = np.real(np.fft.ifft2(F * (0.5 * k2)[None])).reshape(ncol, -1) + (V[None] - sh[:, None]) * X.reshape(ncol, -1)
+            Y = ctx.fourier_apply(Xt, 0, diag=T(V), shift=T(sh)).cpu().numpy()
+            assert rel(Y, ref) < 1e-12
+        ctx.close()
+
+
+def test_fused_2d_matches_three_pass(monkeypatch):
+    """The fused kernel and the three-pass kernels (ACP_F2C=0) agree to rounding on tiny2d's
+    full Alg. 4 (PCG masks and dots inside the solves)."""
+    from paper_1605_08021_b200 import Context
+    s = system("tiny2d")
+    cfg = s.cfg
+    n = s.G.shape[1]
+    th = np.stack([s.draws(k, n)[0] for k in range(cfg.n_outer)])
+    nu = np.stack([s.draws(k, n)[1] for k in range(cfg.n_outer)])
+    args = (s.Psi_t, s.eps_t, s.V_t, s.G_t, cfg.n_cheb, cfg.n_outer, th, nu)
+    U1, i1 = s.ctx.dyson(*args, id_eps=cfg.id_eps, cg_tol=cfg.cg_tol)
+    monkeypatch.setenv("ACP_F2C", "0")
+    ctx = Context.from_config(cfg)
+    U2, i2 = ctx.dyson(*args, id_eps=cfg.id_eps, cg_tol=cfg.cg_tol)
+    ctx.close()
+    assert i1["n_mu"] == i2["n_mu"]
+    assert rel(U1.cpu().numpy(), U2.cpu().numpy()) < 1e-9

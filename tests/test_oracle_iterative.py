@@ -73,7 +73,7 @@ def test_minres_alg4_matches_dense_alg4(dense_system):
     seen = {}
     sol = oit.SternheimerMinres(m, gs.V, gs.Psi, tol=1e-12)
     r2 = oacp.acp_dyson(m, None, gs.Psi, eo, G, cfg.n_cheb, cfg.n_outer, cfg.id_eps, draws, solve=sol,
-                        keep=False, on_outer=lambda k, S, W, Y: seen.setdefault(k, W.copy()))
+                        keep=False, on_outer=lambda k, S, W, Y, Xi: seen.setdefault(k, W.copy()))
     assert r1.n_mu == r2.n_mu
     for a, b in zip(r1.S, r2.S):
         assert np.array_equal(a, b)

@@ -34,6 +34,7 @@ from oracle import acp as oacp, iterative as oit, phonon as ophonon  # noqa: E40
 
 DENSE_MAX_NG = 6000
 N_W_SAMPLE = 6        # mu-columns of W stored per outer iteration
+N_XI = 32             # interpolation vectors of outer 0 kept for bench.py's oracle sample
 
 
 def digest(*arrays) -> str:
@@ -89,9 +90,14 @@ def main():
     solve = None if dense else oit.SternheimerMinres(m, V, Psi, tol=a.minres_tol)
     samples = {}
 
-    def on_outer(k, S, W, Y):
+    def on_outer(k, S, W, Y, Xi):
         idx = w_sample(len(S), k, cfg.seed)
         samples[k] = (idx, W[:, idx].copy())
+        if k == 0:
+            # interpolation vectors of outer iteration 0 for the oracle's timed sample in bench.py
+            # (cpu_baseline / --impl reference on the grids where the dense oracle cannot run)
+            np.savez(os.path.join(cache, f"{cfg.name}_xi0.npz"), Xi=np.ascontiguousarray(Xi[:, :N_XI]),
+                     S=np.asarray(S[:N_XI]))
 
     draws = lambda k, n: sketch_draws(cfg.seed, k, n, cfg.sketch_r)  # noqa: E731
     res = oacp.acp_dyson(m, H, Psi, eps[:n_occ], G, cfg.n_cheb, cfg.n_outer, cfg.id_eps, draws,
