@@ -122,6 +122,29 @@ int acp_compress(acp_context* ctx, const double* d_Psi, const double* d_Gp, int 
                  double id_eps, int n_mu_fixed, int n_mu_max,
                  int* d_S, double* d_Xi, int* h_n_mu);
 
+/* 2'. Sharded compression -- Alg. 2 steps 1-4 with the N_g columns of M~^T
+ *    split across ranks (one process per GPU; the multi-GPU driver paper_1605_08021_b200/parallel.py).
+ *    The pivots, N_mu and Xi equal acp_compress's (same greedy rule: largest remaining column
+ *    norm, exact norms, lowest position on ties; stop at |R~_jj| < id_eps |R~_11|).
+ *  acp_qrs_begin: sketch G~ = G' Omega and the Kronecker rows of this rank's grid points
+ *    [col_begin, col_end) (workspace); h_m receives the sketch height m = N_occ * 2 r_half.
+ *    Arguments as acp_compress.
+ *  acp_qrs_step(s = 0, 1, ...): one pivot step.  s > 0 first applies the winner of step s-1 taken
+ *    from d_recv (world candidates back to back, m + 3 doubles each: norm^2 (-1 = none),
+ *    position, grid index, the column's m current rows); then this rank's best remaining column
+ *    is written to d_send (m + 3 doubles).  The caller all-gathers d_send into d_recv before the
+ *    next step.  Once the factorisation stopped, steps are no-ops (all ranks decide identically).
+ *  acp_qrs_status: (synchronising) stopped flag and N_mu so far.
+ *  acp_qrs_finish: after the stop: d_S (N_mu int32, pivot order, every rank) and this rank's rows
+ *    of Xi, d_XiT[(a - col_begin) * N_mu + mu] = Xi(a, mu) for a in [col_begin, col_end).
+ *  Device pointers d_*, host h_*.  ACP_ERR_INVALID on bad sizes / call order.                   */
+int acp_qrs_begin(acp_context* ctx, const double* d_Psi, const double* d_Gp, int n_cols,
+                  const double* h_theta, const int* h_nu, int r_half, int col_begin, int col_end,
+                  int n_mu_fixed, int n_mu_max, int* h_m);
+int acp_qrs_step(acp_context* ctx, int s, const double* d_recv, int world, double id_eps, double* d_send);
+int acp_qrs_status(acp_context* ctx, int* h_stopped, int* h_n_mu);
+int acp_qrs_finish(acp_context* ctx, int* d_S, double* d_XiT, int* h_n_mu);
+
 /* ------------------------------------------------------------------------ */
 /* 3. Compressed chi0, Alg. 3 steps 2-3.
  *    Solves Q(eps~_c - H)Q zeta~_{c mu} = Q xi_mu (Eq. eqncompressU) for the

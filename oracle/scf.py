@@ -47,12 +47,13 @@ def density(model: Model, Psi: np.ndarray) -> np.ndarray:
 
 def scf(model: Model, tol: float = 1e-12, max_iter: int = 400, n_extra: int = 4,
         rho0: np.ndarray | None = None, history: int = 12, beta: float = 0.5,
-        kerker_k0: float = 0.5, verbose: bool = False, eigensolver=None) -> GroundState:
+        kerker_k0: float = 0.5, verbose: bool = False, eigensolver=None, checkpoint=None) -> GroundState:
     """Self-consistent field iteration to ||rho_out - rho_in|| / ||rho_in|| <= tol.
 
     eigensolver(model, V, nb, X0, scf_res) -> (eps, Psi) replaces the dense diagonalisation (the
     matrix-free LOBPCG of oracle.iterative); X0 = the previous orbitals or None,
-    scf_res = the previous SCF residual (inf at first), which sets how tightly it must solve."""
+    scf_res = the previous SCF residual (inf at first), which sets how tightly it must solve.
+    checkpoint(it, rho) is called every iteration (long runs save rho to resume from via rho0)."""
     m = model.pseudocharge()
     if rho0 is None:
         rho = np.clip(-m, 0.0, None)
@@ -79,7 +80,9 @@ def scf(model: Model, tol: float = 1e-12, max_iter: int = 400, n_extra: int = 4,
         res = rho_out - rho
         err = float(np.linalg.norm(res) / np.linalg.norm(rho))
         if verbose:
-            print(f"scf {it:4d}  res {err:.3e}  gap {eps[model.n_occ] - eps[model.n_occ - 1]:.6f}")
+            print(f"scf {it:4d}  res {err:.3e}  gap {eps[model.n_occ] - eps[model.n_occ - 1]:.6f}", flush=True)
+        if checkpoint:
+            checkpoint(it, rho)
         if err <= tol:
             return GroundState(Psi=Psi[:, : model.n_occ].copy(), eps=eps, rho=rho_out, V=V,
                                n_iter=it, residual=err)

@@ -63,6 +63,11 @@ _sig = {
     "acp_perturbations": [_V, _dp, _V],
     "acp_compress": [_V, _V, _V, ctypes.c_int, _dp, _ip, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                      ctypes.c_int, _V, _V, _ip],
+    "acp_qrs_begin": [_V, _V, _V, ctypes.c_int, _dp, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                      ctypes.c_int, _ip],
+    "acp_qrs_step": [_V, ctypes.c_int, _V, ctypes.c_int, ctypes.c_double, _V],
+    "acp_qrs_status": [_V, _ip, _ip],
+    "acp_qrs_finish": [_V, _V, _V, _ip],
     "acp_apply_chi0": [_V, _V, _V, _V, _V, _V, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                        ctypes.c_double, ctypes.c_int, _V, _dp],
     "acp_dyson": [_V, _V, _V, _V, _V, ctypes.POINTER(acp_dyson_opts), _dp, _ip, _V, _dp],
@@ -231,6 +236,44 @@ class Context:
         n = nm.value
         return S[:n].clone(), Xi[:n].clone(), n
 
+    # -- 2'. sharded compression (multi-GPU driver: parallel.compress_sharded) ----
+    def qrs_begin(self, Psi, Gp, theta, nu, col_begin, col_end, n_mu_fixed=0, n_mu_max=None):
+        self._pre()
+        _chk("Psi", Psi, self.device, shape=(self.n_occ, self.Ng))
+        _chk("Gp", Gp, self.device, shape=(None, self.Ng))
+        n_cols = Gp.shape[0]
+        th, thp = _host(theta)
+        nuh, nup = _host(nu, np.int32)
+        if th.size != n_cols:
+            raise AcpError(f"theta: expected {n_cols} draws, got {th.size}")
+        if n_mu_max is None:
+            n_mu_max = min(self.n_occ * 2 * len(nuh), self.Ng)
+        m = ctypes.c_int(0)
+        self._check(_lib.acp_qrs_begin(self._h, _ptr(Psi), _ptr(Gp), n_cols, thp, nup, len(nuh), col_begin, col_end,
+                                       n_mu_fixed, n_mu_max, ctypes.byref(m)), "acp_qrs_begin")
+        self._qrs = (col_begin, col_end, n_mu_max)
+        return m.value
+
+    def qrs_step(self, s: int, recv, world: int, id_eps: float, send):
+        _chk("recv", recv, self.device)
+        _chk("send", send, self.device)
+        self._check(_lib.acp_qrs_step(self._h, s, _ptr(recv), world, id_eps, _ptr(send)), "acp_qrs_step")
+
+    def qrs_status(self):
+        st, n = ctypes.c_int(0), ctypes.c_int(0)
+        self._check(_lib.acp_qrs_status(self._h, ctypes.byref(st), ctypes.byref(n)), "acp_qrs_status")
+        return bool(st.value), n.value
+
+    def qrs_finish(self):
+        """-> (S (N_mu,) int32, XiT (col_end - col_begin, N_mu): this rank's rows of Xi, N_mu)."""
+        b, e, n_mu_max = self._qrs
+        S = self._empty(n_mu_max, dtype=torch.int32)
+        XiT = self._empty(max(e - b, 1) * n_mu_max)
+        n = ctypes.c_int(0)
+        self._check(_lib.acp_qrs_finish(self._h, _ptr(S), _ptr(XiT), ctypes.byref(n)), "acp_qrs_finish")
+        N = n.value
+        return S[:N].clone(), XiT[: (e - b) * N].view(e - b, N), N
+
     # -- 3. compressed chi0 ----------------------------------------------
     def apply_chi0(self, Psi, eps, V, S, Xi, n_cheb, cg_tol=1e-11, max_iter=2000, mu_range=None, W=None):
         self._pre()
@@ -322,6 +365,13 @@ class Context:
         return D.T.copy(), lam  # column-major -> row-major (D is symmetric anyway)
 
     # -- streams / timing -------------------------------------------------
+    def stream_handle(self) -> int:
+        """The raw cudaStream_t the library launches on (to restore after a temporary switch)."""
+        return int(_lib.acp_get_stream(self._h) or 0)
+
+    def set_stream_handle(self, handle: int):
+        self._check(_lib.acp_set_stream(self._h, ctypes.c_void_p(handle) if handle else None), "acp_set_stream")
+
     def set_stream(self, stream: Optional["torch.cuda.Stream"]):
         """Launch on `stream` (a non-default torch stream, so graphs can be captured)."""
         self._check(_lib.acp_set_stream(self._h, None if stream is None else ctypes.c_void_p(stream.cuda_stream)),

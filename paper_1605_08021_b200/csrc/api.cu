@@ -153,6 +153,41 @@ int acp_compress(acp_context* ctx, const double* d_Psi, const double* d_Gp, int 
     });
 }
 
+int acp_qrs_begin(acp_context* ctx, const double* d_Psi, const double* d_Gp, int n_cols, const double* h_theta,
+                  const int* h_nu, int r_half, int col_begin, int col_end, int n_mu_fixed, int n_mu_max,
+                  int* h_m) {
+    if (!ctx || !d_Psi || !d_Gp || !h_theta || !h_nu || !h_m) return ACP_ERR_INVALID;
+    if (n_cols < 1 || r_half < 1 || r_half > n_cols || n_mu_max < 1) return fail(ctx, ACP_ERR_INVALID, "bad sizes");
+    if (col_begin < 0 || col_end < col_begin || col_end > ctx->Ng) return fail(ctx, ACP_ERR_INVALID, "bad column range");
+    for (int q = 0; q < r_half; ++q)
+        if (h_nu[q] < 1 || h_nu[q] > n_cols) return fail(ctx, ACP_ERR_INVALID, "nu out of range 1..n_cols");
+    return guarded(ctx, [&] {
+        *h_m = acp::qrs_begin(ctx, d_Psi, d_Gp, n_cols, h_theta, h_nu, r_half, col_begin, col_end, n_mu_fixed,
+                              n_mu_max);
+    });
+}
+
+int acp_qrs_step(acp_context* ctx, int s, const double* d_recv, int world, double id_eps, double* d_send) {
+    if (!ctx || !d_recv || !d_send || world < 1 || s < 0) return ACP_ERR_INVALID;
+    if (ctx->qrs_m <= 0) return fail(ctx, ACP_ERR_INVALID, "acp_qrs_step before acp_qrs_begin");
+    return guarded(ctx, [&] { acp::qrs_step(ctx, s, d_recv, world, id_eps, d_send); });
+}
+
+int acp_qrs_status(acp_context* ctx, int* h_stopped, int* h_n_mu) {
+    if (!ctx || !h_stopped || !h_n_mu) return ACP_ERR_INVALID;
+    if (ctx->qrs_m <= 0) return fail(ctx, ACP_ERR_INVALID, "acp_qrs_status before acp_qrs_begin");
+    return guarded(ctx, [&] { acp::qrs_status(ctx, h_stopped, h_n_mu); });
+}
+
+int acp_qrs_finish(acp_context* ctx, int* d_S, double* d_XiT, int* h_n_mu) {
+    if (!ctx || !d_S || !d_XiT || !h_n_mu) return ACP_ERR_INVALID;
+    if (ctx->qrs_m <= 0) return fail(ctx, ACP_ERR_INVALID, "acp_qrs_finish before acp_qrs_begin");
+    return guarded(ctx, [&] {
+        *h_n_mu = acp::qrs_finish(ctx, d_S, d_XiT);
+        acp::sync(ctx);
+    });
+}
+
 int acp_apply_chi0(acp_context* ctx, const double* d_Psi, const double* d_eps, const double* d_V, const int* d_S,
                    const double* d_Xi, int n_mu, int mu_begin, int mu_end, int n_cheb, double cg_tol, int max_iter,
                    double* d_W, double* h_info) {

@@ -98,7 +98,9 @@ struct acp_context {
     int fthreads1 = 0, fept1 = 0;        // 2D: geometry of the one-pair setup transforms
     int fct = 0;                         // 1D: a compiled-length FFT kernel matches the plan
     double2* d_twf2c = nullptr;          // fused 2D operator (fft2c.cu): exp(-2 pi i j / n0), j < n0
-    int f2c_maxcl = 0;                   // fused 2D operator: co-resident clusters (queried once)
+    int f2c_maxcl = 0;                   // fused 2D operator: resident CTAs (queried once)
+    // sharded QRCP (qrcp.cu, acp_qrs_*): this rank's column block and the factorisation sizes
+    int qrs_m = 0, qrs_kmax = 0, qrs_col0 = 0, qrs_nloc = 0, qrs_fixed = 0;
     size_t fsmem1 = 0;
 
     std::map<std::string, acp::DevBuf> bufs;
@@ -307,6 +309,12 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols,
 // ---- dense.cu -----------------------------------------------------------
 // Solve A X = B in place (A: n x n col-major, B: n x nrhs col-major), partial pivoting.
 void lu_solve(acp_context* ctx, double* A, int n, double* B, int nrhs);
+// sharded QRCP (one pivot step per launch; the host all-gathers the candidates between steps)
+int qrs_begin(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, const double* h_theta,
+              const int* h_nu, int r_half, int col_begin, int col_end, int n_fixed, int n_mu_max);
+void qrs_step(acp_context* ctx, int s, const double* recv, int world, double id_eps, double* send);
+void qrs_status(acp_context* ctx, int* stop, int* N);
+int qrs_finish(acp_context* ctx, int* S, double* XiT);
 // Same for [A | B] stored as ONE n x (n + nrhs) column-major array (multi-kernel blocked LU, any n).
 void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs);
 // U X = B for upper-triangular U stored as the first n columns of AB (n x (n + nrhs), ld n).

@@ -1360,4 +1360,361 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
     return N;
 }
 
+
+// ============================================================================ sharded QRCP
+// Alg. 2 steps 2-3 with the N_g columns of M~^T split over ranks (one process
+// per GPU): rank r owns grid points [col0, col0 + nloc).  One pivot step per launch:
+//   (a) s > 0: every CTA selects the winner of step s-1 from the all-gathered candidates (largest
+//       norm^2, lowest position on ties -- the same rule as the one-rank kernels), builds the
+//       Householder vector from the winner's published column, records R11(:, s-1), swaps
+//       positions s-1 <-> the winner's old position, updates the owned columns (exact norms);
+//   (b) the rank's best remaining column (norm^2, position, index, all m rows) goes to `send`.
+// The host all-gathers `send` (NCCL) into `recv` between launches.  The stop rule is decided
+// identically by every CTA of every rank from the gathered data; after it, launches are no-ops.
+struct QrsState {
+    int stop;      // 1 once the rank threshold (or kmax) ended the factorisation
+    int N;         // N_mu when stopped
+    double r11;    // |R~_11|
+};
+
+__global__ void k_qrs_init(int m, int nloc, int col0, int Ng, int n_occ, int r, const double* __restrict__ Psi,
+                           const double* __restrict__ Gt, double* __restrict__ A, int* __restrict__ pos,
+                           int* __restrict__ dn, double* __restrict__ n2) {
+    // one warp per owned column: its Kronecker row psi_i(a) G~(a, q) (row i + q n_occ) and norm^2
+    const int lane = threadIdx.x & 31;
+    const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (lc >= nloc) return;
+    const int a = col0 + lc;
+    double* c = A + (size_t)lc * m;
+    double s = 0.0;
+    for (int e = lane; e < m; e += 32) {
+        const int i = e % n_occ, q = e / n_occ;
+        const double v = Psi[(size_t)i * Ng + a] * Gt[(size_t)q * Ng + a];
+        c[e] = v;
+        s += v * v;
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        n2[lc] = s;
+        pos[lc] = a;
+        dn[lc] = 0;
+    }
+}
+
+template <int KR>
+__global__ void __launch_bounds__(256) k_qrs_step(int m, int nloc, int col0, double* __restrict__ A, int s, int kmax,
+                                                  const double* __restrict__ recv, int world, int stride, double eps,
+                                                  int fixed, int* __restrict__ pos, int* __restrict__ dn,
+                                                  double* __restrict__ n2, QrSlot* __restrict__ slots,
+                                                  double* __restrict__ send, double* __restrict__ R11, int ldr,
+                                                  int* __restrict__ piv, double* __restrict__ rdiag,
+                                                  QrsState* __restrict__ st) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double qsm[];
+    __shared__ double red_d[32];
+    __shared__ int red_i[32];
+    __shared__ int red_j[32];
+    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+    const int lane = tid & 31, warp = uniform_warp(), nwarp = blockDim.x >> 5;
+    if (__ldcg(&st->stop)) return;  // set only by earlier launches: uniform
+    const int cpb = (nloc + G - 1) / G;
+    const int c0 = b * cpb;
+    const int nc = max(0, min(nloc, c0 + cpb) - c0);
+    double* v = qsm;
+    if (s > 0) {
+        const int j = s - 1;
+        // ---- winner of step j among the gathered candidates (identical in every CTA and rank)
+        double bn = -2.0;
+        int bp = 1 << 30, bw = -1;
+        for (int w = 0; w < world; ++w) {
+            const double wn = recv[(size_t)w * stride];
+            const int wp = (int)recv[(size_t)w * stride + 1];
+            if (wn >= 0.0 && (wn > bn || (wn == bn && wp < bp))) {
+                bn = wn;
+                bp = wp;
+                bw = w;
+            }
+        }
+        const double rjj = bw >= 0 ? sqrt(fmax(bn, 0.0)) : 0.0;
+        const double r11 = j == 0 ? rjj : __ldcg(&st->r11);
+        if (bw < 0 || rjj == 0.0 || (fixed <= 0 && rjj < eps * r11)) {
+            if (b == 0 && tid == 0) {
+                st->stop = 1;
+                st->N = j;
+            }
+            return;
+        }
+        const double* x = recv + (size_t)bw * stride + 3;
+        const int cw = (int)recv[(size_t)bw * stride + 2];
+        // ---- Householder vector from the published copy of the winner column
+        double sx = 0.0;
+        for (int i = j + tid; i < m; i += blockDim.x) {
+            const double xi = x[i];
+            v[i] = xi;
+            sx += xi * xi;
+        }
+        for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        if (lane == 0) red_d[warp] = sx;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nwarp; ++w) t += red_d[w];
+            red_d[0] = t;
+        }
+        __syncthreads();
+        const double xn2 = red_d[0];
+        const double xn = sqrt(xn2);
+        const double x0 = v[j];
+        const double alpha = (x0 >= 0.0) ? -xn : xn;
+        const double v0 = x0 - alpha;
+        const double tau = 2.0 / (xn2 - x0 * x0 + v0 * v0);
+        __syncthreads();
+        if (tid == 0) v[j] = v0;
+        if (b == 0) {
+            for (int i = tid; i < j; i += blockDim.x) R11[(size_t)j * ldr + i] = x[i];
+            if (tid == 0) {
+                R11[(size_t)j * ldr + j] = alpha;
+                piv[j] = cw;
+                rdiag[j] = xn;
+                if (j == 0) st->r11 = rjj;
+            }
+        }
+        // ---- position bookkeeping (swap of positions j and bp) for the owned columns
+        for (int lc = tid; lc < nc; lc += blockDim.x) {
+            const int g = c0 + lc;
+            if (col0 + g == cw) {
+                pos[g] = j;
+                dn[g] = 1;
+            } else if (!dn[g] && pos[g] == j) {
+                pos[g] = bp;
+            }
+        }
+        __syncthreads();
+        auto colp = [&](int lc) -> double* { return A + (size_t)(c0 + lc) * m; };
+        if constexpr (KR == 32)
+            qr_update_cols_warp<32>(colp, warp, nc, col0 + c0, cw, j, m, alpha, tau, v, dn + c0, n2 + c0);
+        else if constexpr (KR == 64)
+            qr_update_cols_warp1<64>(colp, warp, nc, col0 + c0, cw, j, m, alpha, tau, v, dn + c0, n2 + c0);
+        else
+            qr_update_cols_chunked2<16>(colp, warp, nc, col0 + c0, cw, j, m, alpha, tau, v, dn + c0, n2 + c0);
+        __threadfence();
+        grid.sync();
+    }
+    if (s >= kmax) {
+        if (b == 0 && tid == 0) {
+            st->stop = 1;
+            st->N = s;
+        }
+        return;
+    }
+    // ---- (b) this CTA's best remaining column, then the rank's best (CTA 0) -> send
+    if (warp == 0) {
+        double bn = -1.0;
+        int bp = 1 << 30, bl = -1;
+        for (int lc = lane; lc < nc; lc += 32) {
+            if (dn[c0 + lc]) continue;
+            const double xv = __ldcg(&n2[c0 + lc]);
+            const int pv = pos[c0 + lc];
+            if (xv > bn || (xv == bn && pv < bp)) {
+                bn = xv;
+                bp = pv;
+                bl = lc;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+            const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+            if (on > bn || (on == bn && op < bp)) {
+                bn = on;
+                bp = op;
+                bl = ol;
+            }
+        }
+        if (lane == 0) {
+            QrSlot sl;
+            sl.n2 = bn;
+            sl.pos = bp;
+            sl.col = bl >= 0 ? c0 + bl : -1;  // local column index
+            slots[b] = sl;
+        }
+    }
+    __threadfence();
+    grid.sync();
+    if (b != 0) return;
+    double bn = -1.0;
+    int bp = 1 << 30, bc = -1;
+    for (int q = tid; q < G; q += blockDim.x) {
+        const double sn = __ldcg(&slots[q].n2);
+        const int sp = __ldcg(&slots[q].pos);
+        const int sc = __ldcg(&slots[q].col);
+        if (sc >= 0 && (sn > bn || (sn == bn && sp < bp))) {
+            bn = sn;
+            bp = sp;
+            bc = sc;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (oc >= 0 && (bc < 0 || on > bn || (on == bn && op < bp))) {
+            bn = on;
+            bp = op;
+            bc = oc;
+        }
+    }
+    if (lane == 0) {
+        red_d[warp] = bn;
+        red_i[warp] = bp;
+        red_j[warp] = bc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < nwarp; ++w)
+            if (red_j[w] >= 0 && (red_j[0] < 0 || red_d[w] > red_d[0] || (red_d[w] == red_d[0] && red_i[w] < red_i[0]))) {
+                red_d[0] = red_d[w];
+                red_i[0] = red_i[w];
+                red_j[0] = red_j[w];
+            }
+        send[0] = red_j[0] >= 0 ? red_d[0] : -1.0;
+        send[1] = (double)red_i[0];
+        send[2] = (double)(red_j[0] >= 0 ? col0 + red_j[0] : -1);
+    }
+    __syncthreads();
+    const int lcw = red_j[0];
+    if (lcw >= 0) {
+        const double* c = A + (size_t)lcw * m;
+        for (int i = tid; i < m; i += blockDim.x) send[3 + i] = __ldcg(&c[i]);
+    }
+}
+
+// After the stop: Xi^T rows of the owned grid points, XiT[lc * N + mu] = (R11^{-1} R(0:N, a))_mu for
+// a non-pivot column a = col0 + lc, delta(mu, position) for a pivot.
+__global__ void k_qrs_gather(int m, int nloc, int N, const double* __restrict__ A, const double* __restrict__ R11,
+                             int ldr, double* __restrict__ AB) {
+    // AB = [R11 | R(0:N, owned)] column-major, ld N
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int jc = blockIdx.y + gridDim.y * blockIdx.z;
+    if (i >= N || jc >= N + nloc) return;
+    AB[(size_t)jc * N + i] = jc < N ? (i <= jc ? R11[(size_t)jc * ldr + i] : 0.0) : A[(size_t)(jc - N) * m + i];
+}
+
+__global__ void k_qrs_xi(int nloc, int N, const double* __restrict__ T, const int* __restrict__ pos,
+                         const int* __restrict__ dn, double* __restrict__ XiT) {
+    const int mu = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lc = blockIdx.y + gridDim.y * blockIdx.z;
+    if (mu >= N || lc >= nloc) return;
+    const bool pv = dn[lc] && pos[lc] < N;
+    XiT[(size_t)lc * N + mu] = pv ? (pos[lc] == mu ? 1.0 : 0.0) : T[(size_t)lc * N + mu];
+}
+
+int qrs_begin(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, const double* h_theta,
+              const int* h_nu, int r_half, int col_begin, int col_end, int n_fixed, int n_mu_max) {
+    const int Ng = ctx->Ng, n_occ = ctx->sys.n_occ;
+    ACP_REQUIRE(n_cols >= 1 && r_half >= 1 && r_half <= n_cols, "invalid sketch size");
+    ACP_REQUIRE(0 <= col_begin && col_begin <= col_end && col_end <= Ng, "invalid column range");
+    const int r = 2 * r_half, m = n_occ * r, nloc = col_end - col_begin;
+    double* d_theta = ctx->wsd("qr_theta", n_cols);
+    int* d_nu = ctx->wsi("qr_nu", r_half);
+    ACP_CUDA(cudaMemcpyAsync(d_theta, h_theta, n_cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ACP_CUDA(cudaMemcpyAsync(d_nu, h_nu, r_half * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    double* Om = ctx->wsd("qr_omega", (size_t)n_cols * r);
+    k_srft_omega<<<dim3(cdiv(n_cols, 128), r_half), 128, 0, ctx->stream>>>(n_cols, r_half, d_theta, d_nu, Om);
+    launched(ctx);
+    double* Gt = ctx->wsd("qr_gt", (size_t)Ng * r);
+    gemm_nn(ctx, Ng, n_cols, r, 1.0, Gp, Ng, Om, n_cols, 0.0, Gt, Ng);
+    int kmax = std::min(m, Ng);
+    if (n_fixed > 0) kmax = std::min(kmax, n_fixed);
+    kmax = std::min(kmax, n_mu_max);
+    const int nl = std::max(nloc, 1);
+    double* A = ctx->wsd("qrs_A", (size_t)m * nl);
+    int* pos = ctx->wsi("qrs_pos", nl);
+    int* dn = ctx->wsi("qrs_dn", nl);
+    double* n2 = ctx->wsd("qrs_n2", nl);
+    ctx->wsd("qrs_R11", (size_t)kmax * kmax);
+    ctx->wsi("qrs_piv", kmax);
+    ctx->wsd("qrs_rdiag", kmax);
+    QrsState* st = static_cast<QrsState*>(ctx->ws("qrs_state", sizeof(QrsState)));
+    ACP_CUDA(cudaMemsetAsync(st, 0, sizeof(QrsState), ctx->stream));
+    if (nloc > 0) {
+        k_qrs_init<<<cdiv(nloc, 8), 256, 0, ctx->stream>>>(m, nloc, col_begin, Ng, n_occ, r, Psi, Gt, A, pos, dn, n2);
+        launched(ctx);
+    }
+    ctx->qrs_m = m;
+    ctx->qrs_kmax = kmax;
+    ctx->qrs_col0 = col_begin;
+    ctx->qrs_nloc = nloc;
+    ctx->qrs_fixed = n_fixed;
+    return m;
+}
+
+void qrs_step(acp_context* ctx, int s, const double* recv, int world, double id_eps, double* send) {
+    const int m = ctx->qrs_m, nloc = ctx->qrs_nloc, kmax = ctx->qrs_kmax, col0 = ctx->qrs_col0;
+    double* A = ctx->wsd("qrs_A", (size_t)m * std::max(nloc, 1));
+    int* pos = ctx->wsi("qrs_pos", std::max(nloc, 1));
+    int* dn = ctx->wsi("qrs_dn", std::max(nloc, 1));
+    double* n2 = ctx->wsd("qrs_n2", std::max(nloc, 1));
+    double* R11 = ctx->wsd("qrs_R11", (size_t)kmax * kmax);
+    int* piv = ctx->wsi("qrs_piv", kmax);
+    double* rdiag = ctx->wsd("qrs_rdiag", kmax);
+    QrsState* st = static_cast<QrsState*>(ctx->ws("qrs_state", sizeof(QrsState)));
+    int sms = 148;
+    ACP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    int G = std::max(1, std::min(sms, cdiv(std::max(nloc, 1), 8)));
+    QrSlot* slots = static_cast<QrSlot*>(ctx->ws("qrs_slots", (size_t)sms * sizeof(QrSlot)));
+    const int stride = m + 3;
+    int fixed = ctx->qrs_fixed;
+    double eps = id_eps;
+    int ldr = kmax;
+    const size_t smem = (size_t)m * sizeof(double);
+    const void* fn = m <= 1024 ? (const void*)k_qrs_step<32> : m <= 2048 ? (const void*)k_qrs_step<64>
+                                                                          : (const void*)k_qrs_step<0>;
+    func_attr(fn, smem);
+    int occ = 0;
+    ACP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+    ACP_REQUIRE(occ >= 1, "sharded QRCP: kernel does not fit");
+    G = std::min(G, occ * sms);
+    void* args[] = {(void*)&m, (void*)&nloc, (void*)&col0, (void*)&A, (void*)&s, (void*)&kmax, (void*)&recv,
+                    (void*)&world, (void*)&stride, (void*)&eps, (void*)&fixed, (void*)&pos, (void*)&dn, (void*)&n2,
+                    (void*)&slots, (void*)&send, (void*)&R11, (void*)&ldr, (void*)&piv, (void*)&rdiag, (void*)&st};
+    ACP_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(256), args, smem, ctx->stream));
+    launched(ctx);
+}
+
+void qrs_status(acp_context* ctx, int* stop, int* N) {
+    QrsState* st = static_cast<QrsState*>(ctx->ws("qrs_state", sizeof(QrsState)));
+    QrsState* hp = static_cast<QrsState*>(ctx->pinned);
+    ACP_CUDA(cudaMemcpyAsync(hp, st, sizeof(QrsState), cudaMemcpyDeviceToHost, ctx->stream));
+    ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+    *stop = hp->stop;
+    *N = hp->N;
+}
+
+int qrs_finish(acp_context* ctx, int* S, double* XiT) {
+    int stop = 0, N = 0;
+    qrs_status(ctx, &stop, &N);
+    ACP_REQUIRE(stop, "sharded QRCP: finish before the factorisation stopped");
+    ACP_REQUIRE(N >= 1, "QRCP selected no rows (zero sketch)");
+    const int m = ctx->qrs_m, nloc = ctx->qrs_nloc, kmax = ctx->qrs_kmax;
+    const double* A = ctx->wsd("qrs_A", (size_t)m * std::max(nloc, 1));
+    const int* pos = ctx->wsi("qrs_pos", std::max(nloc, 1));
+    const int* dn = ctx->wsi("qrs_dn", std::max(nloc, 1));
+    const double* R11 = ctx->wsd("qrs_R11", (size_t)kmax * kmax);
+    const int* piv = ctx->wsi("qrs_piv", kmax);
+    ACP_CUDA(cudaMemcpyAsync(S, piv, N * sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (nloc == 0) return N;
+    double* AB = ctx->wsd("qrs_AB", (size_t)N * (N + nloc));
+    const int ncol = N + nloc, gz = cdiv(ncol, 65535);
+    k_qrs_gather<<<dim3(cdiv(N, 128), cdiv(ncol, gz), gz), 128, 0, ctx->stream>>>(m, nloc, N, A, R11, kmax, AB);
+    launched(ctx);
+    upper_solve_blocked(ctx, AB, N, nloc);
+    const int gz2 = cdiv(nloc, 65535);
+    k_qrs_xi<<<dim3(cdiv(N, 128), cdiv(nloc, gz2), gz2), 128, 0, ctx->stream>>>(nloc, N, AB + (size_t)N * N, pos, dn,
+                                                                                 XiT);
+    launched(ctx);
+    return N;
+}
+
 }  // namespace acp

@@ -1,21 +1,27 @@
-"""Multi-GPU layer: Alg. 4 with the compressed Sternheimer right-hand sides sharded
-across ranks (one process per GPU) and W all-gathered over NCCL (NVLink).
+"""Multi-GPU layer: Alg. 4 with the compression AND the compressed Sternheimer right-hand sides
+sharded across ranks (one process per GPU), exchanges over NCCL (NVLink).
 
-PAPER.md:622-628: the N_c x N_mu equations of Eq. eqncompressU are independent,
-so rank r solves the mu-columns [b_r, e_r) for all Chebyshev nodes and produces
-those columns of W (Eq. eqnW).  The only exchange per outer iteration is the
-all-gather of W (N_g x N_mu doubles).  Compression (Alg. 2) and the small SMW
-update (Eq. dyson4) are replicated: they are deterministic functions of
-identical inputs, so every rank holds the same U after each iteration.
-Shard boundaries are even, so column pairs of the FFT kernel -- and therefore
-every per-column result -- are identical to the single-GPU run.
+* Compression (Alg. 2): rank r owns the grid points [a_r, b_r) -- the columns
+  of M~^T.  Each pivot step is one kernel on every rank plus ONE all-gather of the ranks' best
+  remaining columns (m + 3 doubles each); every rank then selects the same winner (largest norm,
+  lowest position on ties), so the pivots and N_mu equal the one-rank factorisation's.  Each rank
+  solves for its own rows of Xi; one all-gather assembles Xi (N_g x N_mu).
+* Sternheimer solves: the N_c x N_mu equations are independent; rank r solves
+  the mu-columns [b_r, e_r) for all Chebyshev nodes and produces those columns of W (Eq. eqnW);
+  one all-gather (straight into the gathered buffer) assembles W.
+* The SMW update (Eq. dyson4) is an N_mu x N_mu solve: replicated (deterministic, same inputs),
+  so every rank holds the same U after each iteration.
+Shard boundaries of W are even, so column pairs of the FFT kernel -- and therefore every
+per-column result -- are identical to the single-GPU run.
 """
 from __future__ import annotations
 
-from typing import Callable, List, Tuple
+from typing import Callable, Tuple
 
 import torch
 import torch.distributed as dist
+
+CHECK_EVERY = 32   # pivot steps between stop-flag reads (later steps are device no-ops)
 
 
 def shard_bounds(n: int, rank: int, world: int) -> Tuple[int, int, int]:
@@ -27,22 +33,80 @@ def shard_bounds(n: int, rank: int, world: int) -> Tuple[int, int, int]:
     return b, e, chunk
 
 
-def allgather_rows(W_local: torch.Tensor, n: int, chunk: int, group=None) -> torch.Tensor:
-    """Gather per-rank row blocks (chunk x N_g, zero padded) into the first n rows."""
+def grid_bounds(Ng: int, rank: int, world: int) -> Tuple[int, int, int]:
+    """Contiguous split of the N_g grid points (columns of M~^T): (begin, end, chunk)."""
+    chunk = -(-Ng // world)
+    b = min(Ng, rank * chunk)
+    e = min(Ng, b + chunk)
+    return b, e, chunk
+
+
+def allgather_rows(W_local: torch.Tensor, n: int, group=None) -> torch.Tensor:
+    """Gather per-rank row blocks (chunk x N_g each, zero padded) straight into one buffer and
+    return its first n rows (a view: the blocks are stored back to back)."""
     world = dist.get_world_size(group)
-    parts: List[torch.Tensor] = [torch.empty_like(W_local) for _ in range(world)]
-    dist.all_gather(parts, W_local, group=group)
-    return torch.cat(parts, dim=0)[:n].contiguous()
+    out = torch.empty((world * W_local.shape[0],) + tuple(W_local.shape[1:]), dtype=W_local.dtype,
+                      device=W_local.device)
+    dist.all_gather_into_tensor(out, W_local.contiguous(), group=group)
+    return out[:n]
+
+
+def compress_sharded(ops, Psi, Gp, theta, nu, id_eps: float, group=None, n_mu_fixed: int = 0):
+    """Alg. 2 with the grid points split across the ranks of `group`.  Returns (S, Xi, N_mu)
+    exactly as ops.compress would: S (N_mu,) int32 in pivot order, Xi (N_mu, N_g)."""
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    Ng = Psi.shape[1]
+    a, b, chunk = grid_bounds(Ng, rank, world)
+    if Psi.is_cuda and hasattr(ops, "set_stream"):
+        # the pivot kernels, the torch ops and the NCCL all-gathers are ordered by running on ONE
+        # non-default stream (a null-stream handle would send the library to its own stream)
+        cur = torch.cuda.current_stream(Psi.device)
+        st = cur if cur.cuda_stream != 0 else torch.cuda.Stream(device=Psi.device)
+        st.wait_stream(cur)
+        prev = ops.stream_handle() if hasattr(ops, "stream_handle") else None
+        with torch.cuda.stream(st):
+            ops.set_stream(st)
+            out = _compress_sharded_loop(ops, Psi, Gp, theta, nu, id_eps, group, n_mu_fixed, a, b, chunk, world)
+        cur.wait_stream(st)
+        if prev is not None:
+            st.synchronize()
+            ops.set_stream_handle(prev)   # the caller's stream choice for the library stays in force
+        return out
+    return _compress_sharded_loop(ops, Psi, Gp, theta, nu, id_eps, group, n_mu_fixed, a, b, chunk, world)
+
+
+def _compress_sharded_loop(ops, Psi, Gp, theta, nu, id_eps, group, n_mu_fixed, a, b, chunk, world):
+    Ng = Psi.shape[1]
+    m = ops.qrs_begin(Psi, Gp, theta, nu, a, b, n_mu_fixed=n_mu_fixed)
+    stride = m + 3
+    send = torch.zeros(stride, dtype=torch.float64, device=Psi.device)
+    recv = torch.zeros(world * stride, dtype=torch.float64, device=Psi.device)
+    s = 0
+    while True:
+        ops.qrs_step(s, recv, world, id_eps, send)
+        if s % CHECK_EVERY == CHECK_EVERY - 1:
+            stopped, _ = ops.qrs_status()
+            if stopped:
+                break
+        dist.all_gather_into_tensor(recv, send, group=group)
+        s += 1
+    S, XiT, N = ops.qrs_finish()
+    # rows of Xi: rank r holds grid points [a_r, b_r); pad to chunk rows, gather, trim, transpose
+    pad = torch.zeros(chunk, N, dtype=XiT.dtype, device=XiT.device)
+    pad[: b - a] = XiT
+    full = allgather_rows(pad, Ng, group)          # (N_g, N_mu)
+    return S, full.t().contiguous(), N
 
 
 def dyson_sharded(ops, Psi, eps, V, G, n_cheb: int, n_outer: int, draws: Callable[[int], tuple],
-                  id_eps: float, cg_tol: float = 1e-11, group=None):
+                  id_eps: float, cg_tol: float = 1e-11, group=None, shard_compress: bool = True):
     """Alg. 4 (PAPER.md:765-795) on `world` ranks.
 
-    `ops` provides compress / apply_chi0 / smw_update with the signatures of
-    paper_1605_08021_b200.acp.Context (a GPU Context in production; tests pass
-    a CPU stand-in to exercise the sharding and gather logic under gloo).
-    Returns (U, info) with U identical on every rank.
+    `ops` provides qrs_* / compress / apply_chi0 / smw_update with the signatures of
+    paper_1605_08021_b200.acp.Context (a GPU Context in production; tests pass a CPU stand-in to
+    exercise the sharding and gather logic under gloo).  Returns (U, info) with U identical on
+    every rank.
     """
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
@@ -51,7 +115,10 @@ def dyson_sharded(ops, Psi, eps, V, G, n_cheb: int, n_outer: int, draws: Callabl
     info = dict(n_mu=[], local_solves=0, shards=[])
     for k in range(n_outer):
         theta, nu = draws(k)
-        S, Xi, n = ops.compress(Psi, Gp, theta, nu, id_eps=id_eps)
+        if shard_compress:
+            S, Xi, n = compress_sharded(ops, Psi, Gp, theta, nu, id_eps, group)
+        else:
+            S, Xi, n = ops.compress(Psi, Gp, theta, nu, id_eps=id_eps)
         b, e, chunk = shard_bounds(n, rank, world)
         W_loc = torch.zeros(chunk, Xi.shape[1], dtype=Xi.dtype, device=Xi.device)
         if e > b:
@@ -59,7 +126,7 @@ def dyson_sharded(ops, Psi, eps, V, G, n_cheb: int, n_outer: int, draws: Callabl
             _, st = ops.apply_chi0(Psi, eps, V, S, Xi, n_cheb, cg_tol=cg_tol, mu_range=(b, e), W=W_full)
             W_loc[: e - b] = W_full[b:e]
             info["local_solves"] += st["n_solved"]
-        W = allgather_rows(W_loc, n, chunk, group)
+        W = allgather_rows(W_loc, n, group)
         U, Gp = ops.smw_update(G, S, W)
         info["n_mu"].append(n)
         info["shards"].append((b, e))

@@ -47,6 +47,91 @@ class OracleOps:
         W[b:e] = torch.from_numpy(np.ascontiguousarray(Wl.T))
         return W, {"n_solved": n_cheb * (e - b)}
 
+    # -- sharded compression: a numpy restatement of the k_qrs_step protocol (qrcp.cu) ----------
+    def qrs_begin(self, Psi, Gp, theta, nu, a, b, n_mu_fixed=0):
+        from oracle import acp as oacp
+        Gt = oacp.srft_sketch(Gp.T.numpy(), theta, nu)
+        Mt = oacp.sketch_matrix(Psi.T.numpy(), Gt)            # (N_g, m)
+        self.qm = Mt.shape[1]
+        self.a, self.b = a, b
+        self.A = np.ascontiguousarray(Mt[a:b].T)              # m x n_loc, owned grid points
+        self.pos = np.arange(a, b)
+        self.dn = np.zeros(b - a, dtype=bool)
+        self.n2 = np.einsum("ij,ij->j", self.A, self.A)
+        self.kmax = min(self.qm, Mt.shape[0]) if n_mu_fixed <= 0 else min(self.qm, Mt.shape[0], n_mu_fixed)
+        self.fixed = n_mu_fixed
+        self.stop, self.N, self.r11 = False, 0, 0.0
+        self.R11 = np.zeros((self.kmax, self.kmax))
+        self.piv = []
+        return self.qm
+
+    def qrs_step(self, s, recv, world, id_eps, send):
+        if self.stop:
+            return
+        m = self.qm
+        if s > 0:
+            j = s - 1
+            cands = recv.numpy().reshape(world, m + 3)
+            best = None
+            for c in cands:
+                if c[0] >= 0 and (best is None or c[0] > best[0] or (c[0] == best[0] and c[1] < best[1])):
+                    best = c
+            rjj = np.sqrt(max(best[0], 0.0)) if best is not None else 0.0
+            r11 = rjj if j == 0 else self.r11
+            if best is None or rjj == 0.0 or (self.fixed <= 0 and rjj < id_eps * r11):
+                self.stop, self.N = True, j
+                return
+            if j == 0:
+                self.r11 = rjj
+            bp, cw, x = int(best[1]), int(best[2]), best[3:]
+            xn = np.linalg.norm(x[j:])
+            alpha = -xn if x[j] >= 0 else xn
+            v = x[j:].copy()
+            v[0] -= alpha
+            tau = 2.0 / (v @ v)
+            self.R11[:j, j] = x[:j]
+            self.R11[j, j] = alpha
+            self.piv.append(cw)
+            for lc in range(self.b - self.a):
+                g = self.a + lc
+                if g == cw:
+                    self.pos[lc], self.dn[lc] = j, True
+                    self.A[j:, lc] = 0.0
+                    self.A[j, lc] = alpha
+                elif not self.dn[lc]:
+                    if self.pos[lc] == j:
+                        self.pos[lc] = bp
+                    c = self.A[j:, lc]
+                    c -= tau * v * (v @ c)
+                    self.n2[lc] = c[1:] @ c[1:]
+        if s >= self.kmax:
+            self.stop, self.N = True, s
+            return
+        live = np.nonzero(~self.dn)[0]
+        out = np.zeros(m + 3)
+        out[0] = -1.0
+        if len(live):
+            order = sorted(live, key=lambda lc: (-self.n2[lc], self.pos[lc]))
+            lc = order[0]
+            out[0], out[1], out[2] = self.n2[lc], self.pos[lc], self.a + lc
+            out[3:] = self.A[:, lc]
+        send.copy_(torch.from_numpy(out))
+
+    def qrs_status(self):
+        return self.stop, self.N
+
+    def qrs_finish(self):
+        import scipy.linalg as sla
+        N = self.N
+        T = sla.solve_triangular(self.R11[:N, :N], self.A[:N, :], lower=False) if self.b > self.a else \
+            np.zeros((N, 0))
+        XiT = T.T.copy()
+        for lc in range(self.b - self.a):
+            if self.dn[lc] and self.pos[lc] < N:
+                XiT[lc] = 0.0
+                XiT[lc, self.pos[lc]] = 1.0
+        return torch.tensor(self.piv[:N], dtype=torch.int32), torch.from_numpy(XiT), N
+
     def smw_update(self, G, S, W):
         from oracle import acp as oacp
         U, Gp, _ = oacp.smw_update(self.m, G.T.numpy(), W.T.numpy(), S.numpy())
@@ -88,6 +173,44 @@ def _free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+def _compress_worker(rank, world, port, out, fixed):
+    from workloads import sketch_draws
+    from paper_1605_08021_b200.parallel import compress_sharded
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        cfg, m, gs = _system()
+        G = torch.from_numpy(np.ascontiguousarray(m.G_matrix().T))
+        Psi = torch.from_numpy(np.ascontiguousarray(gs.Psi.T))
+        th, nu = sketch_draws(cfg.seed, 0, G.shape[0], cfg.sketch_r)
+        S, Xi, n = compress_sharded(OracleOps(m, None), Psi, G, th, nu, cfg.id_eps, n_mu_fixed=fixed)
+        out[rank] = (S.numpy().copy(), Xi.numpy().copy(), n)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,fixed", [(2, 0), (3, 0), (2, 10)])
+def test_compress_sharded_matches_one_rank(world, fixed):
+    """The sharded pivoted QR protocol (parallel.compress_sharded: per-pivot all-gather of the
+    ranks' best columns, replicated winner selection, per-rank rows of Xi) over gloo reproduces the
+    one-rank factorisation of the oracle: identical pivots and N_mu on every
+    rank, Xi to rounding; N_mu by the threshold rule and fixed."""
+    from workloads import sketch_draws
+    from oracle import acp as oacp
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_compress_worker, args=(world, _free_port(), out, fixed), nprocs=world, join=True,
+                       start_method="fork")
+    cfg, m, gs = _system()
+    G = m.G_matrix()
+    th, nu = sketch_draws(cfg.seed, 0, G.shape[1], cfg.sketch_r)
+    S_o, Xi_o, _ = oacp.compress(m, gs.Psi, G, th, nu, cfg.id_eps, n_fixed=fixed or None)
+    for r in range(world):
+        S, Xi, n = out[r]
+        assert n == len(S_o)
+        assert np.array_equal(S, S_o)
+        assert np.abs(Xi.T - Xi_o).max() < 1e-10 * np.abs(Xi_o).max()
 
 
 def test_dyson_sharded_two_ranks_matches_single_process():
