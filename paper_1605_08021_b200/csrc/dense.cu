@@ -381,125 +381,6 @@ void upper_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
 }
 
 // Solve A X = B in place; AB is n x (n + nrhs) column-major ([A | B], ld n).
-// Warp-row panel (R <= 512 rows): warp w owns panel rows [w*RPW, (w+1)*RPW) with lane j holding
-// column j of each of them in registers, so a row operation is one instruction across the warp
-// and a column costs ONE barrier: the lane of column k finds the warp's best row (first max),
-// the warp publishes (|a_ik|, row) and that row into a parity double-buffered slot, the warp
-// owning row k publishes row k; after the barrier every warp selects the same winner (largest
-// magnitude, lowest row on ties), swaps rows k <-> p from the published copies and eliminates its
-// rows (multiplier broadcast from lane k).  Same pivots and per-element operations as k_lu_panel.
-template <int RPW>
-__global__ void __launch_bounds__(512) k_lu_panel_warp(double* __restrict__ AB, int n, int p0, int pw,
-                                                       int* __restrict__ piv, int* __restrict__ status) {
-    extern __shared__ double lsm[];  // staging [32][R + 1] for coalesced load / store
-    __shared__ double cand_v[2][16];
-    __shared__ int cand_i[2][16];
-    __shared__ double cand_row[2][16][32];
-    __shared__ double krow[2][32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    const int R = n - p0, LS = R + 1;
-    for (int e = tid; e < R * pw; e += blockDim.x) {
-        const int jj = e / R, i = e - jj * R;
-        lsm[jj * LS + i] = AB[(size_t)(p0 + jj) * n + p0 + i];
-    }
-    __syncthreads();
-    const int r0 = warp * RPW;
-    double a[RPW];
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-        const int i = r0 + r;
-        a[r] = (i < R && lane < pw) ? lsm[lane * LS + i] : 0.0;
-    }
-    int sing = 0;
-    for (int kk = 0; kk < pw; ++kk) {
-        const int par = kk & 1;
-        double bv = -1.0;
-        int bi = 1 << 30, br = -1;
-        if (lane == kk) {
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                const int i = r0 + r;
-                const double v = fabs(a[r]);
-                if (i >= kk && i < R && v > bv) {
-                    bv = v;
-                    bi = i;
-                    br = r;
-                }
-            }
-        }
-        bv = __shfl_sync(0xffffffffu, bv, kk);
-        bi = __shfl_sync(0xffffffffu, bi, kk);
-        br = __shfl_sync(0xffffffffu, br, kk);
-        if (br >= 0) {
-            double val = 0.0;
-#pragma unroll
-            for (int r = 0; r < RPW; ++r)
-                if (r == br) val = a[r];
-            cand_row[par][warp][lane] = val;
-        }
-        if (lane == 0) {
-            cand_v[par][warp] = bv;
-            cand_i[par][warp] = bi;
-        }
-        if (kk >= r0 && kk < r0 + RPW) {
-            double val = 0.0;
-#pragma unroll
-            for (int r = 0; r < RPW; ++r)
-                if (r0 + r == kk) val = a[r];
-            krow[par][lane] = val;
-        }
-        __syncthreads();
-        double wv = lane < nw ? cand_v[par][lane] : -1.0;
-        int wi = lane < nw ? cand_i[par][lane] : (1 << 30), ww = lane;
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {  // nw <= 16
-            const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
-            const int ow = __shfl_xor_sync(0xffffffffu, ww, o);
-            if (ov > wv || (ov == wv && oi < wi)) {
-                wv = ov;
-                wi = oi;
-                ww = ow;
-            }
-        }
-        wv = __shfl_sync(0xffffffffu, wv, 0);  // lanes 16..31 reduced only their padding
-        wi = __shfl_sync(0xffffffffu, wi, 0);
-        ww = __shfl_sync(0xffffffffu, ww, 0);
-        const bool zero = !(wv > 0.0);
-        const int pr = zero ? kk : wi;
-        if (tid == 0) piv[p0 + kk] = p0 + pr;
-        sing |= zero;
-        const double kj = krow[par][lane];
-        const double pj = zero ? kj : cand_row[par][ww][lane];
-        const double pk = __shfl_sync(0xffffffffu, pj, kk);
-        const double rp = zero ? 0.0 : 1.0 / pk;
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-            const int i = r0 + r;
-            if (pr != kk) {
-                if (i == kk) a[r] = pj;
-                else if (i == pr) a[r] = kj;
-            }
-            if (i > kk && i < R) {
-                const double l = __shfl_sync(0xffffffffu, a[r], kk) * rp;
-                if (lane == kk) a[r] = l;
-                else if (lane > kk) a[r] -= l * pj;
-            }
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-        const int i = r0 + r;
-        if (i < R && lane < pw) lsm[lane * LS + i] = a[r];
-    }
-    __syncthreads();
-    for (int e = tid; e < R * pw; e += blockDim.x) {
-        const int jj = e / R, i = e - jj * R;
-        AB[(size_t)(p0 + jj) * n + p0 + i] = lsm[jj * LS + i];
-    }
-    if (tid == 0 && sing) *status = 1;
-}
 
 void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
     const int ntot = n + nrhs;
@@ -513,17 +394,7 @@ void lu_solve_blocked(acp_context* ctx, double* AB, int n, int nrhs) {
         const int R = n - p0;
         const size_t pbytes = (size_t)R * pw * sizeof(double);
         const int use_smem = pbytes <= 200 * 1024;
-        if (R <= 512 && getenv("ACP_LU_WARP_PANEL")) {  // opt-in: measured no faster end to end
-            for (const void* f : {(const void*)k_lu_panel_warp<8>, (const void*)k_lu_panel_warp<16>, (const void*)k_lu_panel_warp<32>})
-                func_attr(f, 32 * 513 * (int)sizeof(double));
-            const size_t ls = (size_t)32 * (R + 1) * sizeof(double);
-            if (R <= 128)
-                k_lu_panel_warp<8><<<1, 32 * cdiv(R, 8), ls, ctx->stream>>>(AB, n, p0, pw, piv, st);
-            else if (R <= 256)
-                k_lu_panel_warp<16><<<1, 32 * cdiv(R, 16), ls, ctx->stream>>>(AB, n, p0, pw, piv, st);
-            else
-                k_lu_panel_warp<32><<<1, 32 * cdiv(R, 32), ls, ctx->stream>>>(AB, n, p0, pw, piv, st);
-        } else {
+        {
             const int T = R <= 512 ? 256 : 1024;  // fewer warps -> cheaper barriers on short panels
             k_lu_panel<<<1, T, use_smem ? pbytes : 0, ctx->stream>>>(AB, n, p0, pw, use_smem, piv, st);
         }

@@ -72,14 +72,9 @@ void smw_update(acp_context* ctx, const double* G, const int* S, const double* W
     fourier_op(ctx, f);
     k_smw_gather<<<dim3(cdiv(N, 128), N > n ? N : n), 128, 0, ctx->stream>>>(Ng, N, n, S, KW, G, A, Y);
     launched(ctx);
-    // blocked multi-kernel LU; ACP_SMW_LU=single uses the one-CTA LU when A fits in shared memory
-    // (measured 13.30 vs 11.71 ms/step on configs[1]: one SM does the O(N^3) work)
-    const char* lu = getenv("ACP_SMW_LU");
-    const bool single = lu && std::string(lu) == "single" && (size_t)N * N * sizeof(double) <= 224 * 1024;
-    if (single)
-        lu_solve(ctx, AB, N, AB + (size_t)N * N, n);
-    else
-        lu_solve_blocked(ctx, AB, N, n);
+    // blocked multi-kernel LU (the one-CTA LU measured 13.30 vs 11.71 ms/step on configs[1]: one SM
+    // does the O(N^3) work)
+    lu_solve_blocked(ctx, AB, N, n);
     gemm_nn(ctx, Ng, N, n, 1.0, W, Ng, Y, N, 0.0, U, Ng);
     if (Gp) {
         copy_cols(ctx, Gp, G, (size_t)Ng * n);

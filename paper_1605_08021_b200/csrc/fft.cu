@@ -520,21 +520,19 @@ static void launch_fft(acp_context* ctx, const IoArgs& io, int ncols) {
         // the multiplier-table region is needed only when the symbol comes from a table
         const bool table = IO == IO_OP && io.f.mult != nullptr && io.f.sym < 0;
         if (!table) smem = (size_t)padded(G.n0) * sizeof(double2);
-        // KEEP (register-resident inputs, <= 160 threads, 4 CTAs/SM) for N <= 1280
-        static const bool nokeep = getenv("ACP_FFT_NOKEEP") != nullptr;
-        auto kern = (T > 160 || nokeep) ? (ctx->fept <= 8 ? k_fft1d<8, false, IO> : k_fft1d<16, false, IO>)
+        // KEEP (register-resident inputs, <= 160 threads, 4 CTAs/SM) for N <= 1280 (without: configs[1]
+        // 11.75 vs 11.58 ms/step)
+        auto kern = T > 160 ? (ctx->fept <= 8 ? k_fft1d<8, false, IO> : k_fft1d<16, false, IO>)
                   : ctx->fept <= 2 ? k_fft1d<2, true, IO> : ctx->fept <= 4 ? k_fft1d<4, true, IO>
                   : k_fft1d<8, true, IO>;
         // compiled-length kernels for the configs' grids (hot path only; ACP_FFT_GENERIC=1 off)
-        if (IO == IO_OP && ctx->fct && nokeep && G.n0 == 1280 && ctx->fept == 8) kern = k_fft1d<8, false, IO, 1280>;
-        if (IO == IO_OP && ctx->fct && !nokeep) {
+        if (IO == IO_OP && ctx->fct) {
             if (G.n0 == 1280 && T <= 160 && ctx->fept == 8) kern = k_fft1d<8, true, IO, 1280>;
             else if (G.n0 == 960 && T <= 160 && ctx->fept == 8) kern = k_fft1d<8, true, IO, 960>;
             else if (G.n0 == 256 && T <= 160 && ctx->fept == 4) kern = k_fft1d<4, true, IO, 256>;
             else if (G.n0 == 5120 && T > 160 && ctx->fept == 8)
                 // 2 CTAs/SM (<= 48 registers): K1 400 vs 474 us, configs[2] 241 vs 251 ms/step
-                kern = (T == 640 && !getenv("ACP_FFT_1CTA")) ? k_fft1d<8, false, IO, 5120, 640, 2>
-                                                             : k_fft1d<8, false, IO, 5120>;
+                kern = T == 640 ? k_fft1d<8, false, IO, 5120, 640, 2> : k_fft1d<8, false, IO, 5120>;
         }
         set_smem_attr((const void*)kern, ctx->fsmem, false);
         cudaLaunchConfig_t cfg = {};
@@ -790,42 +788,16 @@ static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
     if (ctx->fct && n0 == n1 && er <= 8 && ec <= 8) {
         if (n0 == 192) {
             // 192 threads per CTA bounded to 6 CTAs/SM (<= 56 registers, no spill): configs[3]
-            // 762 / 787 / 825 ms/step at 6 / 5 / 3 CTAs/SM (ACP_F2_OCC=3|5|6|7 selects)
-            static const int occ = getenv("ACP_F2_OCC") ? atoi(getenv("ACP_F2_OCC")) : 6;
-            if (occ == 7) {
-                ra = k_f2_rows_fwd<8, 192, 192, 7>;
-                cb = k_f2_cols<8, 192, 192, 7>;
-                rc = k_f2_rows_inv<8, 192, 192, 7>;
-            } else if (occ == 6) {
-                ra = k_f2_rows_fwd<8, 192, 192, 6>;
-                cb = k_f2_cols<8, 192, 192, 6>;
-                rc = k_f2_rows_inv<8, 192, 192, 6>;
-            } else if (occ == 5) {
-                ra = k_f2_rows_fwd<8, 192, 192, 5>;
-                cb = k_f2_cols<8, 192, 192, 5>;
-                rc = k_f2_rows_inv<8, 192, 192, 5>;
-            } else {
-                ra = k_f2_rows_fwd<8, 192>;
-                cb = k_f2_cols<8, 192>;
-                rc = k_f2_rows_inv<8, 192>;
-            }
+            // 762 / 787 / 825 ms/step at 6 / 5 / 3 CTAs/SM
+            ra = k_f2_rows_fwd<8, 192, 192, 6>;
+            cb = k_f2_cols<8, 192, 192, 6>;
+            rc = k_f2_rows_inv<8, 192, 192, 6>;
         } else if (n0 == 256) {
             // 256 threads bounded to 5 CTAs/SM (<= 48 registers, small spills): K1 4.06 / 4.51 / 5.31
-            // ms at 4096 columns for 5 / 4 / 3 CTAs/SM (ACP_F2_OCC256 selects)
-            static const int occ = getenv("ACP_F2_OCC256") ? atoi(getenv("ACP_F2_OCC256")) : 5;
-            if (occ == 5) {
-                ra = k_f2_rows_fwd<8, 256, 256, 5>;
-                cb = k_f2_cols<8, 256, 256, 5>;
-                rc = k_f2_rows_inv<8, 256, 256, 5>;
-            } else if (occ == 4) {
-                ra = k_f2_rows_fwd<8, 256, 256, 4>;
-                cb = k_f2_cols<8, 256, 256, 4>;
-                rc = k_f2_rows_inv<8, 256, 256, 4>;
-            } else {
-                ra = k_f2_rows_fwd<8, 256>;
-                cb = k_f2_cols<8, 256>;
-                rc = k_f2_rows_inv<8, 256>;
-            }
+            // ms at 4096 columns for 5 / 4 / 3 CTAs/SM
+            ra = k_f2_rows_fwd<8, 256, 256, 5>;
+            cb = k_f2_cols<8, 256, 256, 5>;
+            rc = k_f2_rows_inv<8, 256, 256, 5>;
         }
     }
     set_smem_attr((const void*)ra, sr, false);
@@ -833,9 +805,7 @@ static bool launch_fft2d_passes(acp_context* ctx, const FopArgs& a) {
     set_smem_attr((const void*)rc, sr, false);
     const double2* tw0 = (const double2*)ctx->d_tw;
     const double2* tw1 = (const double2*)ctx->d_tw1;
-    // pairs per chunk: ACP_F2_CHUNK keeps a chunk's intermediate L2-resident between the passes
-    static const int chunk_env = getenv("ACP_F2_CHUNK") ? atoi(getenv("ACP_F2_CHUNK")) : 0;
-    const int chunk = chunk_env > 0 ? std::min(chunk_env, 65535) : 65535;
+    const int chunk = 65535;  // grid.y limit
     for (int p0 = 0; p0 < npair; p0 += chunk) {
         const int np = std::min(chunk, npair - p0);
         ra<<<dim3(nrb, np), Tr, sr, ctx->stream>>>(G, tw1, a, Z + (size_t)p0 * n0 * n1, p0);
@@ -1067,12 +1037,10 @@ void fft_init(acp_context* ctx) {
     // with a block barrier each), so each CTA gets as many threads as there are radix-2
     // butterflies (<= 1024): every thread holds <= 2-4 values per pass and the chain is short.
     auto round32 = [](int t) { return (t + 31) / 32 * 32; };
-    // tuning knob: ACP_FFT_THREADS overrides the CTA size (sweeps in tools/k1_sweep.py)
-    const int tknob = getenv("ACP_FFT_THREADS") ? atoi(getenv("ACP_FFT_THREADS")) : 0;
     if (dim == 1) {
         // T = N/8 (<= 8 values per thread): with the register-resident inputs this keeps ~100
         // registers/thread and 4 CTAs per SM (k1_sweep on B200: 160 threads best for N = 1280)
-        int T = tknob > 0 ? round32(tknob) : round32((N + 7) / 8);
+        int T = round32((N + 7) / 8);
         T = T < 64 ? 64 : T > 1024 ? 1024 : T;
         ctx->fthreads = T;
         ctx->fept = ept_for(N, T);
@@ -1119,7 +1087,7 @@ void fft_init(acp_context* ctx) {
         ctx->c1 = n1 / cs;
         const int E = std::max(ctx->r0 * n1, ctx->c1 * n0);
         auto geom_for = [&](int np, int& T, int& ept, size_t& smem) {
-            T = tknob > 0 ? round32(tknob) : round32((np * E + 7) / 8);  // k1_sweep: E/8 per pair
+            T = round32((np * E + 7) / 8);  // E/8 per pair (measured best in round 1)
             T = T < 64 ? 64 : T > 1024 ? 1024 : T;
             ept = ept_for(np * E, T);
             const int slice = std::max(ctx->r0 * n1, ctx->c1 * (n0 + 8));
@@ -1130,18 +1098,8 @@ void fft_init(acp_context* ctx) {
         // 1024 threads and the slices fit ~200 KB (amortises barriers and DSMEM latency)
         // Default np = 1: on B200 two pairs per cluster (1 CTA/SM) ran slower than one pair at
         // 2-3 CTAs/SM (configs[3] grid, 512 columns: 923 vs 642 us) -- occupancy beats barrier
-        // amortisation here.  ACP_FFT2D_NP selects 2 or 4 (tested).
+        // amortisation here.
         int np = 1;
-        if (const char* e = getenv("ACP_FFT2D_NP")) {
-            np = std::max(1, std::min(4, atoi(e)));
-            while (np > 1) {
-                int T2, e2;
-                size_t s2;
-                geom_for(np, T2, e2, s2);
-                if (e2 > 0 && e2 <= 8 && s2 <= 200 * 1024) break;
-                np /= 2;
-            }
-        }
         ctx->fnp = np;
         geom_for(np, ctx->fthreads, ctx->fept, ctx->fsmem);
         ACP_REQUIRE(ctx->fept > 0, "2D slice too large for the FFT engine");

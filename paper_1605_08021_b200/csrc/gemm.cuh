@@ -228,7 +228,7 @@ __device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* _
         for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     // Epilogue order EPI: 0 = each half loaded then stored after the K loop (one half live),
     // 1 = both halves loaded after the K loop, 2 = the first half loaded before the K loop (its
-    // operands do not depend on the product).  Selected per call site (ACP_K3_EPI for the update).
+    // operands do not depend on the product).  Selected per call site.
     typename Ep::Regs regs0[2][2][2];
     auto load_half0 = [&]() {
 #pragma unroll
@@ -478,17 +478,10 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     cluster.sync();
 }
 
-// K split of the cluster projection: CS <= 8 ranks of kchunk rows (~160 per rank).  ACP_K2_SHORTK=1
-// instead gives short K (<= 16 x 128) one memory latency per rank (kchunk <= TC_ST * TC_BK, up
-// to 16 ranks): measured slower on configs[1] (K2 17.5 vs 13.3 us; non-portable cluster sizes).
+// K split of the cluster projection: CS <= 8 ranks of kchunk rows (~160 per rank).  (Short K over
+// up to 16 ranks, one memory latency per rank, measured slower on configs[1]: K2 17.5 vs 13.3 us.)
 inline void tn_split(int K, int& CS, int& kchunk) {
-    static const bool shortk = getenv("ACP_K2_SHORTK") != nullptr;
-    const int ring = TC_ST * TC_BK;
-    if (shortk && K <= 16 * ring) {
-        CS = std::max(1, cdiv(K, ring));
-    } else {
-        CS = std::min(8, std::max(1, cdiv(K, 160)));
-    }
+    CS = std::min(8, std::max(1, cdiv(K, 160)));
     kchunk = cdiv(cdiv(K, CS), TC_BK) * TC_BK;
     CS = cdiv(K, kchunk);
 }
@@ -512,37 +505,20 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = ctx->pdl ? 2 : 1;
-    static const int st32 = getenv("ACP_K2_ST32") ? atoi(getenv("ACP_K2_ST32")) : 4;
-    if (m <= 32 && st32 == 2) {
-        cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
-        cfg.dynamicSmemBytes = tn_cluster_smem<32, 2>();
-        func_attr((const void*)k_tn_cluster<32, Hook, 2>, (int)tn_cluster_smem<32, 2>(), true);
-        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook, 2>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc,
-                                    hook));
-    } else if (m <= 32 && st32 == 3) {
-        cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
-        cfg.dynamicSmemBytes = tn_cluster_smem<32, 3>();
-        func_attr((const void*)k_tn_cluster<32, Hook, 3>, (int)tn_cluster_smem<32, 3>(), true);
-        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook, 3>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc,
-                                    hook));
-    } else if (m <= 32) {
+    // the 32-row tile keeps the 4-stage ring (2 / 3 stages: 11.69 / 11.59 vs 11.57 ms/step on configs[1])
+    if (m <= 32) {
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 32));
         cfg.dynamicSmemBytes = tn_cluster_smem<32>();
         func_attr((const void*)k_tn_cluster<32, Hook>, (int)tn_cluster_smem<32>(), true);
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
-    } else if (!getenv("ACP_K2_ST4")) {
+    } else {
         // 2-stage ring (55 KB -> up to 4 CTAs/SM instead of 2): K2 0.70 vs 0.52 of FP64 peak on
-        // configs[2] (223 vs 241 ms/step), 0.78 vs 0.66 on configs[3] (745 vs 762); ACP_K2_ST4=1: 4-stage
+        // configs[2] (223 vs 241 ms/step), 0.78 vs 0.66 on configs[3] (745 vs 762) with 4 stages
         cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 64));
         cfg.dynamicSmemBytes = tn_cluster_smem<64, 2>();
         func_attr((const void*)k_tn_cluster<64, Hook, 2>, (int)tn_cluster_smem<64, 2>(), true);
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<64, Hook, 2>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc,
                                     hook));
-    } else {
-        cfg.gridDim = dim3(CS, cdiv(n, TC_BN), cdiv(m, 64));
-        cfg.dynamicSmemBytes = tn_cluster_smem<64>();
-        func_attr((const void*)k_tn_cluster<64, Hook>, (int)tn_cluster_smem<64>(), true);
-        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<64, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
     }
     launched(ctx);
     return true;

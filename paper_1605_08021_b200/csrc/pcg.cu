@@ -230,19 +230,12 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
     cfg.attrs = at;
     cfg.numAttrs = ctx->pdl ? 1 : 0;
     if (K >= 64) {
-        // epilogue order (nn_tile_big), same-box A/B: configs[3] 836.8 / 824.9 / 828.2 ms and
-        // configs[2] 252.0 / 251.0 / 252.8 ms per step for EPI 0 / 1 / 2 -> 1 (ACP_K3_EPI overrides)
-        static const int epi = getenv("ACP_K3_EPI") ? atoi(getenv("ACP_K3_EPI")) : 1;
-        auto kern = epi == 1 ? k_pcg_update_big<Ep, 1> : epi == 2 ? k_pcg_update_big<Ep, 2> : k_pcg_update_big<Ep, 0>;
-        size_t smem = nn_big_smem();
-        // ACP_K3_ST2=1: 2-stage ring (72 KB) and 3 CTAs/SM for short K (<= 128)
-        static const bool st2 = getenv("ACP_K3_ST2") != nullptr;
-        if (st2 && K <= 128 && epi == 1) {
-            kern = k_pcg_update_big<Ep, 1, 2, 3>;
-            smem = nn_big_smem<2>();
-        }
-        for (const void* f : {(const void*)k_pcg_update_big<Ep, 0>, (const void*)k_pcg_update_big<Ep, 1>, (const void*)k_pcg_update_big<Ep, 2>, (const void*)k_pcg_update_big<Ep, 1, 2, 3>})
-            func_attr(f, (int)nn_big_smem());
+        // epilogue order 1 (nn_tile_big: both halves loaded after the K loop), same-box A/B:
+        // configs[3] 836.8 / 824.9 / 828.2 ms and configs[2] 252.0 / 251.0 / 252.8 ms per step for
+        // orders 0 / 1 / 2; a 2-stage ring with 3 CTAs/SM was slower (804 vs 763 ms, spills)
+        auto kern = k_pcg_update_big<Ep, 1>;
+        const size_t smem = nn_big_smem();
+        func_attr((const void*)kern, (int)smem);
         cfg.gridDim = dim3(cdiv(M, GB_BM), cdiv(n, GB_BN), 1);
         cfg.blockDim = dim3(256, 1, 1);
         cfg.dynamicSmemBytes = smem;
@@ -251,198 +244,11 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
         cfg.gridDim = dim3(cdiv(M, NP_BM), cdiv(n, NP_BN), 1);
         cfg.blockDim = dim3(128, 1, 1);
         cfg.dynamicSmemBytes = 0;
-        // ACP_K3_OCC=4|5|8 (A/B): the EpAlpha instance's resident-CTA bound
-        static const int kocc = getenv("ACP_K3_OCC") ? atoi(getenv("ACP_K3_OCC")) : 0;
-        auto kern = kocc == 4 ? k_pcg_update<Ep, 4> : kocc == 5 ? k_pcg_update<Ep, 5>
-                  : kocc == 8 ? k_pcg_update<Ep, 8> : k_pcg_update<Ep>;
-        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, M, K, n, A, lda, B, ldb, ep));
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_pcg_update<Ep>, M, K, n, A, lda, B, ldb, ep));
     }
     launched(ctx);
 }
 
-// ---------------------------------------------------------------------------------------------
-// K2+K3 fused (configs whose K slice per cluster rank is short, N_g / CS <= PU_KMAX, N_occ <= 32):
-// one thread-block cluster per 32-column tile, rank r owning rows [r*kchunk, (r+1)*kchunk).
-//   1. Psi and Y slices -> shared memory (one cp.async batch), partial C = Psi_s^T Y_s (DMMA);
-//   2. cluster barrier; rank r sums ITS share of the tile over the CS partials in rank order
-//      (DSMEM, as k_tn_cluster; alpha applied), rank 0 runs the CG scalar hook;
-//   3. cluster barrier; every rank gathers the full C from the owners (one remote load per
-//      element, all in flight), cluster barrier;
-//   4. each rank applies the K3 update to ITS rows: Out = Psi_s C from shared memory (DMMA, same
-//      k order as k_pcg_update) and the Ep epilogue (operands loaded ahead of each group's DMMA chain).
-// Bitwise identical to K2 followed by K3 (same partial sums, same reduction and product order);
-// saves a launch and the second pass over Psi / Y.
-constexpr int PU_KMAX = 192, PU_BM = 32, PU_BN = 32, PU_T = 256;
-constexpr int pu_ldk(int kchunk) { return (kchunk + 15) / 16 * 16 + 4; }
-inline size_t pu_smem(int kchunk) {
-    return ((size_t)(PU_BM + PU_BN) * pu_ldk(kchunk) + 2 * (size_t)PU_BM * (PU_BN + 1)) * sizeof(double);
-}
-
-template <class Hook, class Ep>
-__global__ void __launch_bounds__(PU_T, 2) k_proj_update(int K, int m, int n, const double* __restrict__ Psi,
-                                                     const double* __restrict__ Y, int kchunk, double alpha,
-                                                     Hook hook, Ep ep) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
-    extern __shared__ __align__(16) double psm[];
-    const int LDK = pu_ldk(kchunk);
-    constexpr int LDC = PU_BN + 1;
-    double* As = psm;                        // [PU_BM][LDK]  Psi(k, m) at As[m][k - kb]
-    double* Bs = As + PU_BM * LDK;           // [PU_BN][LDK]  Y(k, c) at Bs[c][k - kb]
-    double* Cs = Bs + PU_BN * LDK;           // [PU_BM][LDC]  partial tile (read by the peers)
-    double* Cf = Cs + PU_BM * LDC;           // [PU_BM][LDC]  full C of the tile
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int g = lane >> 2, t = lane & 3;
-    const int wm = warp & 1, wn = warp >> 1;
-    const int CS = gridDim.x, rank = blockIdx.x;
-    const int n0 = blockIdx.y * PU_BN;
-    pdl_wait();
-    pdl_trigger();
-    if (!hook.tile_active(n0, n)) return;
-    const int kb = rank * kchunk;
-    const int ke = min(K, kb + kchunk);
-    const int kl = max(0, ke - kb);          // rows of this rank
-    const int kp = (kl + 3) / 4 * 4;         // padded to the DMMA depth (zero-filled)
-    for (int c = tid; c < PU_BM * (kp / 2); c += PU_T) {
-        const int row = c / (kp / 2), kk = 2 * (c % (kp / 2));
-        const bool v = row < m && kb + kk < ke;
-        cp_async16(As + row * LDK + kk, v ? (const void*)(Psi + (size_t)row * K + kb + kk) : (const void*)Psi, v);
-    }
-    for (int c = tid; c < PU_BN * (kp / 2); c += PU_T) {
-        const int col = c / (kp / 2), kk = 2 * (c % (kp / 2));
-        const bool v = n0 + col < n && kb + kk < ke;
-        cp_async16(Bs + col * LDK + kk, v ? (const void*)(Y + (size_t)(n0 + col) * K + kb + kk) : (const void*)Y, v);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    // 1. partial C (32 x 32): warps 0..3 as 2 (m) x 2 (n), warp tile 16 x 16, k ascending by 4
-    if (warp < 4) {
-        double acc[2][2][2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        for (int ks = 0; ks < kp; ks += 4) {
-            double af[2], bf[2];
-#pragma unroll
-            for (int i = 0; i < 2; ++i) af[i] = As[(wm * 16 + i * 8 + g) * LDK + ks + t];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) bf[j] = Bs[(wn * 16 + j * 8 + g) * LDK + ks + t];
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-        }
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) Cs[(wm * 16 + i * 8 + g) * LDC + wn * 16 + j * 8 + 2 * t + e] = acc[i][j][e];
-    }
-    cluster.sync();
-    // 2. rank r reduces elements r, r + CS, ... over the cluster in rank order (all remote loads in
-    //    flight together, as k_tn_cluster) into its Cf; rank 0 runs the CG scalar hook
-    for (int e = rank * PU_T + tid; e < PU_BM * PU_BN; e += CS * PU_T) {
-        const int row = e / PU_BN, col = e % PU_BN;
-        double part[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) part[q] = q < CS ? cluster.map_shared_rank(Cs, q)[row * LDC + col] : 0.0;
-        double sum = 0.0;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) sum += part[q];
-        Cf[row * LDC + col] = alpha * sum;
-    }
-    if (rank == 0 && tid < PU_BN && n0 + tid < n) hook(n0 + tid);
-    cluster.sync();
-    // 3. gather the full C from the owners' Cf (one remote load per element, all in flight);
-    //    written to the local Cs (every peer is done reading partials after the barrier)
-    {
-        double v[(PU_BM * PU_BN) / PU_T];
-#pragma unroll
-        for (int q = 0; q < (PU_BM * PU_BN) / PU_T; ++q) {
-            const int e = tid + PU_T * q;
-            const int row = e / PU_BN, col = e % PU_BN;
-            v[q] = cluster.map_shared_rank(Cf, (e / PU_T) % CS)[row * LDC + col];
-        }
-#pragma unroll
-        for (int q = 0; q < (PU_BM * PU_BN) / PU_T; ++q) {
-            const int e = tid + PU_T * q;
-            Cs[(e / PU_BN) * LDC + e % PU_BN] = v[q];
-        }
-    }
-    cluster.sync();  // peers' Cf reads done before anyone exits; local Cs complete
-    // 4. Out = Psi_s C for this rank's rows, 8-row groups strided over the warps
-    const int ngr = (kl + 7) / 8;
-    typename Ep::Regs ra[4][2];
-    auto load_group = [&](int gi, typename Ep::Regs (&r)[4][2]) {
-        const int row = kb + gi * 8 + g;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int col = n0 + j * 8 + 2 * t + e;
-                if (row < ke && col < n) ep.load(row, col, r[j][e]);
-            }
-    };
-    auto product_store = [&](int gi, const typename Ep::Regs (&r)[4][2]) {
-        double acc[4][2];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
-#pragma unroll
-        for (int ms = 0; ms < PU_BM; ms += 4) {
-            const double af = As[(ms + t) * LDK + gi * 8 + g];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[j][0], acc[j][1], af, Cs[(ms + t) * LDC + j * 8 + g]);
-        }
-        const int row = kb + gi * 8 + g;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int col = n0 + j * 8 + 2 * t + e;
-                if (row < ke && col < n) ep.store(row, col, acc[j][e], r[j][e]);
-            }
-    };
-    // 8-row groups strided over the 8 warps; the epilogue operands of a group are loaded before
-    // its DMMA chain (independent, so their latency overlaps it)
-    for (int gi = warp; gi < ngr; gi += PU_T / 32) {
-        load_group(gi, ra);
-        product_store(gi, ra);
-    }
-}
-
-template <class Hook, class Ep>
-static bool launch_proj_update(acp_context* ctx, int K, int m, int n, double alpha, const double* Psi, const double* Y,
-                               const Hook& hook, const Ep& ep) {
-    // opt-in (ACP_PCG_FUSED=1): measured 0.45 ms/step SLOWER than K2 + K3 at configs[1] (three
-    // serial cluster barriers per tile and 8x fewer CTAs for the update)
-    if (m > PU_BM || (K & 1) || (((uintptr_t)Psi | (uintptr_t)Y) & 15) || !getenv("ACP_PCG_FUSED")) return false;
-    // the same K split as launch_tn_cluster (identical partial sums)
-    int CS, kchunk;
-    tn_split(K, CS, kchunk);
-    if (kchunk > PU_KMAX) return false;
-    const size_t smem = pu_smem(kchunk);
-    func_attr((const void*)k_proj_update<Hook, Ep>, (int)pu_smem(PU_KMAX), true);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CS, cdiv(n, PU_BN), 1);
-    cfg.blockDim = dim3(PU_T, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CS;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = ctx->pdl ? 2 : 1;
-    ACP_CUDA(cudaLaunchKernelEx(&cfg, k_proj_update<Hook, Ep>, K, m, n, Psi, Y, kchunk, alpha, hook, ep));
-    launched(ctx);
-    return true;
-}
 
 // Number of still-active columns; sets the while-node condition of the PCG graph (continue while
 // columns remain and fewer than max_chunks chunks ran) and counts the trips.
@@ -604,7 +410,6 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
         fourier_op(ctx, f);
         EpBeta ep{Y, P, s.beta, s.active, Ng, mode == SC_INIT ? 1 : 0};
         const ScalHook hk{mode, s, tol2, nvalid, nmu_p};
-        if (launch_proj_update(ctx, Ng, n_occ, n, ctx->dV, Psi, Y, hk, ep)) return;
         ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ, hk),
                     "projection GEMM needs an even grid");
         launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
@@ -622,7 +427,6 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
         fourier_op(ctx, f);
         EpAlpha ep{Y, P, X, R, s.alpha, s.active, Ng};
         const ScalHook hk{SC_ALPHA, s, tol2, nvalid, nmu_p};
-        if (launch_proj_update(ctx, Ng, n_occ, n, ctx->dV, Psi, Y, hk, ep)) return;
         ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ, hk),
                     "projection GEMM needs an even grid");
         launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
@@ -635,8 +439,7 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
     // `chunk` CG iterations + k_count_active, which sets the loop condition (columns still active
     // and fewer than max_iter iterations done) -- no host round trip until every column has
     // converged.  Cached per shapes/pointers; the chunk counter is reset before each launch.
-    static const int chunk_env = getenv("ACP_PCG_CHUNK") ? atoi(getenv("ACP_PCG_CHUNK")) : 0;
-    const int chunk = chunk_env > 0 ? chunk_env : 4;  // CG iterations per while-node trip
+    const int chunk = 4;  // CG iterations per while-node trip (2 / 8: 11.60 / 11.62 vs 11.57 ms/step)
     const int max_chunks = (max_iter + chunk - 1) / chunk;
     int* d_chunks = d_nact + 1;
     char key[512];
@@ -710,9 +513,9 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
         ACP_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
                                                cudaStreamCaptureModeThreadLocal));
         try {
-            // PDL measured slower on configs[1] (14.25 vs 13.84-14.03 ms/step: the early-scheduled
-            // dependent CTAs take SM slots from the 4-CTA/SM FFT wave), so it is opt-in
-            ctx->pdl = getenv("ACP_PDL") != nullptr;
+            // (programmatic dependent launch measured slower on configs[1]: 14.25 vs 13.84-14.03
+            // ms/step -- the early-scheduled dependent CTAs take SM slots from the FFT wave)
+            ctx->pdl = false;
             for (int it = 0; it < chunk; ++it) {
                 hamiltonian_half();
                 precond_half(SC_BETA);
@@ -959,13 +762,7 @@ void apply_chi0(acp_context* ctx, const double* Psi, const double* eps, const do
                                                                          B);
     launched(ctx);
     EpW ep{X, W, Ng, nmu_p, 0, mu_begin, 2.0 * ctx->sys.occ, 1};
-    if (getenv("ACP_W_PER_NODE")) {
-        for (int c = 0; c < n_cheb; ++c) {
-            ep.c = c;
-            ep.first = c == 0;
-            launch_nn_ep(ctx, Ng, n_occ, cnt, Psi, Ng, B + (size_t)c * cnt * n_occ, n_occ, ep);
-        }
-    } else if (n_occ < 64 && (size_t)n_cheb * cnt * Ng * sizeof(double) <= ((size_t)256 << 20) &&
+    if (n_occ < 64 && (size_t)n_cheb * cnt * Ng * sizeof(double) <= ((size_t)256 << 20) &&
                !getenv("ACP_W_SEQ")) {
         // small problems (configs[1]): all nodes in parallel, then the ordered sum
         double* T = ctx->wsd("chi_Wterms", (size_t)n_cheb * cnt * Ng);
