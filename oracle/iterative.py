@@ -135,13 +135,15 @@ class SternheimerMinres:
         return X - self.Psi @ (self.m.dV * (self.Psi.T @ X))
 
     def A(self, shift, X):
-        """Q(shift - H)Q X."""
-        QX = self.Q(X)
-        return self.Q(shift * QX - self.ops.hamiltonian(self.V, QX))
+        """Q(shift - H)Q X for X in range(Q) -- every vector MINRES feeds here is (the right-hand
+        side is Q rhs, the preconditioner's outputs are projected), so the inner Q is the identity
+        on it and only the outer Q is applied (it also removes any rounding drift)."""
+        return self.Q(shift * X - self.ops.hamiltonian(self.V, X))
 
     def Minv(self, X):
-        """Q M^{-1} Q X, M^{-1} = F^{-1} (|k|^2/2 + tau)^{-1} F (symmetric positive on range(Q))."""
-        return self.Q(self.ops.multiply(self.pre, self.Q(X)))
+        """Q M^{-1} Q X for X in range(Q) (MINRES applies it to residuals, which are),
+        M^{-1} = F^{-1} (|k|^2/2 + tau)^{-1} F: symmetric positive definite on range(Q)."""
+        return self.Q(self.ops.multiply(self.pre, X))
 
     def __call__(self, shift: float, rhs: np.ndarray) -> np.ndarray:
         out = np.empty_like(rhs)
@@ -151,65 +153,72 @@ class SternheimerMinres:
         return out
 
     def _minres(self, shift, b):
-        """Paige-Saunders MINRES, one scalar recurrence per column (x0 = 0)."""
+        """Paige-Saunders MINRES, one scalar recurrence per column (x0 = 0).  The working arrays
+        hold the columns still iterating; converged columns leave them at the residual checks."""
         n = b.shape[1]
         eps = np.finfo(np.float64).eps
-        x = np.zeros_like(b)
+        xout = np.zeros_like(b)
         bnorm = np.linalg.norm(b, axis=0)
-        todo = bnorm > 0
-        r1 = b.copy()
+        cols = np.nonzero(bnorm > 0)[0]            # global column index of each working column
+        if len(cols) == 0:
+            self.iterations.append(0)
+            return xout
+        bw = b[:, cols].copy()
+        x = np.zeros_like(bw)
+        r1 = bw.copy()
         y = self.Minv(r1)
         beta1 = np.sqrt(np.maximum(np.einsum("ij,ij->j", r1, y), 0.0))
-        oldb = np.zeros(n)
+        oldb = np.zeros(len(cols))
         beta = beta1.copy()
-        dbar = np.zeros(n)
-        epsln = np.zeros(n)
+        dbar = np.zeros(len(cols))
+        epsln = np.zeros(len(cols))
         phibar = beta1.copy()
-        cs = -np.ones(n)
-        sn = np.zeros(n)
-        w = np.zeros_like(b)
-        w2 = np.zeros_like(b)
+        cs = -np.ones(len(cols))
+        sn = np.zeros(len(cols))
+        w = np.zeros_like(bw)
+        w2 = np.zeros_like(bw)
         r2 = r1.copy()
-        active = todo.copy()
         itn = 0
         check_every = 10
-        while active.any() and itn < self.maxiter:
+        while len(cols) and itn < self.maxiter:
             itn += 1
-            a = np.nonzero(active)[0]
-            s = 1.0 / beta[a]
-            v = y[:, a] * s
+            v = y / beta
             ya = self.A(shift, v)
             if itn >= 2:
-                ya -= (beta[a] / oldb[a]) * r1[:, a]
+                ya -= (beta / oldb) * r1
             alfa = np.einsum("ij,ij->j", v, ya)
-            ya -= (alfa / beta[a]) * r2[:, a]
-            r1[:, a] = r2[:, a]
-            r2[:, a] = ya
-            yn = self.Minv(ya)
-            y[:, a] = yn
-            oldb[a] = beta[a]
-            beta[a] = np.sqrt(np.maximum(np.einsum("ij,ij->j", ya, yn), 0.0))
-            oldeps = epsln[a]
-            delta = cs[a] * dbar[a] + sn[a] * alfa
-            gbar = sn[a] * dbar[a] - cs[a] * alfa
-            epsln[a] = sn[a] * beta[a]
-            dbar[a] = -cs[a] * beta[a]
-            gamma = np.maximum(np.hypot(gbar, beta[a]), eps)
-            cs[a] = gbar / gamma
-            sn[a] = beta[a] / gamma
-            phi = cs[a] * phibar[a]
-            phibar[a] = sn[a] * phibar[a]
-            w1 = w2[:, a]
-            w2[:, a] = w[:, a]
-            w[:, a] = (v - oldeps * w1 - delta * w2[:, a]) / gamma
-            x[:, a] += phi * w[:, a]
-            if itn % check_every == 0 or (phibar[a] <= 0.01 * self.tol * beta1[a]).any():
+            ya -= (alfa / beta) * r2
+            r1, r2 = r2, ya
+            y = self.Minv(ya)
+            oldb = beta
+            beta = np.sqrt(np.maximum(np.einsum("ij,ij->j", ya, y), 0.0))
+            oldeps = epsln
+            delta = cs * dbar + sn * alfa
+            gbar = sn * dbar - cs * alfa
+            epsln = sn * beta
+            dbar = -cs * beta
+            gamma = np.maximum(np.hypot(gbar, beta), eps)
+            cs = gbar / gamma
+            sn = beta / gamma
+            phi = cs * phibar
+            phibar = sn * phibar
+            w1 = w2
+            w2 = w
+            w = (v - oldeps * w1 - delta * w2) / gamma
+            x += phi * w
+            if itn % check_every == 0 or (phibar <= 0.01 * self.tol * beta1).any():
                 # stop on the true residual of the column (the recurrence's estimate is in the
-                # M^{-1} norm)
-                res = np.linalg.norm(b[:, a] - self.A(shift, x[:, a]), axis=0)
-                done = res <= self.tol * bnorm[a]
-                active[a[done]] = False
-        if active.any():
-            raise RuntimeError(f"MINRES: {int(active.sum())} columns not converged after {itn} iterations")
+                # M^{-1} norm); converged columns leave the working set
+                res = np.linalg.norm(bw - self.A(shift, x), axis=0)
+                done = res <= self.tol * bnorm[cols]
+                if done.any():
+                    xout[:, cols[done]] = x[:, done]
+                    keep = ~done
+                    cols = cols[keep]
+                    bw, x, r1, r2, y, w, w2 = (arr[:, keep] for arr in (bw, x, r1, r2, y, w, w2))
+                    beta1, oldb, beta, dbar, epsln, phibar, cs, sn = (
+                        arr[keep] for arr in (beta1, oldb, beta, dbar, epsln, phibar, cs, sn))
+        if len(cols):
+            raise RuntimeError(f"MINRES: {len(cols)} columns not converged after {itn} iterations")
         self.iterations.append(itn)
-        return x
+        return xout

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libacp_b200.so")
-SOURCES = ["fft.cu", "fft2c.cu", "gemm.cu", "pcg.cu", "qrcp.cu", "dense.cu", "dyson.cu", "scf.cu", "api.cu"]
+SOURCES = ["fft.cu", "fft2c.cu", "gemm.cu", "pcg.cu", "qrcp.cu", "qrcp_kron.cu", "dense.cu", "dyson.cu", "scf.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]

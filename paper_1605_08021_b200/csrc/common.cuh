@@ -309,6 +309,10 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols,
 // ---- dense.cu -----------------------------------------------------------
 // Solve A X = B in place (A: n x n col-major, B: n x nrhs col-major), partial pivoting.
 void lu_solve(acp_context* ctx, double* A, int n, double* B, int nrhs);
+// structured (Kronecker) QRCP for large sketches (qrcp_kron.cu)
+bool kq_supported(int r);
+int kq_compress(acp_context* ctx, const double* Psi, const double* Gt, int r, int kmax, double id_eps, int n_fixed,
+                int n_mu_max, int* S, double* Xi);
 // sharded QRCP (one pivot step per launch; the host all-gathers the candidates between steps)
 int qrs_begin(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, const double* h_theta,
               const int* h_nu, int r_half, int col_begin, int col_end, int n_fixed, int n_mu_max);

@@ -1195,6 +1195,19 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
     launched(ctx);
     double* Gt = ctx->wsd("qr_gt", (size_t)Ng * r);
     gemm_nn(ctx, Ng, n_cols, r, 1.0, Gp, Ng, Om, n_cols, 0.0, Gt, Ng);
+    int kmax = m < Ng ? m : Ng;
+    if (n_fixed > 0 && n_fixed < kmax) kmax = n_fixed;
+    if (n_mu_max < kmax && n_fixed > 0) ACP_REQUIRE(false, "n_mu_fixed exceeds n_mu_max");
+    // Large sketches (m > 256 rows, m N_g > 16M entries: configs[3], [4]): the structured QRCP
+    // that never forms M~^T (qrcp_kron.cu); smaller ones (configs[2]: 7 vs 24 ms) keep the
+    // formed-sketch kernels.  ACP_QRCP_KRON=1 / ACP_QRCP_DENSE=1 force either.
+    const bool big = m > 256 && (size_t)m * Ng > ((size_t)16 << 20);
+    if (kq_supported(r) && m > 64 && !getenv("ACP_QRCP_DENSE") && !getenv("ACP_QRCP_GRID") &&
+        !getenv("ACP_QRCP_SMEM") && (big || getenv("ACP_QRCP_KRON"))) {
+        // kmax <= n_mu_max: the columns of Q / R11 are sized by the caller's capacity
+        return kq_compress(ctx, Psi, Gt, r, std::min(kmax, std::max(n_mu_max, 1) + (n_fixed > 0 ? 0 : 1)), id_eps,
+                           n_fixed, n_mu_max, S, Xi);
+    }
     // Kronecker rows
     double* A = ctx->wsd("qr_A", (size_t)m * Ng);
     {
@@ -1204,9 +1217,6 @@ int compress(acp_context* ctx, const double* Psi, const double* Gp, int n_cols, 
         launched(ctx);
     }
     // QRCP: one persistent cooperative kernel
-    int kmax = m < Ng ? m : Ng;
-    if (n_fixed > 0 && n_fixed < kmax) kmax = n_fixed;
-    if (n_mu_max < kmax && n_fixed > 0) ACP_REQUIRE(false, "n_mu_fixed exceeds n_mu_max");
     int* perm = ctx->wsi("qr_perm", Ng);
     double* rdiag = ctx->wsd("qr_rdiag", m < Ng ? m : Ng);
     int* d_nmu = ctx->wsi("qr_nmu", 1);

@@ -100,14 +100,17 @@ def test_full_size_alg4_and_D(name):
     ctx.close()
 
 
+@pytest.mark.parametrize("dense", [False, True])
 @pytest.mark.parametrize("n_occ,Ng", [(64, 2400), (256, 3000)])
-def test_qrcp_pivots_full_m(n_occ, Ng):
-    """Alg. 2 steps 2-3 at the sketch heights of configs[3] / configs[4]:
-    m = N_occ r = 1024 (global-memory persistent kernel, rows in registers) and m = 4096 (the
-    chunked persistent kernel: eight 512-row chunks per column), seeded inputs, 160 pivots --
-    bit-exact pivots and Xi to 1e-9 against the oracle's QRCP."""
+def test_qrcp_pivots_full_m(n_occ, Ng, dense, monkeypatch):
+    """Alg. 2 steps 2-3 at the sketch heights of configs[3] / configs[4],
+    m = N_occ r = 1024 and 4096, seeded inputs, 160 pivots -- bit-exact pivots and Xi to 1e-9
+    against the oracle's QRCP: the structured Kronecker QRCP (default, qrcp_kron.cu) and the
+    formed-sketch persistent kernels (ACP_QRCP_DENSE: rows in registers at m = 1024, eight
+    512-row chunks per column at m = 4096)."""
     from paper_1605_08021_b200 import Context
     from oracle import acp as oacp
+    monkeypatch.setenv("ACP_QRCP_DENSE" if dense else "ACP_QRCP_KRON", "1")
     rng = np.random.default_rng(n_occ)
     n_pert = 40
     Psi = rng.standard_normal((Ng, n_occ))
@@ -125,3 +128,30 @@ def test_qrcp_pivots_full_m(n_occ, Ng):
     assert np.array_equal(S_g.cpu().numpy(), S_o)
     assert rel(Xi_g.cpu().numpy().T, Xi_o) < 1e-9
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["c2_1d_semiconductor", "c3g_2d_8x8"])
+def test_kronecker_qrcp_equals_formed_sketch_qrcp(name, monkeypatch):
+    """The structured QRCP (screening by downdated norms, exact verification of the candidates,
+    CGS2) and the formed-sketch persistent kernel (exact norms every step) on the configs' own
+    ground states: identical pivots and N_mu, Xi to 1e-10."""
+    from paper_1605_08021_b200 import Context
+    gs_p = os.path.join(ROOT, "tests", "cache", f"{name}_gs.npz")
+    if not os.path.exists(gs_p):
+        pytest.skip("no cached oracle ground state")
+    gs = np.load(gs_p)
+    cfg = get_config(name)
+    R = atom_positions(cfg)
+    G = Model(cfg, R).G_matrix()
+    th, nu = sketch_draws(cfg.seed, 0, G.shape[1], cfg.sketch_r)
+    monkeypatch.setenv("ACP_QRCP_KRON", "1")
+    ctx = Context.from_config(cfg)
+    S1, Xi1, n1 = ctx.compress(T(gs["Psi"].T), T(G.T), th, nu, id_eps=cfg.id_eps)
+    monkeypatch.delenv("ACP_QRCP_KRON")
+    monkeypatch.setenv("ACP_QRCP_DENSE", "1")
+    ctx2 = Context.from_config(cfg)
+    S2, Xi2, n2 = ctx2.compress(T(gs["Psi"].T), T(G.T), th, nu, id_eps=cfg.id_eps)
+    assert n1 == n2 and torch.equal(S1, S2)
+    assert rel(Xi1.cpu().numpy(), Xi2.cpu().numpy()) < 1e-10
+    ctx.close()
+    ctx2.close()

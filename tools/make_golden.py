@@ -54,6 +54,7 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--minres-tol", type=float, default=1e-12)
     ap.add_argument("--scf-tol", type=float, default=None)
+    ap.add_argument("--minres-block", type=int, default=64)
     a = ap.parse_args()
     cfg = get_config(a.config)
     cache = os.path.join(ROOT, "tests", "cache")
@@ -91,7 +92,7 @@ def main():
     n_occ = cfg.n_occ
     G = m.G_matrix()
     H = m.hamiltonian_dense(V) if dense else None
-    solve = None if dense else oit.SternheimerMinres(m, V, Psi, tol=a.minres_tol)
+    solve = None if dense else oit.SternheimerMinres(m, V, Psi, tol=a.minres_tol, block=a.minres_block)
     samples = {}
 
     def on_outer(k, S, W, Y, Xi):
