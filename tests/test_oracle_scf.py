@@ -25,6 +25,22 @@ def test_paper_section_4_1_ground_state(name):
     assert abs(gs.rho.max() - ref["rho_max"]) <= 5e-5
 
 
+@pytest.mark.slow
+def test_paper_section_4_2_triangular_gap():
+    """eps_99 - eps_98 = 1.2637 for the 98-atom triangular lattice of PAPER.md:1064-1066
+    (printed to 4 decimals; readings R19: kappa = 0.01, 7 x 7 rectangular two-atom cells).  Pins the
+    oracle's 2D conventions (Yukawa symbol, 2D Gaussian pseudocharge, non-square cell).  The SCF
+    restarts from the density tools/probe_paper_2d.py (oracle only) converged on this grid, so it must
+    hold it as a fixed point within a few iterations instead of running ~30 from scratch."""
+    cfg = get_config("paper_2d_triangular")
+    m = Model(cfg, atom_positions(cfg))
+    rho0 = np.load(os.path.join(os.path.dirname(__file__), "golden", "paper_2d_tri98_rho.npy"))
+    gs = scf(m, tol=1e-9, rho0=rho0, max_iter=4)
+    assert gs.n_iter <= 3
+    assert abs(m.integrate(gs.rho) - 98.0) < 1e-9
+    assert abs(gs.gap - GOLD["paper_2d_triangular"]["gap"]) <= 5e-5
+
+
 def test_free_particle_spectrum():
     """SPEC.md:221: V = 0 -> eigenvalues {0, 1/2 (2pi/L)^2 (x2), 1/2 (4pi/L)^2 (x2), ...}."""
     cfg = small_config()

@@ -43,13 +43,19 @@ class SystemConfig:
     n_outer: int = 4
     cg_tol: float = 1e-11
     scf_tol: float = 1e-12
+    lattice: str = "square"        # "square" (n_side^d atoms) or "triangular" (2D, 2 n_side^2 atoms)
 
     @property
     def n_atoms(self) -> int:
+        if self.lattice == "triangular":
+            return 2 * self.n_side ** 2
         return self.n_side ** self.dim
 
     @property
     def cell(self) -> Tuple[float, ...]:
+        if self.lattice == "triangular":
+            # n_side x n_side rectangular cells a x a sqrt(3), two atoms each (R19)
+            return (self.n_side * self.spacing, self.n_side * self.spacing * 3.0 ** 0.5)
         return tuple(self.n_side * self.spacing for _ in range(self.dim))
 
     @property
@@ -101,6 +107,13 @@ CONFIGS: Dict[str, SystemConfig] = {
         name="paper_1d_semiconductor", dim=1, n_side=60, spacing=2.4, Z=1.0, sigma=0.3,
         kappa=0.1, eps0=10.0, grid=(960,), n_occ=60, occ=1.0, n_cheb=20,
         jitter=0.0, seed=0),
+    # PAPER.md:1064-1066, 1100 (section 4.2): triangular lattice, nearest neighbour 1.2, eps0 = 0.05,
+    # Z = 1, sigma = 0.24, N_A = 2 x 7^2 = 98, one electron per orbital; kappa = 0.01 and the
+    # supercell are readings (R19); grid spacing 0.175 (gap converged to 1e-6 there).
+    "paper_2d_triangular": SystemConfig(
+        name="paper_2d_triangular", dim=2, n_side=7, spacing=1.2, Z=1.0, sigma=0.24,
+        kappa=0.01, eps0=0.05, grid=(48, 84), n_occ=98, occ=1.0, n_cheb=30,
+        jitter=0.0, seed=0, sketch_r=16, n_outer=2, lattice="triangular"),
 }
 
 # configs[3] / configs[4] with eps0 = 1 instead of 10 (reading R13): at eps0 = 10

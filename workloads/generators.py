@@ -20,8 +20,15 @@ from .configs import SystemConfig
 def atom_positions(cfg: SystemConfig) -> np.ndarray:
     """(N_A, d) positions in bohr, wrapped into the periodic cell."""
     rng = np.random.default_rng([cfg.seed, 1])
-    idx = np.indices((cfg.n_side,) * cfg.dim).reshape(cfg.dim, -1).T  # (N_A, d), C order
-    R = idx.astype(np.float64) * cfg.spacing
+    if cfg.lattice == "triangular":
+        # rectangular cells a x a sqrt(3) with atoms at (0, 0) and (a/2, a sqrt(3)/2) (DESIGN.md R19)
+        a, h = cfg.spacing, cfg.spacing * np.sqrt(3.0)
+        idx = np.indices((cfg.n_side, cfg.n_side)).reshape(2, -1).T.astype(np.float64)
+        base = idx * np.array([a, h])
+        R = np.stack([base, base + np.array([a / 2, h / 2])], axis=1).reshape(-1, 2)
+    else:
+        idx = np.indices((cfg.n_side,) * cfg.dim).reshape(cfg.dim, -1).T  # (N_A, d), C order
+        R = idx.astype(np.float64) * cfg.spacing
     if cfg.jitter > 0:
         R = R + rng.uniform(-cfg.jitter, cfg.jitter, size=R.shape)
     L = np.asarray(cfg.cell)
