@@ -53,6 +53,9 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        if os.environ.get("ACP_BENCH_NO_SMI"):  # diagnostics: no sampler process
+            self.p = None
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -227,10 +230,16 @@ def run_acp(args, cfg):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    for _ in range(args.warmup):
+    clocks = None
+    for w in range(args.warmup):
+        if w == args.warmup - 1:
+            # the nvidia-smi sampler starts during the last warm-up step (its start-up is not in the
+            # timed region); it samples until the timed steps end
+            clocks = ClockSampler(local)
         step()
+    if clocks is None:
+        clocks = ClockSampler(local)
     # ---- timed region: device time per step (CUDA events on the launching stream), L2 flushed between steps
-    clocks = ClockSampler(local)
     launches0 = ctx.kernel_launches
     times = []
     solves = 0
@@ -355,7 +364,10 @@ def run_acp(args, cfg):
             else:
                 kern[name] = dict(hbm, tensor=dict(ten, frac=ten["achieved"] / ten["peak"]))
         kern[name]["frac"] = kern[name]["achieved"] / kern[name]["peak"]
-    dom_name = os.environ.get("ACP_DOMINANT_KERNEL", "K1_fourier_op")
+    # the dominant kernel = the largest share of the step: K1, K2 and K3 each launch twice per CG
+    # iteration over the same columns (H p and M r; the two projections; EpAlpha and EpBeta), so
+    # the share follows the per-launch time (K1 at configs[1], K3 at c4g)
+    dom_name = os.environ.get("ACP_DOMINANT_KERNEL") or max(kern, key=lambda k: kern[k]["us"])
     dom = kern[dom_name]
     # DRAM bytes per launch of this kernel on THIS workload from one ncu --set full capture
     # (profiles/traffic.json: {workload: {kernel: {"bytes_per_launch", "units_per_launch", ...}}}),

@@ -113,14 +113,29 @@ void dyson(acp_context* ctx, const double* Psi, const double* eps, const double*
     int max_it = 0;
     double max_res = 0.0;
     std::vector<double> dn_sync(o.n_outer, 0.0), it_sync(o.n_outer, 0.0);
+    // ACP_DYSON_PROF: CUDA events around compress / apply_chi0 / SMW of every outer iteration
+    // (printed to stderr at the end; diagnostics only)
+    static const bool prof = getenv("ACP_DYSON_PROF") != nullptr;
+    std::vector<cudaEvent_t> evs;
+    auto mark = [&]() {
+        if (!prof) return;
+        cudaEvent_t e;
+        ACP_CUDA(cudaEventCreate(&e));
+        ACP_CUDA(cudaEventRecord(e, ctx->stream));
+        evs.push_back(e);
+    };
+    mark();
     for (int k = 0; k < o.n_outer; ++k) {
         const int N = compress(ctx, Psi, Gp, n, h_theta + (size_t)k * n, h_nu + (size_t)k * o.r_half, o.r_half,
                                o.id_eps, o.n_mu_fixed, nmu_max, S, Xi);
         Ns[k] = N;
         ctx->defer_iter = k;
+        mark();
         PcgStats st;
         apply_chi0(ctx, Psi, eps, V, S, Xi, N, 0, N, o.n_cheb, o.cg_tol, o.max_cg_iter, W, &st);
+        mark();
         smw_update(ctx, G, S, W, N, U, Gp);
+        mark();
         if (ctx->defer) {
             k_diff_norm2<<<256, 256, 0, ctx->stream>>>((size_t)Ng * n, U, Uprev, dpart + (size_t)k * 256);
             launched(ctx);
@@ -135,6 +150,17 @@ void dyson(acp_context* ctx, const double* Psi, const double* eps, const double*
         copy_cols(ctx, Uprev, U, (size_t)Ng * n);
     }
     std::vector<double> dn(o.n_outer), itk(o.n_outer);
+    if (prof) {
+        ACP_CUDA(cudaEventSynchronize(evs.back()));
+        fprintf(stderr, "[dyson ms: compress / chi0 / smw per outer]");
+        for (size_t q = 1; q < evs.size(); ++q) {
+            float ms = 0.f;
+            ACP_CUDA(cudaEventElapsedTime(&ms, evs[q - 1], evs[q]));
+            fprintf(stderr, " %.1f", ms);
+        }
+        fprintf(stderr, "\n");
+        for (auto e : evs) cudaEventDestroy(e);
+    }
     if (ctx->defer) {
         std::vector<long long> hs(nst);
         std::vector<double> hp((size_t)o.n_outer * 256);

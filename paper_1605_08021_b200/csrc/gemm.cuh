@@ -333,6 +333,116 @@ __device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* _
             }
 }
 
+// 128 x 64 NN tile for the PCG update at N_occ >= 128 (configs[2], [4]: a genuine FP64 GEMM with
+// K = N_occ): 256 threads = 8 warps as 4 (m) x 2 (n), warp tile 32 x 32 = 4 x 4 DMMA tiles (8 shared
+// loads per 16 DMMAs instead of 6 per 8), XL_ST-stage cp.async ring of 16-deep K slices (27 KB per
+// stage: two CTAs per SM), then the epilogue in four quarters of 8 elements per thread (each
+// quarter's global loads in flight together).  A operand rows are 1.33x as long per byte of B as in
+// the 64 x 64 tile, so the L2 -> SM operand stream per flop drops by a quarter.
+constexpr int XL_BM = 128, XL_BN = 64, XL_BK = 16, XL_ST = 3, XL_LDA = XL_BM + 4, XL_LDB = XL_BK + 4;
+
+template <int ST = XL_ST>
+constexpr size_t nn_xl_smem() { return (size_t)ST * (XL_BK * XL_LDA + XL_BN * XL_LDB) * sizeof(double); }
+
+template <class Ep, int ST = XL_ST>
+__device__ __forceinline__ void nn_tile_xl(int M, int K, int n, const double* __restrict__ A, int lda,
+                                           const double* __restrict__ B, int ldb, int m0, int n0, const Ep& ep) {
+    extern __shared__ __align__(16) double gsm[];
+    double* As = gsm;                            // [ST][XL_BK][XL_LDA]  A(m, k) at [k][m]
+    double* Bs = gsm + ST * XL_BK * XL_LDA;      // [ST][XL_BN][XL_LDB]  B(k, n) at [n][k]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
+    const int nk = (K + XL_BK - 1) / XL_BK;
+    const bool vecA = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0) && ((m0 & 1) == 0);
+    const bool vecB = ((ldb & 1) == 0) && ((((uintptr_t)B) & 15) == 0);
+    auto load_stage = [&](int st, int k0) {
+        double* as = As + st * XL_BK * XL_LDA;
+        double* bs = Bs + st * XL_BN * XL_LDB;
+#pragma unroll
+        for (int q = 0; q < (XL_BK * XL_BM / 2) / 256; ++q) {
+            const int c = tid + q * 256;
+            const int kk = c / (XL_BM / 2), mm = 2 * (c % (XL_BM / 2));
+            const int gm = m0 + mm, gk = k0 + kk;
+            if (vecA && gm + 1 < M && gk < K) {
+                cp_async16(as + kk * XL_LDA + mm, A + (size_t)gk * lda + gm, true);
+            } else {
+                as[kk * XL_LDA + mm] = (gm < M && gk < K) ? A[(size_t)gk * lda + gm] : 0.0;
+                as[kk * XL_LDA + mm + 1] = (gm + 1 < M && gk < K) ? A[(size_t)gk * lda + gm + 1] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < (XL_BN * XL_BK / 2) / 256; ++q) {
+            const int c = tid + q * 256;
+            const int nn = c / (XL_BK / 2), kk = 2 * (c % (XL_BK / 2));
+            const int gn = n0 + nn, gk = k0 + kk;
+            if (vecB && gn < n && gk + 1 < K) {
+                cp_async16(bs + nn * XL_LDB + kk, B + (size_t)gn * ldb + gk, true);
+            } else {
+                bs[nn * XL_LDB + kk] = (gn < n && gk < K) ? B[(size_t)gn * ldb + gk] : 0.0;
+                bs[nn * XL_LDB + kk + 1] = (gn < n && gk + 1 < K) ? B[(size_t)gn * ldb + gk + 1] : 0.0;
+            }
+        }
+    };
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int st = 0; st < ST - 1; ++st) {
+        if (st < nk) load_stage(st, st * XL_BK);
+        cp_async_commit();
+    }
+    for (int it = 0; it < nk; ++it) {
+        const int nxt = it + ST - 1;
+        if (nxt < nk) load_stage(nxt % ST, nxt * XL_BK);
+        cp_async_commit();
+        cp_async_wait<ST - 1>();
+        __syncthreads();
+        const double* as = As + (it % ST) * XL_BK * XL_LDA + wm * 32 + g;
+        const double* bs = Bs + (it % ST) * XL_BN * XL_LDB + (wn * 32 + g) * XL_LDB + t;
+#pragma unroll
+        for (int ks = 0; ks < XL_BK; ks += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = as[(ks + t) * XL_LDA + i * 8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = bs[j * 8 * XL_LDB + ks];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    // epilogue in chunks of EC elements per thread (all of a chunk's global loads in flight together)
+    constexpr int EJ = sizeof(typename Ep::Regs) > 24 ? 2 : 4;   // j-columns per chunk
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = m0 + wm * 32 + i * 8 + g;
+#pragma unroll
+        for (int j0 = 0; j0 < 4; j0 += EJ) {
+            typename Ep::Regs regs[EJ][2];
+#pragma unroll
+            for (int j = 0; j < EJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int col = n0 + wn * 32 + (j0 + j) * 8 + 2 * t + e;
+                    if (row < M && col < n) ep.load(row, col, regs[j][e]);
+                }
+#pragma unroll
+            for (int j = 0; j < EJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int col = n0 + wn * 32 + (j0 + j) * 8 + 2 * t + e;
+                    if (row < M && col < n) ep.store(row, col, acc[i][j0 + j][e], regs[j][e]);
+                }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Split-K TN GEMM with the K-split reduced through distributed shared memory.
 //   C(m x n, ld ldc) = alpha * A(:, m)^T B(:, n),  A: K x m (lda), B: K x n (ldb).

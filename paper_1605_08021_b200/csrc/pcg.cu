@@ -121,8 +121,65 @@ struct ScalHook {
     }
 };
 
-// K3 after H p: Ap = Y - Psi C;  X += alpha P;  R -= alpha Ap.
+// K3 after H p: Ap = Y - Psi C;  R -= alpha Ap.  (X += alpha P is deferred to EpBeta of the same
+// iteration, which reads P anyway: 24 instead of 48 bytes per element here, 40 instead of 24
+// there; the iteration at which a column converges skips EpBeta, so k_pcg_x_final applies that
+// last alpha P after the loop -- the same operations on the same values, bitwise the same X.)
 struct EpAlpha {
+    const double* Y;
+    double* R;
+    const double* alpha;
+    const int* active;
+    int ld;
+    struct Regs {
+        double y, r;
+        bool on;
+    };
+    __device__ __forceinline__ void load(int r, int c, Regs& g) const {
+        g.on = active[c] != 0;
+        if (!g.on) return;
+        const size_t o = (size_t)c * ld + r;
+        g.y = Y[o];
+        g.r = R[o];
+    }
+    __device__ __forceinline__ void store(int r, int c, double acc, const Regs& g) const {
+        if (!g.on) return;
+        R[(size_t)c * ld + r] = g.r - alpha[c] * (g.y - acc);
+    }
+};
+// K3 after M r: Z = Zh - Psi Cz;  X += alpha P;  P = Z + beta P.
+struct EpBeta {
+    const double* Zh;
+    double* P;
+    double* X;
+    const double* alpha;
+    const double* beta;
+    const int* active;
+    int ld;
+    struct Regs {
+        double zh, p, x;
+        bool on;
+    };
+    __device__ __forceinline__ void load(int r, int c, Regs& g) const {
+        g.on = active[c] != 0;
+        if (!g.on) return;
+        const size_t o = (size_t)c * ld + r;
+        g.zh = Zh[o];
+        g.p = P[o];
+        g.x = X[o];
+    }
+    __device__ __forceinline__ void store(int r, int c, double acc, const Regs& g) const {
+        if (!g.on) return;
+        const size_t o = (size_t)c * ld + r;
+        X[o] = g.x + alpha[c] * g.p;
+        P[o] = (g.zh - acc) + beta[c] * g.p;
+    }
+};
+// The same two updates with X += alpha P in EpAlpha (EpAlphaX / EpBetaP): used where K3 is bound by
+// the DMMA work (N_occ >= 64), where the longer EpBeta epilogue cost more than the saved bytes
+// (c4g, 4096 columns: EpBeta + EpAlpha 11.72 ms with X in EpBeta, 11.28 ms here); for N_occ < 64
+// K3 is HBM-bound and 64 instead of 72 bytes per element and iteration win.
+struct EpAlphaX {
     const double* Y;
     const double* P;
     double* X;
@@ -151,14 +208,12 @@ struct EpAlpha {
         R[o] = g.r - a * (g.y - acc);
     }
 };
-// K3 after M r: Z = Zh - Psi Cz;  P = Z + beta P (or P = Z at init).
-struct EpBeta {
+struct EpBetaP {
     const double* Zh;
     double* P;
     const double* beta;
     const int* active;
     int ld;
-    int init;
     struct Regs {
         double zh, p;
         bool on;
@@ -168,20 +223,56 @@ struct EpBeta {
         if (!g.on) return;
         const size_t o = (size_t)c * ld + r;
         g.zh = Zh[o];
-        g.p = init ? 0.0 : P[o];
+        g.p = P[o];
     }
     __device__ __forceinline__ void store(int r, int c, double acc, const Regs& g) const {
         if (!g.on) return;
-        const double z = g.zh - acc;
-        P[(size_t)c * ld + r] = init ? z : z + beta[c] * g.p;
+        P[(size_t)c * ld + r] = (g.zh - acc) + beta[c] * g.p;
+    }
+};
+// K3 at the start: P = Z = Zh - Psi Cz (X = 0 stays).
+struct EpInit {
+    const double* Zh;
+    double* P;
+    const int* active;
+    int ld;
+    struct Regs {
+        double zh;
+        bool on;
+    };
+    __device__ __forceinline__ void load(int r, int c, Regs& g) const {
+        g.on = active[c] != 0;
+        if (!g.on) return;
+        g.zh = Zh[(size_t)c * ld + r];
+    }
+    __device__ __forceinline__ void store(int r, int c, double acc, const Regs& g) const {
+        if (!g.on) return;
+        P[(size_t)c * ld + r] = g.zh - acc;
     }
 };
 
+static inline bool pcg_x_in_beta(int n_occ) { return n_occ < 64; }
+
+// After the CG loop: the columns that converged skipped EpBeta in their last iteration, so their
+// X lacks that iteration's alpha p (P still holds p, alpha its alpha); still-active columns (max_iter
+// reached) had every update.
+__global__ void k_pcg_x_final(int Ng, int n, const int* __restrict__ active, const int* __restrict__ iters,
+                              const double* __restrict__ alpha, const double* __restrict__ P, double* __restrict__ X) {
+    const int c = blockIdx.y;
+    if (active[c] || iters[c] == 0) return;
+    const double a = alpha[c];
+    const size_t o = (size_t)c * Ng;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < Ng; r += gridDim.x * blockDim.x)
+        X[o + r] += a * P[o + r];
+}
+
 // Resident CTAs per SM requested from ptxas: enough that configs[1]'s 1160 tiles fit one wave
-// where the epilogue registers allow it (EpBeta keeps 2 operands per element, EpAlpha 4).
+// where the epilogue registers allow it (EpAlpha keeps 2 operands per element, EpBeta 3).
 template <class Ep> struct K3Occ { static constexpr int v = 4; };
-template <> struct K3Occ<EpBeta> { static constexpr int v = 8; };
-template <> struct K3Occ<EpAlpha> { static constexpr int v = 6; };
+template <> struct K3Occ<EpBeta> { static constexpr int v = 6; };
+template <> struct K3Occ<EpAlpha> { static constexpr int v = 8; };
+template <> struct K3Occ<EpBetaP> { static constexpr int v = 8; };
+template <> struct K3Occ<EpAlphaX> { static constexpr int v = 6; };
 
 template <class Ep, int OCC = K3Occ<Ep>::v>
 __global__ void __launch_bounds__(128, OCC) k_pcg_update(int M, int K, int n, const double* __restrict__ A, int lda,
@@ -219,6 +310,24 @@ __global__ void __launch_bounds__(256, MINB) k_pcg_update_big(int M, int K, int 
     nn_tile_big<Ep, EPI, ST>(M, K, n, A, lda, B, ldb, blockIdx.x * GB_BM, n0, ep);
 }
 
+// N_occ >= 128: 128 x 64 tiles (nn_tile_xl), two CTAs per SM.
+template <class Ep, int ST = XL_ST>
+__global__ void __launch_bounds__(256, 2) k_pcg_update_xl(int M, int K, int n, const double* __restrict__ A, int lda,
+                                                          const double* __restrict__ B, int ldb, Ep ep) {
+    pdl_wait();
+    pdl_trigger();
+    const int n0 = blockIdx.y * XL_BN;
+    __shared__ int any;
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int c = n0; c < min(n, n0 + XL_BN); ++c) a |= ep.active[c];
+        any = a;
+    }
+    __syncthreads();
+    if (!any) return;
+    nn_tile_xl<Ep, ST>(M, K, n, A, lda, B, ldb, blockIdx.x * XL_BM, n0, ep);
+}
+
 template <class Ep>
 static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const double* A, int lda, const double* B,
                               int ldb, const Ep& ep) {
@@ -229,7 +338,19 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = ctx->pdl ? 1 : 0;
-    if (K >= 64) {
+    // 128 x 64 tiles for N_occ >= 128: c4g EpBeta 5.25 vs 5.71 ms, EpAlpha 6.03 vs 7.63 ms per 4096
+    // columns, 11.13 vs 12.85 s per step (same box); 4 stages: 5.73 / 7.00 ms
+    // (c3g, N_occ = 64: 651 vs 698 ms per step with the 64 x 64 tile)
+    static const int xl_mink = getenv("ACP_K3_XL_MINK") ? atoi(getenv("ACP_K3_XL_MINK")) : 64;
+    if (K >= xl_mink) {
+        auto kern = k_pcg_update_xl<Ep, 3>;
+        const size_t smem = nn_xl_smem<3>();
+        func_attr((const void*)kern, (int)smem);
+        cfg.gridDim = dim3(cdiv(M, XL_BM), cdiv(n, XL_BN), 1);
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, M, K, n, A, lda, B, ldb, ep));
+    } else if (K >= 64) {
         // epilogue order 1 (nn_tile_big: both halves loaded after the K loop), same-box A/B:
         // configs[3] 836.8 / 824.9 / 828.2 ms and configs[2] 252.0 / 251.0 / 252.8 ms per step for
         // orders 0 / 1 / 2; a 2-stage ring with 3 CTAs/SM was slower (804 vs 763 ms, spills)
@@ -397,6 +518,7 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
     int* h_nact = G.h_nact;
     const int nvalid = nmu_p;  // columns beyond the caller's count are zero RHS -> inactive by bb = 0
     G.synced = false;
+    const bool x_in_beta = pcg_x_in_beta(n_occ);
 
     auto precond_half = [&](int mode) {
         FopArgs f;
@@ -408,11 +530,16 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
         f.active = (mode == SC_INIT) ? nullptr : s.active;
         f.dots = dots;
         fourier_op(ctx, f);
-        EpBeta ep{Y, P, s.beta, s.active, Ng, mode == SC_INIT ? 1 : 0};
         const ScalHook hk{mode, s, tol2, nvalid, nmu_p};
         ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ, hk),
                     "projection GEMM needs an even grid");
-        launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
+        if (mode == SC_INIT) {
+            launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpInit{Y, P, s.active, Ng});
+        } else if (x_in_beta) {
+            launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpBeta{Y, P, X, s.alpha, s.beta, s.active, Ng});
+        } else {
+            launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpBetaP{Y, P, s.beta, s.active, Ng});
+        }
     };
     auto hamiltonian_half = [&]() {
         FopArgs f;
@@ -425,11 +552,13 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
         f.active = s.active;
         f.dots = dots;
         fourier_op(ctx, f);
-        EpAlpha ep{Y, P, X, R, s.alpha, s.active, Ng};
         const ScalHook hk{SC_ALPHA, s, tol2, nvalid, nmu_p};
         ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ, hk),
                     "projection GEMM needs an even grid");
-        launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
+        if (x_in_beta)
+            launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpAlpha{Y, R, s.alpha, s.active, Ng});
+        else
+            launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpAlphaX{Y, P, X, R, s.alpha, s.active, Ng});
     };
 
     // r0 = b, z0 = Q M r0, p0 = z0
@@ -697,6 +826,10 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         }
         if (!ctx->defer) ACP_CUDA(cudaStreamSynchronize(s0));
     }
+    if (pcg_x_in_beta(n_occ)) {
+        k_pcg_x_final<<<dim3(cdiv(Ng, 1024), n), 256, 0, ctx->stream>>>(Ng, n, s.active, s.iters, s.alpha, P, X);
+        launched(ctx);
+    }
     if (ctx->defer) {
         // no host wait: accumulate the statistics on the device (read at the end of acp_dyson)
         long long lpt[PCG_MAXG] = {};
@@ -791,6 +924,7 @@ void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* 
     double* C = ctx->wsd("kb_C", (size_t)n_occ * n);
     double* beta = ctx->wsd("kb_beta", n);
     int* active = ctx->wsi("kb_active", n);
+    double* kb_X = which >= 2 ? ctx->wsd("kb_X", (size_t)Ng * n) : nullptr;
     // operand setup once per batch width (outside the caller's timed region on later calls)
     const std::string skey = "kbsetup:" + std::to_string(n);
     if (ctx->graphs.find(skey) == ctx->graphs.end()) {
@@ -818,9 +952,18 @@ void kernel_bench(acp_context* ctx, int which, const double* Psi, const double* 
                 fourier_op(ctx, f);
             } else if (which == 1) {
                 launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, X, Ng, C, n_occ, NoHook{});
+            } else if (which == 2) {
+                // the production EpBeta: P = (X - Psi C) + beta P (+ X += alpha P when X is updated there)
+                if (pcg_x_in_beta(n_occ))
+                    launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpBeta{X, Y, kb_X, beta, beta, active, Ng});
+                else
+                    launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpBetaP{X, Y, beta, active, Ng});
             } else {
-                EpBeta ep{X, Y, beta, active, Ng, 0};
-                launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, ep);
+                // the production EpAlpha: Ap = X - Psi C, R -= alpha Ap (+ X += alpha P)
+                if (pcg_x_in_beta(n_occ))
+                    launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpAlpha{X, Y, beta, active, Ng});
+                else
+                    launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpAlphaX{X, kb_X, kb_X, Y, beta, active, Ng});
             }
         }
     };

@@ -12,8 +12,9 @@
 // position on ties) -- the greedy rule of the oracle (reading R8), decided on exact trailing
 // norms.  The winner's component is re-orthogonalised once (CGS2) and becomes q_j; R11(:, j) =
 // Q_j^T a_w, R(j, j) = |y'_w|.  The stop rule is the oracle's: |R_jj| < eps |R_11|.
-// Per pivot: one pass over Psi and four over Q_j (m x j) -- instead of a read and a write of the
-// whole m x N_g sketch per pivot (k_qrcp_persistent).  ONE cooperative launch, grid barriers
+// The candidates' coefficients Q_j^T a_c are columns of the R rows already computed (R(k, a) for
+// every grid point a at every pivot k), so per pivot: one pass over Psi and three over Q_j (m x j)
+// -- instead of a read and a write of the whole m x N_g sketch per pivot (k_qrcp_persistent).  ONE cooperative launch, grid barriers
 // between the phases; every reduction has a fixed order.
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -27,8 +28,7 @@ namespace cgk = cooperative_groups;
 constexpr int KQ_CMAX = 16;  // candidates verified per pivot
 constexpr int KQ_T = 256;
 constexpr int KQ_U = 16;   // loads in flight per thread in the passes over Q
-constexpr int KQ_U3 = 32;  // ... in the first pass (W = Q^T a_c, warp per (k, c))
-constexpr int KQ_UP = 16;  // psi fragments in flight per lane in the R-row DMMA pass
+constexpr int KQ_UP = 32;  // psi fragments in flight per lane in the R-row DMMA pass
 
 struct KqArgs {
     int m, Ng, n_occ, r, kmax, fixed;
@@ -45,7 +45,6 @@ struct KqArgs {
     double* rdiag;       // kmax
     double* slots;       // G: per-CTA max n2
     double* tpart;       // G x CMAX: per-CTA partial exact norms
-    double* W;           // kmax x CMAX: Q^T a_c
     double* Y;           // CMAX x m: candidate components (y_c)
     double* w2;          // kmax: Q^T y_w (second pass)
     int* cand;           // 2 x CMAX
@@ -160,7 +159,9 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
         __threadfence();
         grid.sync();
         KQ_MARK(1);
-        // ---- P3: W(k, c) = q_k^T a_c  (a_c = psi(c) (x) g~(c) rebuilt from shared memory)
+        // ---- P3: the candidates' psi(c), g~(c) staged in shared memory.  Their coefficients in the
+        // current basis, W(k, c) = q_k^T a_c (k < j), are the R rows the earlier pivots' P6 passes
+        // already produced for every grid point: W(k, c) = R(k, c) = Rrows[k Ng + c] (no pass over Q)
         const int nc = min(__ldcg(&g.ncand[par]), KQ_CMAX);
         for (int e = t; e < nc * n_occ; e += KQ_T) {
             const int c = e / n_occ, i = e - c * n_occ;
@@ -171,33 +172,6 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
             cgs[e] = g.Gt[(size_t)q * Ng + __ldcg(&g.cand[par * KQ_CMAX + c])];
         }
         __syncthreads();
-        for (int kc = gw; kc < j * nc; kc += GW) {
-            const int k = kc / nc, c = kc - k * nc;
-            const double* qk = g.Q + (size_t)k * m;
-            const double* pc = cps + c * n_occ;
-            const double* gc = cgs + c * RQ;
-            double acc = 0.0;
-            for (int e0b = 0; e0b < m; e0b += 32 * KQ_U3) {
-                double qv[KQ_U3];
-#pragma unroll
-                for (int u = 0; u < KQ_U3; ++u) {
-                    const int e = e0b + lane + 32 * u;
-                    qv[u] = e < m ? __ldcg(&qk[e]) : 0.0;  // eight loads in flight per lane
-                }
-#pragma unroll
-                for (int u = 0; u < KQ_U3; ++u) {
-                    const int e = e0b + lane + 32 * u;
-                    if (e < m) {
-                        const int q = e / n_occ, i = e - q * n_occ;
-                        acc += qv[u] * (pc[i] * gc[q]);
-                    }
-                }
-            }
-            acc = kq_warp_sum(acc);
-            if (lane == 0) g.W[(size_t)k * KQ_CMAX + c] = acc;
-        }
-        __threadfence();
-        grid.sync();
         KQ_MARK(2);
         // ---- P4: y_c = a_c - Q W(:, c) on the owned rows, exact norms (per-CTA partials)
         {
@@ -207,6 +181,7 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
             double* sacc = qs;  // scratch: slices x nrow
             const int rr = t % max(nrow, 1), sl = t / max(nrow, 1);
             for (int c = 0; c < nc; ++c) {
+                const int ac = __ldcg(&g.cand[par * KQ_CMAX + c]);
                 if (nrow > 0 && sl < slices) {
                     const int e = e0 + rr;
                     double s = 0.0;
@@ -216,7 +191,7 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
                         for (int u = 0; u < KQ_U; ++u) {  // eight independent load pairs in flight
                             const int k = kb + u * slices;
                             qv[u] = k < j ? __ldcg(&g.Q[(size_t)k * m + e]) : 0.0;
-                            wv[u] = k < j ? __ldcg(&g.W[(size_t)k * KQ_CMAX + c]) : 0.0;
+                            wv[u] = k < j ? __ldcg(&g.Rrows[(size_t)k * Ng + ac]) : 0.0;
                         }
 #pragma unroll
                         for (int u = 0; u < KQ_U; ++u) s += qv[u] * wv[u];
@@ -373,7 +348,7 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
             if (t < nrow) g.Q[(size_t)j * m + e0 + t] = qs[t] / nrm;
             // R11(:, j) = Q^T a_w (first pass + correction), spread over all CTAs
             for (int k = b * KQ_T + t; k < j; k += G * KQ_T)
-                g.R11[(size_t)j * g.kmax + k] = __ldcg(&g.W[(size_t)k * KQ_CMAX + wc]) + __ldcg(&g.w2[k]);
+                g.R11[(size_t)j * g.kmax + k] = __ldcg(&g.Rrows[(size_t)k * Ng + aw]) + __ldcg(&g.w2[k]);
             if (b == 0 && t == 0) {
                 g.R11[(size_t)j * g.kmax + j] = nrm;
                 g.piv[j] = aw;
@@ -512,7 +487,6 @@ int kq_compress(acp_context* ctx, const double* Psi, const double* Gt, int r, in
     g.rdiag = ctx->wsd("kq_rdiag", kmax);
     g.slots = ctx->wsd("kq_slots", 4 * (size_t)sms);
     g.tpart = ctx->wsd("kq_tpart", 4 * (size_t)sms * KQ_CMAX);
-    g.W = ctx->wsd("kq_W", (size_t)kmax * KQ_CMAX);
     g.Y = ctx->wsd("kq_Y", (size_t)KQ_CMAX * m);
     g.w2 = ctx->wsd("kq_w2", kmax);
     g.cand = ctx->wsi("kq_cand", 2 * KQ_CMAX);

@@ -50,10 +50,16 @@ def _load(name):
     return gold, gs
 
 
-@pytest.mark.parametrize("name", ["c2_1d_semiconductor", "c3g_2d_8x8", "c4g_2d_16x16"])
+def _outer_only(gold) -> bool:
+    import json
+    return bool(json.loads(str(gold["meta"])).get("outer_only", 0))
+
+
+@pytest.mark.parametrize("name", ["c2_1d_semiconductor", "c3g_2d_8x8"])
 def test_full_size_alg4_and_D(name):
     from paper_1605_08021_b200 import Context
     gold, gs = _load(name)
+    assert not _outer_only(gold)
     cfg = get_config(name)
     R = atom_positions(cfg)
     assert np.array_equal(R, gs["R"])
@@ -97,6 +103,34 @@ def test_full_size_alg4_and_D(name):
     assert rel(D2, gold["D"]) < 1e-8, rel(D2, gold["D"])
     assert np.abs(lam2 - gold["lam"]).max() / np.abs(gold["lam"]).max() < 1e-7
     assert np.allclose(info["diff"], gold["diff"], rtol=1e-6)
+    ctx.close()
+
+
+def test_full_size_c4g_outer0():
+    """configs[4] (as c4g): the oracle's full Alg. 4 needs ~85k MINRES solves on the 256^2 grid
+    (days of host CPU), so its golden run (tools/make_golden.py --outer-only 1) holds outer
+    iteration 0 only: Alg. 2 on G' = G at m = N_occ r = 4096 (pivots and N_mu bit-exact) and
+    Eq. eqncompressU + Eq. eqnW on the seeded mu-sample (W to 1e-9) -- the production path
+    bench.py times (structured Kronecker QRCP, fused 2D K1, K2/K3 at N_occ = 256)."""
+    from paper_1605_08021_b200 import Context
+    name = "c4g_2d_16x16"
+    gold, gs = _load(name)
+    assert _outer_only(gold)
+    cfg = get_config(name)
+    R = atom_positions(cfg)
+    assert np.array_equal(R, gs["R"])
+    G = Model(cfg, R).G_matrix()
+    ctx = Context.from_config(cfg)
+    Psi_t, eps_t, V_t = T(gs["Psi"].T), T(gs["eps"]), T(gs["V"])
+    th, nu = sketch_draws(cfg.seed, 0, G.shape[1], cfg.sketch_r)
+    S, Xi, nk = ctx.compress(Psi_t, T(G.T), th, nu, id_eps=cfg.id_eps)
+    assert nk == int(gold["n_mu"][0]), (nk, int(gold["n_mu"][0]))
+    assert np.array_equal(S.cpu().numpy(), gold["S"]), "pivots differ at outer 0"
+    idx = torch.as_tensor(gold["W0_idx"], device="cuda")
+    # the sampled mu-columns only (their solves are independent of the other columns')
+    W, info = ctx.apply_chi0(Psi_t, eps_t, V_t, S[idx].contiguous(), Xi[idx].contiguous(), cfg.n_cheb,
+                             cg_tol=cfg.cg_tol)
+    assert rel(W.cpu().numpy().T, gold["W0"]) < 1e-9, rel(W.cpu().numpy().T, gold["W0"])
     ctx.close()
 
 

@@ -1,6 +1,6 @@
 """Write the oracle's end-to-end results for one full-size config (calls only oracle/ + workloads/).
 
-  python tools/make_golden.py <config> [--outer-only K]
+  python tools/make_golden.py <config> [--outer-only 1]
 
 Produces
   tests/cache/<config>_gs.npz      the oracle's ground state (Psi, eps, V, rho) -- the INPUT the GPU
@@ -55,6 +55,12 @@ def main():
     ap.add_argument("--minres-tol", type=float, default=1e-12)
     ap.add_argument("--scf-tol", type=float, default=None)
     ap.add_argument("--minres-block", type=int, default=64)
+    ap.add_argument("--gs-only", action="store_true",
+                    help="(re)build the cached ground state (+ outer 0's interpolation vectors for bench.py) and "
+                         "check it against the committed golden file's input digest; no Alg. 4")
+    ap.add_argument("--outer-only", type=int, default=0,
+                    help="1: outer iteration 0 only -- pivots, N_mu and W on the mu-sample (configs[4]: "
+                         "the ~85k MINRES solves of the full Alg. 4 are days of CPU)")
     a = ap.parse_args()
     cfg = get_config(a.config)
     cache = os.path.join(ROOT, "tests", "cache")
@@ -91,6 +97,18 @@ def main():
         log(f"ground state: {gs.n_iter} SCF iterations, residual {gs.residual:.2e}, gap {gs.gap:.6f}")
     n_occ = cfg.n_occ
     G = m.G_matrix()
+    if a.gs_only:
+        dg = digest(Psi, eps, V, rho, R)
+        gp = os.path.join(gold, f"{cfg.name}_acp.npz")
+        if os.path.exists(gp):
+            want = str(np.load(gp)["input_digest"])
+            log(f"input digest {dg} vs golden {want}: {'MATCH' if dg == want else 'MISMATCH'}")
+        th, nu = sketch_draws(cfg.seed, 0, G.shape[1], cfg.sketch_r)
+        S, Xi, _ = oacp.compress(m, Psi, G, th, nu, cfg.id_eps)
+        np.savez(os.path.join(cache, f"{cfg.name}_xi0.npz"), Xi=np.ascontiguousarray(Xi[:, :N_XI]),
+                 S=np.asarray(S[:N_XI]))
+        log(f"outer 0 interpolation vectors cached (N_mu = {len(S)})")
+        return
     H = m.hamiltonian_dense(V) if dense else None
     solve = None if dense else oit.SternheimerMinres(m, V, Psi, tol=a.minres_tol, block=a.minres_block)
     samples = {}
@@ -105,6 +123,26 @@ def main():
                      S=np.asarray(S[:N_XI]))
 
     draws = lambda k, n: sketch_draws(cfg.seed, k, n, cfg.sketch_r)  # noqa: E731
+    if a.outer_only:
+        # Alg. 2 on G' = G (outer 0), then Eq. eqncompressU + Eq. eqnW for the
+        # sampled mu only: W's columns are independent (each solves its own right-hand sides)
+        th, nu = draws(0, G.shape[1])
+        S, Xi, _ = oacp.compress(m, Psi, G, th, nu, cfg.id_eps)
+        log(f"outer 0: N_mu = {len(S)}")
+        np.savez(os.path.join(cache, f"{cfg.name}_xi0.npz"), Xi=np.ascontiguousarray(Xi[:, :N_XI]),
+                 S=np.asarray(S[:N_XI]))
+        idx = w_sample(len(S), 0, cfg.seed)
+        W0 = oacp.compressed_W(m, H, Psi, eps[:n_occ], S[idx], np.ascontiguousarray(Xi[:, idx]), cfg.n_cheb,
+                               solve=solve)
+        out = dict(n_mu=np.asarray([len(S)]), S=np.asarray(S, dtype=np.int64), W0_idx=idx, W0=W0,
+                   input_digest=digest(Psi, eps, V, rho, R),
+                   meta=json.dumps(dict(config=cfg.name, outer_only=1,
+                                        path="dense" if dense else "matrix-free (LOBPCG + MINRES)",
+                                        minres_tol=None if dense else a.minres_tol,
+                                        seconds=round(time.time() - t_start, 1), script="tools/make_golden.py")))
+        np.savez_compressed(os.path.join(gold, f"{cfg.name}_acp.npz"), **out)
+        log("written (outer 0 only)")
+        return
     res = oacp.acp_dyson(m, H, Psi, eps[:n_occ], G, cfg.n_cheb, cfg.n_outer, cfg.id_eps, draws,
                          solve=solve, keep=False, log=log, on_outer=on_outer)
     D = ophonon.dynamical_matrix(m, rho, G, res.U)
