@@ -129,6 +129,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // threads' generic-proxy accesses of shared memory happen-before later bulk (async-proxy) writes
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+
 // ---------------------------------------------------------------- work items
 struct Item {
     int p, phase, q;   // pair, phase (0 A, 1 B, 2 C), item within the phase
@@ -473,6 +474,12 @@ __global__ void __launch_bounds__(256, MB) k_f2c(F2cArgs g) {
             }
             __syncthreads();
             if (t == 0) {
+                // an inactive pair's items do no work but still keep the ring's slot chain: its
+                // counts tell pair p + R that the slot is free, so they may only be given after the
+                // slot's previous user (pair p - R) is done with it -- counting them at once let
+                // pair p + R overwrite S1 / S2 while pair p - R still read them (outer 1 of c4g:
+                // PCG iteration counts varied between identical steps, once no convergence)
+                if (cur.skip == 1) deps_ready<N>(g, cur, true);
                 __threadfence();
                 atomicAdd(&cnt[3 * cur.p + cur.phase], 1);
             }

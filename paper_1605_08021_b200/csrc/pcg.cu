@@ -328,6 +328,15 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update_xl(int M, int K, int n, c
     nn_tile_xl<Ep, ST>(M, K, n, A, lda, B, ldb, blockIdx.x * XL_BM, n0, ep);
 }
 
+// N_occ >= 64, warp-specialised persistent form of the 128 x 64 tile (nn_ws_persistent).
+template <class Ep>
+__global__ void __launch_bounds__(WS_T, 1) k_pcg_update_ws(int M, int K, int n, const double* __restrict__ A, int lda,
+                                                           const double* __restrict__ B, int ldb, Ep ep) {
+    pdl_wait();
+    pdl_trigger();
+    nn_ws_persistent<Ep>(M, K, n, A, lda, B, ldb, ep);
+}
+
 template <class Ep>
 static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const double* A, int lda, const double* B,
                               int ldb, const Ep& ep) {
@@ -342,7 +351,23 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
     // columns, 11.13 vs 12.85 s per step (same box); 4 stages: 5.73 / 7.00 ms
     // (c3g, N_occ = 64: 651 vs 698 ms per step with the 64 x 64 tile)
     static const int xl_mink = getenv("ACP_K3_XL_MINK") ? atoi(getenv("ACP_K3_XL_MINK")) : 64;
-    if (K >= xl_mink) {
+    // warp-specialised persistent form for 64 <= N_occ < 256 (same box, ws / xl: c3g EpBeta 2.49 / 2.62,
+    // EpAlpha 2.98 / 3.39 ms per 7680 columns; c2 0.276 / 0.302, 0.294 / 0.355 ms per 4096); at N_occ
+    // = 256 one CTA of 8 DMMA warps per SM is slower than two XL CTAs (c4g EpBeta 5.90 vs 5.46 ms)
+    static const int ws_env = getenv("ACP_K3_WS") ? atoi(getenv("ACP_K3_WS")) : -1;
+    const bool ws = ws_env >= 0 ? ws_env != 0 : K < 256;
+    if (K >= xl_mink && ws) {
+        auto kern = k_pcg_update_ws<Ep>;
+        const size_t smem = nn_ws_smem();
+        func_attr((const void*)kern, (int)smem);
+        int sms = 148;
+        ACP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        const long long tiles = (long long)cdiv(M, XL_BM) * cdiv(n, XL_BN);
+        cfg.gridDim = dim3((unsigned)std::min<long long>(sms, tiles), 1, 1);
+        cfg.blockDim = dim3(WS_T, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, M, K, n, A, lda, B, ldb, ep));
+    } else if (K >= xl_mink) {
         auto kern = k_pcg_update_xl<Ep, 3>;
         const size_t smem = nn_xl_smem<3>();
         func_attr((const void*)kern, (int)smem);
