@@ -53,6 +53,37 @@ def test_free_electron_chi0_full_grid(name, m2max):
     ctx.close()
 
 
+def test_free_electron_chi0_c4g_grid_inactive_pairs():
+    """The configs[4] grid (256 x 256: the fused persistent 2D K1 with its ring of plane slots) with
+    2400 column pairs, two thirds of them inactive from the start (zero right-hand sides) and
+    interleaved with active ones: inactive pairs must still keep the ring's slot chain (a count
+    given too early let pair p + R overwrite a plane pair p - R still read).  W against the
+    free-electron closed form, zero columns exactly zero, and two runs bitwise equal."""
+    from paper_1605_08021_b200 import Context
+    base = get_config("c4g_2d_16x16")
+    Psi, eps, occ = plane_wave_ground_state(base.grid, base.cell, 18)
+    n_occ = Psi.shape[1]
+    cfg = dataclasses.replace(base, n_occ=n_occ)
+    m = Model(cfg, np.zeros((cfg.n_atoms, cfg.dim)))
+    rng = np.random.default_rng(77)
+    n_mu = 400
+    S = np.sort(rng.choice(m.Ng, n_mu, replace=False)).astype(np.int32)
+    Xi = rng.standard_normal((m.Ng, n_mu)) * rng.uniform(0.1, 10.0, n_mu)
+    live = (np.arange(n_mu) // 2) % 3 == 0
+    Xi[:, ~live] = 0.0
+    ctx = Context.from_config(cfg)
+    args = (T(Psi.T), T(eps), T(np.zeros(m.Ng)), T(S, torch.int32), T(Xi.T), cfg.n_cheb)
+    W1, info = ctx.apply_chi0(*args, cg_tol=1e-11, max_iter=4000)
+    W2, _ = ctx.apply_chi0(*args, cg_tol=1e-11, max_iter=4000)
+    assert torch.equal(W1, W2), "apply_chi0 is not reproducible"
+    assert info["n_solved"] == cfg.n_cheb * int(live.sum()) and info["max_rel_res"] <= 1e-11
+    Wg = W1.cpu().numpy().T
+    assert not Wg[:, ~live].any()
+    W_o = oacp.compressed_W_free_electron(m, Psi, eps, occ, S[live], Xi[:, live], cfg.n_cheb)
+    assert rel(Wg[:, live], W_o) < 1e-8
+    ctx.close()
+
+
 @pytest.mark.parametrize("name", ["c2_1d_semiconductor", "c3g_2d_8x8"])
 def test_smw_update_full_size(name):
     from paper_1605_08021_b200 import Context
