@@ -239,6 +239,7 @@ int acp_sym_eigvals(acp_context* ctx, int n, const double* d_A, double* d_w);
  *           2: K3 fused update Y <- (X - Psi C) + beta Y (NN DMMA tile + PCG epilogue EpBeta)
  *           3: K3 with the EpAlpha epilogue: Ap = X - Psi C, Y += alpha P, R -= alpha Ap
  *              (P, R: library workspace of N_g x n_cols each)
+ *           4: K3 main loop only (an epilogue that moves no data; timing probe)
  * d_Psi: N_g x n_occ; d_X, d_Y: N_g x n_cols. */
 int acp_kernel_bench(acp_context* ctx, int which, const double* d_Psi, const double* d_V, const double* d_X,
                      int n_cols, double* d_Y, int reps);

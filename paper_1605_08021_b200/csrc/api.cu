@@ -294,7 +294,7 @@ int acp_sym_eigvals(acp_context* ctx, int n, const double* d_A, double* d_w) {
 
 int acp_kernel_bench(acp_context* ctx, int which, const double* d_Psi, const double* d_V, const double* d_X,
                      int n_cols, double* d_Y, int reps) {
-    if (!ctx || !d_Psi || !d_V || !d_X || !d_Y || n_cols < 1 || reps < 1 || which < 0 || which > 3)
+    if (!ctx || !d_Psi || !d_V || !d_X || !d_Y || n_cols < 1 || reps < 1 || which < 0 || which > 4)
         return ACP_ERR_INVALID;
     return guarded(ctx, [&] { acp::kernel_bench(ctx, which, d_Psi, d_V, d_X, n_cols, d_Y, reps); });
 }

@@ -340,6 +340,7 @@ __device__ __forceinline__ void nn_tile_big(int M, int K, int n, const double* _
 // quarter's global loads in flight together).  A operand rows are 1.33x as long per byte of B as in
 // the 64 x 64 tile, so the L2 -> SM operand stream per flop drops by a quarter.
 constexpr int XL_BM = 128, XL_BN = 64, XL_BK = 16, XL_ST = 3, XL_LDA = XL_BM + 4, XL_LDB = XL_BK + 4;
+constexpr int XL_GM = 16;   // m-tiles per rasterisation group
 
 template <int ST = XL_ST>
 constexpr size_t nn_xl_smem() { return (size_t)ST * (XL_BK * XL_LDA + XL_BN * XL_LDB) * sizeof(double); }
@@ -627,17 +628,21 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
     constexpr int TI = WTM / 8;               // DMMA tiles along m per warp
     const int CS = gridDim.x;
     const int rank = blockIdx.x;              // == cluster rank (cluster = (CS,1,1))
-    const int n0 = blockIdx.y * TC_BN, m0 = blockIdx.z * BM;
+    // (walking the m-tiles of a column tile back to back, so its B slice is read from HBM once,
+    // measured slower: c4g 4096 columns 4.95 vs 4.77 ms, 38088 columns 50.2 vs 46.9 ms)
+    const int mt = gridDim.z;
+    const int mtile = blockIdx.z;
+    const int n0 = blockIdx.y * TC_BN, m0 = mtile * BM;
     pdl_wait();
     pdl_trigger();
     // Column tiles whose columns have all converged are skipped.  The decision must be uniform
     // over the cluster (a CTA that leaves early would strand its peers at the cluster barrier and
-    // DSMEM reads).  With one m-tile (gridDim.z == 1) the only writer of the flags is this
+    // DSMEM reads).  With one m-tile (mt == 1) the only writer of the flags is this
     // cluster's own hook, which runs after the barrier below, so every rank reads the same
     // values.  With several m-tiles the hook of the z = 0 cluster may flip the flags while the
     // z > 0 clusters of the same column tile read them: there rank 0 decides and pushes its
     // decision to every peer before a cluster barrier.
-    if (gridDim.z == 1) {
+    if (mt == 1) {
         if (!hook.tile_active(n0, n)) return;
     } else {
         __shared__ int s_act;
@@ -730,7 +735,7 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
         const int gm = m0 + row, gn = n0 + col;
         if (gm < m && gn < n) C[(size_t)gn * ldc + gm] = alpha * s;
     }
-    if (rank == 0 && blockIdx.z == 0 && tid < TC_BN && n0 + tid < n) hook(n0 + tid);
+    if (rank == 0 && mtile == 0 && tid < TC_BN && n0 + tid < n) hook(n0 + tid);
     cluster.sync();
 }
 
