@@ -326,35 +326,25 @@ __global__ void __launch_bounds__(256, MINB) k_pcg_update_big(int M, int K, int 
 // N_occ >= 128: 128 x 64 tiles (nn_tile_xl), two CTAs per SM.
 template <class Ep, int ST = XL_ST>
 __global__ void __launch_bounds__(256, 2) k_pcg_update_xl(int M, int K, int n, const double* __restrict__ A, int lda,
-                                                          const double* __restrict__ B, int ldb, Ep ep, int stagger_ns) {
+                                                          const double* __restrict__ B, int ldb, Ep ep) {
     pdl_wait();
     pdl_trigger();
     // grouped rasterisation: XL_GM m-tiles (XL_GM x 128 rows of Psi, 4 MB at N_occ = 256) sweep
     // all column tiles together, so Psi is read from HBM once per launch instead of once per column
     // tile (c4g, 4096 columns: 8.6 GB of the kernel's 12.9 GB DRAM reads were Psi re-reads)
-    const int mt = (M + XL_BM - 1) / XL_BM, nt = (n + XL_BN - 1) / XL_BN, ntiles = mt * nt;
-    // persistent (two CTAs per SM, static tile walk); the second half of the grid starts ~half a
-    // tile later, so the two CTAs of an SM stay out of phase and one's HBM-bound epilogue overlaps
-    // the other's DMMA main loop (in lockstep both ran their epilogues at once)
-    if (stagger_ns > 0 && blockIdx.x >= gridDim.x / 2) {
-        const long long t0 = clock64();
-        while (clock64() - t0 < (long long)stagger_ns * 2) { }
-    }
+    const int mt = (M + XL_BM - 1) / XL_BM, nt = (n + XL_BN - 1) / XL_BN;
+    const int b = blockIdx.x, grp = b / (XL_GM * nt), gm0 = grp * XL_GM, gsz = min(XL_GM, mt - gm0);
+    const int loc = b - grp * XL_GM * nt;
+    const int m0 = (gm0 + loc % gsz) * XL_BM, n0 = (loc / gsz) * XL_BN;
     __shared__ int any;
-    for (int b = blockIdx.x; b < ntiles; b += gridDim.x) {
-        const int grp = b / (XL_GM * nt), gm0 = grp * XL_GM, gsz = min(XL_GM, mt - gm0);
-        const int loc = b - grp * XL_GM * nt;
-        const int m0 = (gm0 + loc % gsz) * XL_BM, n0 = (loc / gsz) * XL_BN;
-        __syncthreads();   // the previous tile's shared-memory reads are done
-        if (threadIdx.x == 0) {
-            int a = 0;
-            for (int c = n0; c < min(n, n0 + XL_BN); ++c) a |= ep.active[c];
-            any = a;
-        }
-        __syncthreads();
-        if (!any) continue;
-        nn_tile_xl<Ep, ST>(M, K, n, A, lda, B, ldb, m0, n0, ep);
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int c = n0; c < min(n, n0 + XL_BN); ++c) a |= ep.active[c];
+        any = a;
     }
+    __syncthreads();
+    if (!any) return;
+    nn_tile_xl<Ep, ST>(M, K, n, A, lda, B, ldb, m0, n0, ep);
 }
 
 // N_occ >= 64, warp-specialised persistent form of the 128 x 64 tile (nn_ws_persistent).
@@ -400,14 +390,10 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
         auto kern = k_pcg_update_xl<Ep, 3>;
         const size_t smem = nn_xl_smem<3>();
         func_attr((const void*)kern, (int)smem);
-        int sms = 148;
-        ACP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-        const long long tiles = (long long)cdiv(M, XL_BM) * cdiv(n, XL_BN);
-        static const int stagger = getenv("ACP_K3_STAGGER") ? atoi(getenv("ACP_K3_STAGGER")) : 20000;
-        cfg.gridDim = dim3((unsigned)std::min<long long>(2LL * sms, tiles), 1, 1);
+        cfg.gridDim = dim3((unsigned)((long long)cdiv(M, XL_BM) * cdiv(n, XL_BN)), 1, 1);
         cfg.blockDim = dim3(256, 1, 1);
         cfg.dynamicSmemBytes = smem;
-        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, M, K, n, A, lda, B, ldb, ep, stagger));
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, M, K, n, A, lda, B, ldb, ep));
     } else if (K >= 64) {
         // epilogue order 1 (nn_tile_big: both halves loaded after the K loop), same-box A/B:
         // configs[3] 836.8 / 824.9 / 828.2 ms and configs[2] 252.0 / 251.0 / 252.8 ms per step for
