@@ -604,6 +604,7 @@ constexpr int TC_BN = 32, TC_BK = 32, TC_PAD = 4, TC_ST = 4;  // TC_ST-stage cp.
 struct NoHook {
     __device__ __forceinline__ void operator()(int) const {}
     __device__ __forceinline__ bool tile_active(int, int) const { return true; }
+    __device__ __forceinline__ bool tile_active_w(int, int, int) const { return true; }
 };
 
 template <int BM, int ST = TC_ST>
@@ -741,6 +742,130 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
 
 // K split of the cluster projection: CS <= 8 ranks of kchunk rows (~160 per rank).  (Short K over
 // up to 16 ranks, one memory latency per rank, measured slower on configs[1]: K2 17.5 vs 13.3 us.)
+// 128 x 64 output tile of the split-K TN GEMM for m >= 128 (K2 at N_occ >= 128): 256 threads as
+// 4 (m) x 2 (n) warps with 32 x 32 warp tiles (4 x 4 DMMA tiles: 8 shared loads per 16 DMMAs, the
+// tile shape of the K3 main loop that reached 0.85 of the FP64 peak), 2-stage cp.async ring of
+// 32-deep K slices (110 KB: two CTAs per SM), the same cluster split of K with the partial tiles
+// reduced over the cluster in rank order through DSMEM, and the same per-column hook.
+constexpr int TX_BM = 128, TX_BN = 64, TX_ST = 2;
+constexpr size_t tn_xl_smem() { return (size_t)TX_ST * (TX_BM + TX_BN) * (TC_BK + TC_PAD) * sizeof(double); }
+
+template <class Hook>
+__global__ void __launch_bounds__(256, 2) k_tn_cluster_xl(int K, int m, int n, const double* __restrict__ A, int lda,
+                                                          const double* __restrict__ B, int ldb, int kchunk,
+                                                          double alpha, double* __restrict__ C, int ldc, Hook hook) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) double tsm[];
+    constexpr int LD = TC_BK + TC_PAD, ST = TX_ST;
+    double* As = tsm;                           // [ST][TX_BM][LD]  A(k, m) at [m][k]
+    double* Bs = tsm + ST * TX_BM * LD;         // [ST][TX_BN][LD]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
+    const int CS = gridDim.x;
+    const int rank = blockIdx.x;
+    const int n0 = blockIdx.y * TX_BN, m0 = blockIdx.z * TX_BM;
+    pdl_wait();
+    pdl_trigger();
+    // tile skipping decided uniformly per cluster (see k_tn_cluster)
+    if (gridDim.z == 1) {
+        if (!hook.tile_active_w(n0, n, TX_BN)) return;
+    } else {
+        __shared__ int s_act;
+        if (rank == 0 && tid < CS) {
+            const int act = hook.tile_active_w(n0, n, TX_BN) ? 1 : 0;
+            *cluster.map_shared_rank(&s_act, tid) = act;
+        }
+        cluster.sync();
+        if (!s_act) return;
+    }
+    const int kb = rank * kchunk;
+    const int ke = min(K, kb + kchunk);
+    const int nk = ke > kb ? (ke - kb + TC_BK - 1) / TC_BK : 0;
+    auto load_stage = [&](int s, int k0) {
+        double* as = As + s * TX_BM * LD;
+        double* bs = Bs + s * TX_BN * LD;
+#pragma unroll
+        for (int q = 0; q < (TX_BM * (TC_BK / 2)) / 256; ++q) {
+            const int c = tid + q * 256;
+            const int row = c / (TC_BK / 2), kk = 2 * (c % (TC_BK / 2));
+            const int gm = m0 + row, gk = k0 + kk;
+            const bool v = gm < m && gk < ke;
+            cp_async16(as + row * LD + kk, v ? (const void*)(A + (size_t)gm * lda + gk) : (const void*)A, v);
+        }
+#pragma unroll
+        for (int q = 0; q < (TX_BN * (TC_BK / 2)) / 256; ++q) {
+            const int c = tid + q * 256;
+            const int col = c / (TC_BK / 2), kk = 2 * (c % (TC_BK / 2));
+            const int gn = n0 + col, gk = k0 + kk;
+            const bool v = gn < n && gk < ke;
+            cp_async16(bs + col * LD + kk, v ? (const void*)(B + (size_t)gn * ldb + gk) : (const void*)B, v);
+        }
+    };
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int st = 0; st < ST - 1; ++st) {
+        if (st < nk) load_stage(st, kb + st * TC_BK);
+        cp_async_commit();
+    }
+    for (int it = 0; it < nk; ++it) {
+        const int nxt = it + ST - 1;
+        if (nxt < nk) load_stage(nxt % ST, kb + nxt * TC_BK);
+        cp_async_commit();
+        cp_async_wait<ST - 1>();
+        __syncthreads();
+        const double* as = As + (it % ST) * TX_BM * LD + (wm * 32 + g) * LD + t;
+        const double* bs = Bs + (it % ST) * TX_BN * LD + (wn * 32 + g) * LD + t;
+#pragma unroll
+        for (int ks = 0; ks < TC_BK; ks += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = as[i * 8 * LD + ks];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = bs[j * 8 * LD + ks];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    constexpr int LDC = TX_BN + 1;
+    double* Cs = tsm;   // [TX_BM][LDC] (67 KB, inside the 110 KB ring)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                Cs[(wm * 32 + i * 8 + g) * LDC + wn * 32 + j * 8 + 2 * t + e] = acc[i][j][e];
+    cluster.sync();
+    for (int e = rank * 256 + tid; e < TX_BM * TX_BN; e += CS * 256) {
+        const int row = e % TX_BM, col = e / TX_BM;
+        double part[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) part[q] = q < CS ? cluster.map_shared_rank(Cs, q)[row * LDC + col] : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) s += part[q];
+        const int gm = m0 + row, gn = n0 + col;
+        if (gm < m && gn < n) C[(size_t)gn * ldc + gm] = alpha * s;
+    }
+    if (rank == 0 && blockIdx.z == 0 && tid < TX_BN && n0 + tid < n) hook(n0 + tid);
+    cluster.sync();
+}
+
+inline bool tn_xl_on() {
+    static const int v = getenv("ACP_K2_XL") ? atoi(getenv("ACP_K2_XL")) : 1;
+    return v != 0;
+}
 inline void tn_split(int K, int& CS, int& kchunk) {
     CS = std::min(8, std::max(1, cdiv(K, 160)));
     kchunk = cdiv(cdiv(K, CS), TC_BK) * TC_BK;
@@ -772,6 +897,15 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
         cfg.dynamicSmemBytes = tn_cluster_smem<32>();
         func_attr((const void*)k_tn_cluster<32, Hook>, (int)tn_cluster_smem<32>(), true);
         ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster<32, Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
+    } else if (m >= 256 && n >= 16384 && tn_xl_on()) {
+        // c4g production widths (38088 / 46848 columns): 44.9 vs 47.6 ms per 38088 columns; at 4096
+        // columns (5.26 vs 5.04 ms) and for N_occ = 128 (configs[2]: 0.513 vs 0.469 ms per 8192) the
+        // 64 x 32 tile wins (more clusters for the SMs)
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.gridDim = dim3(CS, cdiv(n, TX_BN), cdiv(m, TX_BM));
+        cfg.dynamicSmemBytes = tn_xl_smem();
+        func_attr((const void*)k_tn_cluster_xl<Hook>, (int)tn_xl_smem(), true);
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster_xl<Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
     } else {
         // 2-stage ring (55 KB -> up to 4 CTAs/SM instead of 2): K2 0.70 vs 0.52 of FP64 peak on
         // configs[2] (223 vs 241 ms/step), 0.78 vs 0.66 on configs[3] (745 vs 762) with 4 stages

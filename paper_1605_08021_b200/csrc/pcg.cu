@@ -86,10 +86,11 @@ struct ScalHook {
     double tol2;
     int n_valid_mu;
     int nmu_p;
-    __device__ __forceinline__ bool tile_active(int n0, int n) const {
+    __device__ __forceinline__ bool tile_active(int n0, int n) const { return tile_active_w(n0, n, 32); }
+    __device__ __forceinline__ bool tile_active_w(int n0, int n, int w) const {
         if (mode == SC_INIT) return true;
         int a = 0;
-        for (int c = n0; c < min(n, n0 + 32); ++c) a |= s.active[c];
+        for (int c = n0; c < min(n, n0 + w); ++c) a |= s.active[c];
         return a != 0;
     }
     __device__ __forceinline__ void operator()(int j) const {
