@@ -55,6 +55,9 @@ def main():
     ap.add_argument("--minres-tol", type=float, default=1e-12)
     ap.add_argument("--scf-tol", type=float, default=None)
     ap.add_argument("--minres-block", type=int, default=64)
+    ap.add_argument("--resume-res", type=float, default=None,
+                    help="SCF residual of the checkpointed density: sets the first LOBPCG tolerance on resume "
+                         "(otherwise the loose first-iteration one)")
     ap.add_argument("--gs-only", action="store_true",
                     help="(re)build the cached ground state (+ outer 0's interpolation vectors for bench.py) and "
                          "check it against the committed golden file's input digest; no Alg. 4")
@@ -90,7 +93,13 @@ def main():
             rho0 = np.load(ck) if os.path.exists(ck) else None
             if rho0 is not None:
                 log("resuming the SCF from the checkpointed density")
-            gs = scf(m, tol=a.scf_tol or 1e-9, eigensolver=oit.lobpcg_eigensolver(tol=1e-10), verbose=True,
+            es = oit.lobpcg_eigensolver(tol=1e-10)
+            if rho0 is not None and a.resume_res:
+                base = es
+
+                def es(model, V, nb, X0, scf_res=0.0):  # noqa: F811
+                    return base(model, V, nb, X0, scf_res if np.isfinite(scf_res) else a.resume_res)
+            gs = scf(m, tol=a.scf_tol or 1e-9, eigensolver=es, verbose=True,
                      rho0=rho0, checkpoint=lambda it, rho: np.save(ck, rho) if it % 5 == 0 else None)
         Psi, eps, V, rho = gs.Psi, gs.eps, gs.V, gs.rho
         np.savez(gs_path, Psi=Psi, eps=eps, V=V, rho=rho, R=R, residual=gs.residual, n_iter=gs.n_iter)
