@@ -345,7 +345,7 @@ constexpr int XL_GM = 16;   // m-tiles per rasterisation group
 template <int ST = XL_ST>
 constexpr size_t nn_xl_smem() { return (size_t)ST * (XL_BK * XL_LDA + XL_BN * XL_LDB) * sizeof(double); }
 
-template <class Ep, int ST = XL_ST>
+template <class Ep, int ST = XL_ST, bool SE = false>
 __device__ __forceinline__ void nn_tile_xl(int M, int K, int n, const double* __restrict__ A, int lda,
                                            const double* __restrict__ B, int ldb, int m0, int n0, const Ep& ep) {
     extern __shared__ __align__(16) double gsm[];
@@ -418,6 +418,37 @@ __device__ __forceinline__ void nn_tile_xl(int M, int K, int n, const double* __
         __syncthreads();
     }
     cp_async_wait<0>();
+    if constexpr (SE) {
+        // staged epilogue: the accumulators go through shared memory (the operand ring is free now),
+        // then thread = row (coalesced 256-byte column segments per warp) with the 64 accumulator
+        // registers released, so 16-32 elements' operand loads are in flight per thread
+        __syncthreads();
+        double* Cs = gsm;   // [XL_BN][XL_BM + 4]: 67.6 KB inside the 81 KB ring
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    Cs[(wn * 32 + j * 8 + 2 * t + e) * (XL_BM + 4) + wm * 32 + i * 8 + g] = acc[i][j][e];
+        __syncthreads();
+        const int r = tid % XL_BM, h = tid / XL_BM, row = m0 + r;
+        constexpr int EC = sizeof(typename Ep::Regs) > 24 ? 8 : 16;
+        for (int c0 = h * (XL_BN / 2); c0 < (h + 1) * (XL_BN / 2); c0 += EC) {
+            typename Ep::Regs regs[EC];
+#pragma unroll
+            for (int c = 0; c < EC; ++c) {
+                const int col = n0 + c0 + c;
+                if (row < M && col < n) ep.load(row, col, regs[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < EC; ++c) {
+                const int col = n0 + c0 + c;
+                if (row < M && col < n) ep.store(row, col, Cs[(c0 + c) * (XL_BM + 4) + r], regs[c]);
+            }
+        }
+        return;
+    }
     // epilogue in chunks of EC elements per thread (all of a chunk's global loads in flight together)
     constexpr int EJ = sizeof(typename Ep::Regs) > 24 ? 2 : 4;   // j-columns per chunk
 #pragma unroll

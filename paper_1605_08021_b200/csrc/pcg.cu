@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(256, MINB) k_pcg_update_big(int M, int K, int 
 }
 
 // N_occ >= 128: 128 x 64 tiles (nn_tile_xl), two CTAs per SM.
-template <class Ep, int ST = XL_ST>
+template <class Ep, int ST = XL_ST, bool SE = false>
 __global__ void __launch_bounds__(256, 2) k_pcg_update_xl(int M, int K, int n, const double* __restrict__ A, int lda,
                                                           const double* __restrict__ B, int ldb, Ep ep) {
     pdl_wait();
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update_xl(int M, int K, int n, c
     }
     __syncthreads();
     if (!any) return;
-    nn_tile_xl<Ep, ST>(M, K, n, A, lda, B, ldb, m0, n0, ep);
+    nn_tile_xl<Ep, ST, SE>(M, K, n, A, lda, B, ldb, m0, n0, ep);
 }
 
 // N_occ >= 64, warp-specialised persistent form of the 128 x 64 tile (nn_ws_persistent).
@@ -388,7 +388,10 @@ static void launch_pcg_update(acp_context* ctx, int M, int K, int n, const doubl
         cfg.dynamicSmemBytes = smem;
         ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, M, K, n, A, lda, B, ldb, ep));
     } else if (K >= xl_mink) {
-        auto kern = k_pcg_update_xl<Ep, 3>;
+        // staged epilogue (accumulators through shared memory, thread = row): c4g 38088 columns EpBeta
+        // 48.57 vs 50.39 ms, EpAlpha 50.87 vs 52.96 ms, step 10.12 vs 10.26 s
+        static const int se = getenv("ACP_K3_SE") ? atoi(getenv("ACP_K3_SE")) : 1;
+        auto kern = se ? k_pcg_update_xl<Ep, 3, true> : k_pcg_update_xl<Ep, 3, false>;
         const size_t smem = nn_xl_smem<3>();
         func_attr((const void*)kern, (int)smem);
         cfg.gridDim = dim3((unsigned)((long long)cdiv(M, XL_BM) * cdiv(n, XL_BN)), 1, 1);
