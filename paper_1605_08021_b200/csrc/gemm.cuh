@@ -778,17 +778,18 @@ __global__ void __launch_bounds__(128) k_tn_cluster(int K, int m, int n, const d
 // tile shape of the K3 main loop that reached 0.85 of the FP64 peak), 2-stage cp.async ring of
 // 32-deep K slices (110 KB: two CTAs per SM), the same cluster split of K with the partial tiles
 // reduced over the cluster in rank order through DSMEM, and the same per-column hook.
-constexpr int TX_BM = 128, TX_BN = 64, TX_ST = 2;
-constexpr size_t tn_xl_smem() { return (size_t)TX_ST * (TX_BM + TX_BN) * (TC_BK + TC_PAD) * sizeof(double); }
+constexpr int TX_BM = 128, TX_BN = 64;
+template <int BK, int ST>
+constexpr size_t tn_xl_smem() { return (size_t)ST * (TX_BM + TX_BN) * (BK + TC_PAD) * sizeof(double); }
 
-template <class Hook>
+template <class Hook, int BK = 32, int ST = 2>
 __global__ void __launch_bounds__(256, 2) k_tn_cluster_xl(int K, int m, int n, const double* __restrict__ A, int lda,
                                                           const double* __restrict__ B, int ldb, int kchunk,
                                                           double alpha, double* __restrict__ C, int ldc, Hook hook) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) double tsm[];
-    constexpr int LD = TC_BK + TC_PAD, ST = TX_ST;
+    constexpr int LD = BK + TC_PAD;
     double* As = tsm;                           // [ST][TX_BM][LD]  A(k, m) at [m][k]
     double* Bs = tsm + ST * TX_BM * LD;         // [ST][TX_BN][LD]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -813,22 +814,22 @@ __global__ void __launch_bounds__(256, 2) k_tn_cluster_xl(int K, int m, int n, c
     }
     const int kb = rank * kchunk;
     const int ke = min(K, kb + kchunk);
-    const int nk = ke > kb ? (ke - kb + TC_BK - 1) / TC_BK : 0;
+    const int nk = ke > kb ? (ke - kb + BK - 1) / BK : 0;
     auto load_stage = [&](int s, int k0) {
         double* as = As + s * TX_BM * LD;
         double* bs = Bs + s * TX_BN * LD;
 #pragma unroll
-        for (int q = 0; q < (TX_BM * (TC_BK / 2)) / 256; ++q) {
+        for (int q = 0; q < (TX_BM * (BK / 2)) / 256; ++q) {
             const int c = tid + q * 256;
-            const int row = c / (TC_BK / 2), kk = 2 * (c % (TC_BK / 2));
+            const int row = c / (BK / 2), kk = 2 * (c % (BK / 2));
             const int gm = m0 + row, gk = k0 + kk;
             const bool v = gm < m && gk < ke;
             cp_async16(as + row * LD + kk, v ? (const void*)(A + (size_t)gm * lda + gk) : (const void*)A, v);
         }
 #pragma unroll
-        for (int q = 0; q < (TX_BN * (TC_BK / 2)) / 256; ++q) {
+        for (int q = 0; q < (TX_BN * (BK / 2)) / 256; ++q) {
             const int c = tid + q * 256;
-            const int col = c / (TC_BK / 2), kk = 2 * (c % (TC_BK / 2));
+            const int col = c / (BK / 2), kk = 2 * (c % (BK / 2));
             const int gn = n0 + col, gk = k0 + kk;
             const bool v = gn < n && gk < ke;
             cp_async16(bs + col * LD + kk, v ? (const void*)(B + (size_t)gn * ldb + gk) : (const void*)B, v);
@@ -841,19 +842,19 @@ __global__ void __launch_bounds__(256, 2) k_tn_cluster_xl(int K, int m, int n, c
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
     for (int st = 0; st < ST - 1; ++st) {
-        if (st < nk) load_stage(st, kb + st * TC_BK);
+        if (st < nk) load_stage(st, kb + st * BK);
         cp_async_commit();
     }
     for (int it = 0; it < nk; ++it) {
         const int nxt = it + ST - 1;
-        if (nxt < nk) load_stage(nxt % ST, kb + nxt * TC_BK);
+        if (nxt < nk) load_stage(nxt % ST, kb + nxt * BK);
         cp_async_commit();
         cp_async_wait<ST - 1>();
         __syncthreads();
         const double* as = As + (it % ST) * TX_BM * LD + (wm * 32 + g) * LD + t;
         const double* bs = Bs + (it % ST) * TX_BN * LD + (wn * 32 + g) * LD + t;
 #pragma unroll
-        for (int ks = 0; ks < TC_BK; ks += 4) {
+        for (int ks = 0; ks < BK; ks += 4) {
             double af[4], bf[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) af[i] = as[i * 8 * LD + ks];
@@ -869,7 +870,7 @@ __global__ void __launch_bounds__(256, 2) k_tn_cluster_xl(int K, int m, int n, c
     cp_async_wait<0>();
     __syncthreads();
     constexpr int LDC = TX_BN + 1;
-    double* Cs = tsm;   // [TX_BM][LDC] (67 KB, inside the 110 KB ring)
+    double* Cs = tsm;   // [TX_BM][LDC] (67 KB, inside the >= 92 KB ring)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -934,9 +935,12 @@ bool launch_tn_cluster(acp_context* ctx, int K, int m, int n, double alpha, cons
         // 64 x 32 tile wins (more clusters for the SMs)
         cfg.blockDim = dim3(256, 1, 1);
         cfg.gridDim = dim3(CS, cdiv(n, TX_BN), cdiv(m, TX_BM));
-        cfg.dynamicSmemBytes = tn_xl_smem();
-        func_attr((const void*)k_tn_cluster_xl<Hook>, (int)tn_xl_smem(), true);
-        ACP_CUDA(cudaLaunchKernelEx(&cfg, k_tn_cluster_xl<Hook>, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
+        static const int v3 = getenv("ACP_K2_XL3") ? atoi(getenv("ACP_K2_XL3")) : 0;
+        auto kern = v3 ? k_tn_cluster_xl<Hook, 16, 3> : k_tn_cluster_xl<Hook, 32, 2>;
+        const size_t smem = v3 ? tn_xl_smem<16, 3>() : tn_xl_smem<32, 2>();
+        cfg.dynamicSmemBytes = smem;
+        func_attr((const void*)kern, (int)smem, true);
+        ACP_CUDA(cudaLaunchKernelEx(&cfg, kern, K, m, n, A, lda, B, ldb, kchunk, alpha, C, ldc, hook));
     } else {
         // 2-stage ring (55 KB -> up to 4 CTAs/SM instead of 2): K2 0.70 vs 0.52 of FP64 peak on
         // configs[2] (223 vs 241 ms/step), 0.78 vs 0.66 on configs[3] (745 vs 762) with 4 stages
