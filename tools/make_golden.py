@@ -3,8 +3,10 @@
   python tools/make_golden.py <config> [--outer-only 1]
 
 Produces
-  tests/cache/<config>_gs.npz      the oracle's ground state (Psi, eps, V, rho) -- the INPUT the GPU
-                                   parity test feeds to the CUDA path (git-ignored: up to 134 MB)
+  tests/golden/<config>_gs.npz     the oracle's ground state (Psi, eps, V, rho) -- the INPUT the GPU
+                                   parity test feeds to the CUDA path; committed when Psi is at most
+                                   GS_COMMIT_MAX bytes (configs[2], c3g), else tests/cache/ (c4g:
+                                   134 MB, git-ignored)
   tests/golden/<config>_acp.npz    the oracle's Alg. 4 + D results on that input (committed):
                                    per-outer N_mu, pivots S, ||U^k - U^{k-1}||, W on a seeded
                                    mu-sample, D, lambda, and a digest of the input arrays
@@ -35,6 +37,7 @@ from oracle import acp as oacp, iterative as oit, phonon as ophonon  # noqa: E40
 DENSE_MAX_NG = 6000
 N_W_SAMPLE = 6        # mu-columns of W stored per outer iteration
 N_XI = 32             # interpolation vectors of outer 0 kept for bench.py's oracle sample
+GS_COMMIT_MAX = 32 << 20   # ground states up to this size go to tests/golden/ (tracked)
 
 
 def digest(*arrays) -> str:
@@ -77,7 +80,10 @@ def main():
     R = atom_positions(cfg)
     m = Model(cfg, R)
     dense = m.Ng <= DENSE_MAX_NG
-    gs_path = os.path.join(cache, f"{cfg.name}_gs.npz")
+    small = m.Ng * cfg.n_occ * 8 <= GS_COMMIT_MAX
+    gs_path = os.path.join(gold if small else cache, f"{cfg.name}_gs.npz")
+    if not os.path.exists(gs_path) and os.path.exists(os.path.join(cache, f"{cfg.name}_gs.npz")):
+        gs_path = os.path.join(cache, f"{cfg.name}_gs.npz")
     if os.path.exists(gs_path):
         z = np.load(gs_path)
         Psi, eps, V, rho = z["Psi"], z["eps"], z["V"], z["rho"]
@@ -102,6 +108,7 @@ def main():
             gs = scf(m, tol=a.scf_tol or 1e-9, eigensolver=es, verbose=True,
                      rho0=rho0, checkpoint=lambda it, rho: np.save(ck, rho) if it % 5 == 0 else None)
         Psi, eps, V, rho = gs.Psi, gs.eps, gs.V, gs.rho
+        gs_path = os.path.join(gold if small else cache, f"{cfg.name}_gs.npz")
         np.savez(gs_path, Psi=Psi, eps=eps, V=V, rho=rho, R=R, residual=gs.residual, n_iter=gs.n_iter)
         log(f"ground state: {gs.n_iter} SCF iterations, residual {gs.residual:.2e}, gap {gs.gap:.6f}")
     n_occ = cfg.n_occ
