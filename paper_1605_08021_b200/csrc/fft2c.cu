@@ -27,13 +27,18 @@
 #include "common.cuh"
 #include "fft2c.cuh"
 
+// 16-line batches per queue item (A/B at build time: -DACP_F2C_BPI=1 / 4; run R5f)
+#ifndef ACP_F2C_BPI
+#define ACP_F2C_BPI 2
+#endif
+
 namespace acp {
 
 template <int N>
 struct F2C {
     static constexpr int N2 = N / 16;
     static constexpr int CS = N / 16;               // 16-line batches per phase and pair
-    static constexpr int BPI = CS >= 2 ? 2 : 1;     // batches per item
+    static constexpr int BPI = CS >= ACP_F2C_BPI ? ACP_F2C_BPI : 1;  // batches per item
     static constexpr int IPP = CS / BPI;            // items per phase and pair
     static constexpr int TB = N2 * 17 + 1;          // exchange row stride, steps 1 -> 2 (odd)
     static constexpr int TB2 = 16 * (N2 + 1) + 1;   // exchange row stride, inverse steps (odd)
@@ -52,7 +57,7 @@ static size_t f2c_smem(int N) {
     }
     return 0;
 }
-static int f2c_ipp(int N) { return (N / 16) / (N / 16 >= 2 ? 2 : 1); }
+static int f2c_ipp(int N) { return (N / 16) / (N / 16 >= ACP_F2C_BPI ? ACP_F2C_BPI : 1); }
 
 struct F2cArgs {
     FopArgs a;
@@ -551,8 +556,10 @@ static F2cGeom f2c_geom(acp_context* ctx) {
     const int ipp = f2c_ipp(N);
     F2cGeom G;
     G.grid = ctx->f2c_maxcl;
-    // the grid holds ~grid items at once (3 ipp per step); B / C items trail by d steps
-    G.d = (G.grid + 3 * ipp - 1) / (3 * ipp) + 2;
+    // the grid holds ~grid items at once (3 ipp per step); B / C items trail by d steps.  Twice
+    // the in-flight depth (c4g: d = 16, ring 36 slots = 72 MB, L2-resident): 26.96 vs 27.93 ms per
+    // 38088 columns at d = 9; d = 4 / 6 / 12 / 24 / 32: 35.5 / 31.9 / 27.0 / 27.05 / 27.7 (run R5b)
+    G.d = 2 * ((G.grid + 3 * ipp - 1) / (3 * ipp)) + 2;
     if (const char* e = getenv("ACP_F2C_SKEW")) G.d = std::max(1, atoi(e));
     G.R = 2 * G.d + 4;
     return G;
