@@ -27,9 +27,10 @@
 #include "common.cuh"
 #include "fft2c.cuh"
 
-// 16-line batches per queue item (A/B at build time: -DACP_F2C_BPI=1 / 4; run R5f)
+// 16-line batches per queue item (A/B at build time, -DACP_F2C_BPI=n).  c4g, 38088 columns, best queue
+// skew each: 1 -> 32.0 ms, 2 -> 26.94, 4 -> 25.50, 8 -> 26.1, 16 -> 28.8 (runs R5f, R5g)
 #ifndef ACP_F2C_BPI
-#define ACP_F2C_BPI 2
+#define ACP_F2C_BPI 4
 #endif
 
 namespace acp {
@@ -556,10 +557,11 @@ static F2cGeom f2c_geom(acp_context* ctx) {
     const int ipp = f2c_ipp(N);
     F2cGeom G;
     G.grid = ctx->f2c_maxcl;
-    // the grid holds ~grid items at once (3 ipp per step); B / C items trail by d steps.  Twice
-    // the in-flight depth (c4g: d = 16, ring 36 slots = 72 MB, L2-resident): 26.96 vs 27.93 ms per
-    // 38088 columns at d = 9; d = 4 / 6 / 12 / 24 / 32: 35.5 / 31.9 / 27.0 / 27.05 / 27.7 (run R5b)
-    G.d = 2 * ((G.grid + 3 * ipp - 1) / (3 * ipp)) + 2;
+    // the grid holds ~grid items at once (3 ipp per step); B / C items trail by d steps.  What
+    // matters is the ring (R = 2d + 4 slots, 2 MB each at 256^2): best at R ~ 36-44 (72-88 MB, L2-
+    // resident) -- c4g at 4 batches per item: d = 12 / 16 / 20 / 28 / 36: 27.9 / 25.54 / 25.50 / 26.1 /
+    // 27.0 ms; at 2 per item d = 9 / 16 / 32: 27.93 / 26.96 / 27.7 (runs R5b, R5g)
+    G.d = (G.grid + 3 * ipp - 1) / (3 * ipp) + 6;
     if (const char* e = getenv("ACP_F2C_SKEW")) G.d = std::max(1, atoi(e));
     G.R = 2 * G.d + 4;
     return G;
