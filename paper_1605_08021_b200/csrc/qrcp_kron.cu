@@ -52,6 +52,8 @@ struct KqArgs {
     int* out_nmu;
     int* overflow;       // set when more than CMAX columns were within the screening window
     long long* prof;     // debug (ACP_KQ_PROF): CTA 0's cycles per phase, summed over pivots, or null
+    int psi_keep;        // grid points a < psi_keep: Psi loads marked L2 evict_last, the rest evict_first
+    int q_last;          // 1: the passes over Q mark their loads L2 evict_last
 };
 
 #define KQ_MARK(ph)                                                          \
@@ -67,6 +69,28 @@ __device__ __forceinline__ void dmma_kq(double& d0, double& d1, double a, double
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
+}
+
+// Psi (N_g x N_occ, 134 MB at c4g) does not fit the 126 MB L2 and is streamed in the same order
+// every pivot: its loads carry an L2 policy (a share of the grid points may be pinned evict_last,
+// the rest streams evict_first) so that it does not flush Q from L2.
+__device__ __forceinline__ unsigned long long kq_pol(bool keep) {
+    unsigned long long p;
+    if (keep) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double kq_ld_ro(const double* a, unsigned long long pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+    return v;
+}
+// Q is written by the kernel itself: L2-only (cg) loads, optionally with a cache hint
+__device__ __forceinline__ double kq_ld_q(const double* a, bool hint, unsigned long long pol) {
+    if (!hint) return __ldcg(a);
+    double v;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+    return v;
 }
 
 __device__ __forceinline__ double kq_warp_sum(double v) {
@@ -110,6 +134,8 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
     double maxn0 = 0.0, r11 = 0.0;
     int N = g.kmax;
     long long tmark = (g.prof && b == 0 && t == 0) ? clock64() : 0;
+    const unsigned long long pkeep = kq_pol(true), pstream = kq_pol(false);
+    const bool qh = g.q_last != 0;
     // P1: per-CTA max of the screening norms (for pivot jn; also resets the candidate counter
     // pivot jn + 1 will use -- nobody touches it before then).  Run once here and then at the end
     // of every pivot's R-row pass, so it shares that pass's grid barrier.
@@ -190,7 +216,7 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
 #pragma unroll
                         for (int u = 0; u < KQ_U; ++u) {  // eight independent load pairs in flight
                             const int k = kb + u * slices;
-                            qv[u] = k < j ? __ldcg(&g.Q[(size_t)k * m + e]) : 0.0;
+                            qv[u] = k < j ? kq_ld_q(&g.Q[(size_t)k * m + e], qh, pkeep) : 0.0;
                             wv[u] = k < j ? __ldcg(&g.Rrows[(size_t)k * Ng + ac]) : 0.0;
                         }
 #pragma unroll
@@ -280,7 +306,7 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
 #pragma unroll
                 for (int u = 0; u < KQ_U; ++u) {
                     const int e = e0b + lane + 32 * u;
-                    qv[u] = e < m ? __ldcg(&qk[e]) : 0.0;
+                    qv[u] = e < m ? kq_ld_q(&qk[e], qh, pkeep) : 0.0;
                     yv[u] = e < m ? __ldcg(&yw[e]) : 0.0;
                 }
 #pragma unroll
@@ -306,7 +332,7 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
 #pragma unroll
                     for (int u = 0; u < KQ_U; ++u) {
                         const int k = kb + u * slices;
-                        qv[u] = k < j ? __ldcg(&g.Q[(size_t)k * m + e]) : 0.0;
+                        qv[u] = k < j ? kq_ld_q(&g.Q[(size_t)k * m + e], qh, pkeep) : 0.0;
                         wv[u] = k < j ? __ldcg(&g.w2[k]) : 0.0;
                     }
 #pragma unroll
@@ -385,12 +411,15 @@ __global__ void __launch_bounds__(KQ_T, 2) k_kq(KqArgs g) {
                 const int arow = a8 + gq;
                 const bool va = arow < a1;
                 double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+                const unsigned long long ppsi = a8 < g.psi_keep ? pkeep : pstream;  // warp-uniform
                 for (int ib = 0; ib < n_occ; ib += 4 * KQ_UP) {
                     double af[KQ_UP];
 #pragma unroll
                     for (int u = 0; u < KQ_UP; ++u) {  // KQ_UP fragments of psi in flight
                         const int i = ib + 4 * u + tq;
-                        af[u] = (va && i < n_occ) ? g.Psi[(size_t)i * Ng + arow] : 0.0;
+                        af[u] = (va && i < n_occ) ? (g.psi_keep < 0 ? g.Psi[(size_t)i * Ng + arow]
+                                                             : kq_ld_ro(&g.Psi[(size_t)i * Ng + arow], ppsi))
+                                               : 0.0;
                     }
 #pragma unroll
                     for (int u = 0; u < KQ_UP; ++u) {
@@ -493,6 +522,17 @@ int kq_compress(acp_context* ctx, const double* Psi, const double* Gt, int r, in
     g.ncand = ctx->wsi("kq_ncand", 4);
     g.out_nmu = ctx->wsi("kq_nmu", 1);
     g.overflow = ctx->wsi("kq_overflow", 1);
+    {
+        // share of Psi pinned in L2 across pivots (percent of the grid points; ACP_KQ_PSI_KEEP)
+        static const char* e = getenv("ACP_KQ_PSI_KEEP");
+        // default 0: the whole Psi pass streams evict_first, which keeps Q (the three passes per pivot)
+        // L2-resident -- c4g compress 417 vs 430 ms; pinning 30 / 50 / 70 / 90 % of Psi: 427 / 430 / 432 /
+        // 433 ms; Q loads evict_last: no change (run R5j).  < 0: plain loads.
+        const int pct = e ? std::min(100, atoi(e)) : 0;
+        g.psi_keep = pct < 0 ? -1 : (int)((long long)Ng * pct / 100);
+        static const char* eq = getenv("ACP_KQ_QLAST");
+        g.q_last = eq ? atoi(eq) : 0;
+    }
     static const bool prof = getenv("ACP_KQ_PROF") != nullptr;
     g.prof = prof ? reinterpret_cast<long long*>(ctx->ws("kq_prof", 16 * sizeof(long long))) : nullptr;
     if (prof) ACP_CUDA(cudaMemsetAsync(g.prof, 0, 16 * sizeof(long long), ctx->stream));
