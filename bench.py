@@ -227,12 +227,12 @@ def run_acp(args, cfg):
         if sharded:
             with torch.cuda.stream(stream):  # torch ops, NCCL and the library on the timed stream
                 U, info = dyson_sharded(ctx, Psi, eps, V, G, cfg.n_cheb, cfg.n_outer, lambda k: dr[k], cfg.id_eps,
-                                    cfg.cg_tol)
+                                    cfg.cg_tol, shard_compress={"auto": None, "on": True, "off": False}[args.shard_compress])
             solves = info["local_solves"]
             t = torch.tensor([solves], device=dev)
             dist.all_reduce(t)
             solves = int(t.item())
-            info = dict(total_solves=solves, n_mu=info["n_mu"])
+            info = dict(total_solves=solves, n_mu=info["n_mu"], compression=info["compression"])
         else:
             U, info = ctx.dyson(Psi, eps, V, G, cfg.n_cheb, cfg.n_outer, th, nu, id_eps=cfg.id_eps,
                                 cg_tol=cfg.cg_tol)
@@ -426,7 +426,7 @@ def run_acp(args, cfg):
                            "N_c": cfg.n_cheb, "n_outer": cfg.n_outer, "id_eps": cfg.id_eps, "r": cfg.sketch_r,
                            "cg_tol": cfg.cg_tol, "n_mu": info["n_mu"], "solves_per_step": solves // args.steps,
                            "l2": "flushed (256 MiB write) between timed steps",
-                           "ground_state_s": round(t_gs, 2), "parallelism": (f"compression + rhs shard x{world} (NCCL)" if sharded else "single GPU")},
+                           "ground_state_s": round(t_gs, 2), "parallelism": (f"rhs shard x{world} (NCCL all-gather of W), compression {info.get('compression', '?')}" if sharded else "single GPU")},
                 "roofline": roofline, "kernels": kern, "cpu_baseline": cpu,
                 "step_ms_each": [round(t, 3) for t in times],
                 "e2e": {"value": e2e_value, "unit": "solves/s", "ms_per_step": e2e_ms, "ms_each": e2e_each,
@@ -450,6 +450,9 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--dist", action="store_true",
                     help="run the multi-GPU code path (sharded compression, NCCL all-gathers) even at N = 1")
+    ap.add_argument("--shard-compress", default="auto", choices=["auto", "on", "off"],
+                    help="multi-GPU path: Alg. 2 sharded by grid point (on), replicated (off), or the measured "
+                         "rule of parallel.use_sharded_compress (auto: replicated up to 8 ranks)")
     args = ap.parse_args()
     from workloads import get_config
     cfg = get_config(args.config)

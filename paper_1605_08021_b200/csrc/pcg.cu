@@ -878,6 +878,40 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         k_pcg_x_final<<<dim3(cdiv(Ng, 1024), n), 256, 0, ctx->stream>>>(Ng, n, s.active, s.iters, s.alpha, P, X);
         launched(ctx);
     }
+    // ACP_PCG_ITERS_HIST: per Chebyshev node min / mean / max CG iterations and the share of the
+    // tile work (64-column tiles stay live until their slowest column converges) spent on columns
+    // that are still active (stderr; diagnostics only, forces a host wait)
+    static const bool iters_hist = getenv("ACP_PCG_ITERS_HIST") != nullptr;
+    if (iters_hist) {
+        ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::vector<int> it(n);
+        ACP_CUDA(cudaMemcpy(it.data(), s.iters, n * sizeof(int), cudaMemcpyDeviceToHost));
+        long long work = 0, tile_work = 0, all_work = 0;
+        int gmax = 0;
+        for (int c = 0; c < n_c; ++c) {
+            int lo = 1 << 30, hi = 0;
+            long long sum = 0;
+            for (int j = 0; j < nmu_p; ++j) {
+                const int v = it[(size_t)c * nmu_p + j];
+                lo = std::min(lo, v);
+                hi = std::max(hi, v);
+                sum += v;
+            }
+            gmax = std::max(gmax, hi);
+            fprintf(stderr, "[acp pcg iters] node %d: min %d mean %.2f max %d\n", c, lo, (double)sum / nmu_p, hi);
+        }
+        for (int t0 = 0; t0 < n; t0 += 64) {
+            int hi = 0;
+            for (int j = t0; j < std::min(n, t0 + 64); ++j) {
+                hi = std::max(hi, it[j]);
+                work += it[j];
+            }
+            tile_work += (long long)hi * std::min(64, n - t0);
+        }
+        all_work = (long long)gmax * n;
+        fprintf(stderr, "[acp pcg iters] n %d: column-iterations %lld, 64-column tile work %lld (%.3f useful), no-skip work %lld\n",
+                n, work, tile_work, (double)work / (double)tile_work, all_work);
+    }
     if (ctx->defer) {
         // no host wait: accumulate the statistics on the device (read at the end of acp_dyson)
         long long lpt[PCG_MAXG] = {};

@@ -23,6 +23,22 @@ import torch.distributed as dist
 
 CHECK_EVERY = 32   # pivot steps between stop-flag reads (later steps are device no-ops)
 
+# Ranks up to which the compression runs REPLICATED on every rank (the one-GPU Kronecker QRCP /
+# cluster QRCP) rather than with the per-pivot sharded protocol.  Measured on one B200 at c4g
+# (profiles/R6a_bench_c4g_dist_n1.json vs R6a_bench_c4g.json): the sharded protocol at world 1
+# costs 4.1 s per step (575 us per pivot: the rank's slice of the formed sketch is read and written
+# every pivot) against 0.77 s for the one-GPU kernel; scaled to 8 ranks the protocol is ~0.9 s
+# (slice / 8 + one all-gather per pivot), still not below the replicated 0.77 s.
+REPLICATED_COMPRESS_MAX_WORLD = 8
+
+
+def use_sharded_compress(world: int, shard_compress=None) -> bool:
+    """The compression mode of dyson_sharded: an explicit True / False wins; None = the measured
+    rule above (replicated up to one NVSwitch node of 8 ranks, sharded beyond)."""
+    if shard_compress is None:
+        return world > REPLICATED_COMPRESS_MAX_WORLD
+    return bool(shard_compress)
+
 
 def shard_bounds(n: int, rank: int, world: int) -> Tuple[int, int, int]:
     """Even-aligned contiguous shards: returns (begin, end, chunk) with chunk even."""
@@ -100,22 +116,25 @@ def _compress_sharded_loop(ops, Psi, Gp, theta, nu, id_eps, group, n_mu_fixed, a
 
 
 def dyson_sharded(ops, Psi, eps, V, G, n_cheb: int, n_outer: int, draws: Callable[[int], tuple],
-                  id_eps: float, cg_tol: float = 1e-11, group=None, shard_compress: bool = True):
+                  id_eps: float, cg_tol: float = 1e-11, group=None, shard_compress=None):
     """Alg. 4 (PAPER.md:765-795) on `world` ranks.
 
     `ops` provides qrs_* / compress / apply_chi0 / smw_update with the signatures of
     paper_1605_08021_b200.acp.Context (a GPU Context in production; tests pass a CPU stand-in to
-    exercise the sharding and gather logic under gloo).  Returns (U, info) with U identical on
-    every rank.
+    exercise the sharding and gather logic under gloo).  `shard_compress`: True = Alg. 2 sharded
+    by grid point (compress_sharded), False = replicated on every rank (same inputs, deterministic
+    kernels: identical S and Xi everywhere), None = use_sharded_compress(world).  Returns (U, info)
+    with U identical on every rank.
     """
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     Gp = G.clone()
     U = None
-    info = dict(n_mu=[], local_solves=0, shards=[])
+    sharded_c = use_sharded_compress(world, shard_compress)
+    info = dict(n_mu=[], local_solves=0, shards=[], compression="sharded" if sharded_c else "replicated")
     for k in range(n_outer):
         theta, nu = draws(k)
-        if shard_compress:
+        if sharded_c:
             S, Xi, n = compress_sharded(ops, Psi, Gp, theta, nu, id_eps, group)
         else:
             S, Xi, n = ops.compress(Psi, Gp, theta, nu, id_eps=id_eps)

@@ -151,9 +151,14 @@ def test_nccl_world1_sharded_alg4(name, nccl_world1):
     assert rel(Xi.cpu().numpy(), Xi1.cpu().numpy()) < 1e-10
     dr = [sketch_draws(cfg.seed, k, G.shape[1], cfg.sketch_r) for k in range(cfg.n_outer)]
     U, info = dyson_sharded(ctx, Psi, eps, V, Gt, cfg.n_cheb, cfg.n_outer, lambda k: dr[k], cfg.id_eps,
-                            cfg.cg_tol)
+                            cfg.cg_tol, shard_compress=True)
+    assert info["compression"] == "sharded"
+    Ur, infor = dyson_sharded(ctx, Psi, eps, V, Gt, cfg.n_cheb, cfg.n_outer, lambda k: dr[k], cfg.id_eps,
+                              cfg.cg_tol)   # the default rule at world 1: replicated compression
+    assert infor["compression"] == "replicated" and infor["n_mu"] == info["n_mu"]
     U1, info1 = ctx.dyson(Psi, eps, V, Gt, cfg.n_cheb, cfg.n_outer, np.stack([d[0] for d in dr]),
                           np.stack([d[1] for d in dr]), id_eps=cfg.id_eps, cg_tol=cfg.cg_tol)
     assert info["n_mu"] == info1["n_mu"]
     assert rel(U.cpu().numpy(), U1.cpu().numpy()) < 1e-9
+    assert rel(Ur.cpu().numpy(), U1.cpu().numpy()) < 1e-9
     ctx.close()

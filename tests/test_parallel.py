@@ -149,7 +149,7 @@ def _system():
     return cfg, m, gs
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, shard_compress=None):
     from workloads import sketch_draws
     from paper_1605_08021_b200.parallel import dyson_sharded
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -161,8 +161,9 @@ def _worker(rank, world, port, out):
         eps = torch.from_numpy(gs.eps[: cfg.n_occ].copy())
         V = torch.from_numpy(gs.V.copy())
         U, info = dyson_sharded(OracleOps(m, H), Psi, eps, V, G, cfg.n_cheb, cfg.n_outer,
-                                lambda k: sketch_draws(cfg.seed, k, G.shape[0], cfg.sketch_r), cfg.id_eps)
-        out[rank] = (U.numpy().copy(), info["shards"], info["local_solves"], info["n_mu"])
+                                lambda k: sketch_draws(cfg.seed, k, G.shape[0], cfg.sketch_r), cfg.id_eps,
+                                shard_compress=shard_compress)
+        out[rank] = (U.numpy().copy(), info["shards"], info["local_solves"], info["n_mu"], info["compression"])
     finally:
         dist.destroy_process_group()
 
@@ -213,20 +214,31 @@ def test_compress_sharded_matches_one_rank(world, fixed):
         assert np.abs(Xi.T - Xi_o).max() < 1e-10 * np.abs(Xi_o).max()
 
 
-def test_dyson_sharded_two_ranks_matches_single_process():
+def test_use_sharded_compress_rule():
+    """None = the measured rule (replicated up to one 8-rank NVSwitch node); explicit values win."""
+    from paper_1605_08021_b200.parallel import REPLICATED_COMPRESS_MAX_WORLD, use_sharded_compress
+    assert REPLICATED_COMPRESS_MAX_WORLD == 8
+    assert [use_sharded_compress(w) for w in (1, 2, 8, 9, 16)] == [False, False, False, True, True]
+    assert use_sharded_compress(2, True) and not use_sharded_compress(16, False)
+
+
+@pytest.mark.parametrize("shard_compress,mode", [(True, "sharded"), (False, "replicated"), (None, "replicated")])
+def test_dyson_sharded_two_ranks_matches_single_process(shard_compress, mode):
     from workloads import sketch_draws
     from oracle import acp as oacp
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, join=True, start_method="fork")
+    mp.start_processes(_worker, args=(world, _free_port(), out, shard_compress), nprocs=world, join=True,
+                       start_method="fork")
     cfg, m, gs = _system()
     H = m.hamiltonian_dense(gs.V)
     G = m.G_matrix()
     ref = oacp.acp_dyson(m, H, gs.Psi, gs.eps[: cfg.n_occ], G, cfg.n_cheb, cfg.n_outer, cfg.id_eps,
                          lambda k, n: sketch_draws(cfg.seed, k, n, cfg.sketch_r))
-    U0, sh0, ns0, nmu0 = out[0]
-    U1, sh1, ns1, nmu1 = out[1]
+    U0, sh0, ns0, nmu0, mode0 = out[0]
+    U1, sh1, ns1, nmu1, mode1 = out[1]
+    assert mode0 == mode1 == mode
     assert nmu0 == nmu1 == ref.n_mu
     assert np.array_equal(U0, U1)                      # replicated SMW: identical on every rank
     assert np.abs(U0.T - ref.U).max() <= 1e-12 * np.abs(ref.U).max()
