@@ -69,6 +69,7 @@ struct F2cArgs {
     double2* S;            // ring of R slots, 2 N^2 complex each (S1 then S2)
     int R;                 // ring slots
     int d;                 // queue skew (steps between A and B, B and C of a pair)
+    int discard;           // 1: a consumed plane block is dropped from L2 (discard.global.L2) instead of written back
     int npair;
     int nsteps;            // npair + 2 d
     int* queue;            // [0] = next item; then cnt[3 * npair] (A, B, C done-counts per pair)
@@ -456,6 +457,15 @@ __global__ void __launch_bounds__(256, MB) k_f2c(F2cArgs g) {
         if (cur.skip == 0) {
             mbar_wait(&bars[buf], uses[buf] & 1);
             ++uses[buf];
+            if (g.discard && cur.phase != 0) {
+                // the plane block of this batch (16 N complex, contiguous, read only by this batch)
+                // is in the stage now: its L2 lines hold dead data until pair p + R rewrites them
+                const size_t NN = (size_t)N * N;
+                const char* blk = reinterpret_cast<const char*>(
+                    g.S + (size_t)(cur.p % g.R) * 2 * NN + (cur.phase == 2 ? NN : 0) + (size_t)((cur.q * K::BPI + cb) * 16) * N);
+                for (int l = t; l < 16 * N * (int)sizeof(double2) / 128; l += 256)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(blk + (size_t)l * 128) : "memory");
+            }
             f2c_batch<N>(g, cur, cb, sm + (size_t)buf * K::BUF, tws, hk[0], hk[1], d);
             fence_proxy_async();  // this stage's generic accesses precede its next bulk refill
         }
@@ -592,6 +602,7 @@ void launch_f2c(acp_context* ctx, const FopArgs& a, double2* S, int* queue, doub
     g.npair = (a.n + 1) / 2;
     g.R = std::min(G.R, g.npair);
     g.d = G.d;
+    g.discard = getenv("ACP_F2C_DISCARD") ? atoi(getenv("ACP_F2C_DISCARD")) : 0;
     g.nsteps = g.npair + 2 * G.d;
     g.queue = queue;
     g.part = part;

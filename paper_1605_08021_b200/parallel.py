@@ -1,5 +1,7 @@
-"""Multi-GPU layer: Alg. 4 with the compression AND the compressed Sternheimer right-hand sides
-sharded across ranks (one process per GPU), exchanges over NCCL (NVLink).
+"""Multi-GPU layer: Alg. 4 with the compressed Sternheimer right-hand sides sharded across ranks
+(one process per GPU) and the compression either sharded by grid point or replicated
+(use_sharded_compress: replicated up to 8 ranks, where the one-GPU Kronecker QRCP beats the
+per-pivot protocol); exchanges over NCCL (NVLink).
 
 * Compression (Alg. 2): rank r owns the grid points [a_r, b_r) -- the columns
   of M~^T.  Each pivot step is one kernel on every rank plus ONE all-gather of the ranks' best
