@@ -29,6 +29,13 @@
 
 // 16-line batches per queue item (A/B at build time, -DACP_F2C_BPI=n).  c4g, 38088 columns, best queue
 // skew each: 1 -> 32.0 ms, 2 -> 26.94, 4 -> 25.50, 8 -> 26.1, 16 -> 28.8 (runs R5f, R5g)
+// -DACP_F2C_DISCARD=m (A/B at build time): drop a consumed plane block from L2 (discard.global.L2)
+// instead of letting it be written back -- 1: all threads before the batch, 2: after it, 3: one warp
+// after it.  c4g, 38088 columns, m = 1: DRAM writes 59.2 -> 29.8 GB per launch but 26.07 vs 25.18 ms
+// (run R6c): the kernel is not DRAM-bound, the CCTLs cost issue slots.  Default 0.
+#ifndef ACP_F2C_DISCARD
+#define ACP_F2C_DISCARD 0
+#endif
 #ifndef ACP_F2C_BPI
 #define ACP_F2C_BPI 4
 #endif
@@ -69,7 +76,6 @@ struct F2cArgs {
     double2* S;            // ring of R slots, 2 N^2 complex each (S1 then S2)
     int R;                 // ring slots
     int d;                 // queue skew (steps between A and B, B and C of a pair)
-    int discard;           // 1: a consumed plane block is dropped from L2 (discard.global.L2) instead of written back
     int npair;
     int nsteps;            // npair + 2 d
     int* queue;            // [0] = next item; then cnt[3 * npair] (A, B, C done-counts per pair)
@@ -195,6 +201,19 @@ __device__ __forceinline__ bool deps_ready(const F2cArgs& g, const Item& it, boo
         }
     }
     return true;
+}
+
+// The plane block of batch b of a B / C item (16 N complex, contiguous, read only by that batch) is in
+// the stage: its L2 lines hold dead data until pair p + R rewrites them -- drop them instead of
+// letting the L2 write them back (experiment R6c / R6d, ACP_F2C_DISCARD).
+template <int N>
+__device__ __forceinline__ void f2c_discard(const F2cArgs& g, const Item& it, int b, int lane, int nl) {
+    using K = F2C<N>;
+    const size_t NN = (size_t)N * N;
+    const char* blk = reinterpret_cast<const char*>(g.S + (size_t)(it.p % g.R) * 2 * NN + (it.phase == 2 ? NN : 0) +
+                                                    (size_t)((it.q * K::BPI + b) * 16) * N);
+    for (int l = lane; l < 16 * N * (int)sizeof(double2) / 128; l += nl)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(blk + (size_t)l * 128) : "memory");
 }
 
 // Thread 0: fetch batch b of item `it` into stage `buf` (its dependencies hold).
@@ -457,16 +476,10 @@ __global__ void __launch_bounds__(256, MB) k_f2c(F2cArgs g) {
         if (cur.skip == 0) {
             mbar_wait(&bars[buf], uses[buf] & 1);
             ++uses[buf];
-            if (g.discard && cur.phase != 0) {
-                // the plane block of this batch (16 N complex, contiguous, read only by this batch)
-                // is in the stage now: its L2 lines hold dead data until pair p + R rewrites them
-                const size_t NN = (size_t)N * N;
-                const char* blk = reinterpret_cast<const char*>(
-                    g.S + (size_t)(cur.p % g.R) * 2 * NN + (cur.phase == 2 ? NN : 0) + (size_t)((cur.q * K::BPI + cb) * 16) * N);
-                for (int l = t; l < 16 * N * (int)sizeof(double2) / 128; l += 256)
-                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(blk + (size_t)l * 128) : "memory");
-            }
+            if (ACP_F2C_DISCARD == 1 && cur.phase != 0) f2c_discard<N>(g, cur, cb, t, 256);
             f2c_batch<N>(g, cur, cb, sm + (size_t)buf * K::BUF, tws, hk[0], hk[1], d);
+            if (ACP_F2C_DISCARD == 2 && cur.phase != 0) f2c_discard<N>(g, cur, cb, t, 256);
+            if (ACP_F2C_DISCARD == 3 && cur.phase != 0 && t >= 224) f2c_discard<N>(g, cur, cb, t - 224, 32);
             fence_proxy_async();  // this stage's generic accesses precede its next bulk refill
         }
         if (last && cur.skip != 2) {
@@ -602,7 +615,6 @@ void launch_f2c(acp_context* ctx, const FopArgs& a, double2* S, int* queue, doub
     g.npair = (a.n + 1) / 2;
     g.R = std::min(G.R, g.npair);
     g.d = G.d;
-    g.discard = getenv("ACP_F2C_DISCARD") ? atoi(getenv("ACP_F2C_DISCARD")) : 0;
     g.nsteps = g.npair + 2 * G.d;
     g.queue = queue;
     g.part = part;
