@@ -325,10 +325,16 @@ def run_acp(args, cfg):
     n_all = cfg.n_cheb * ((n_mu + 1) // 2 * 2)
     ngroups = min(cfg.n_cheb, 4) if n_all * ctx.Ng <= (16 << 20) else 1
     ncols = (cfg.n_cheb // ngroups) * ((n_mu + 1) // 2 * 2)
+    nmu_p = (n_mu + 1) // 2 * 2
+    sweep = int(os.environ.get("ACP_PCG_SWEEP", -1))
+    if sweep < 0:  # pcg.cu's node sweep: large batches (N_mu' >= 768) run one Chebyshev node per warm-started group
+        sweep = 1 if (ngroups == 1 and cfg.n_cheb >= 3 and nmu_p >= 768) else 0
+    if 0 < sweep < cfg.n_cheb:
+        ncols = sweep * nmu_p
     # X and Y for the kernel timing must fit beside the library's PCG workspace
     free_b, _ = torch.cuda.mem_get_info(dev)
     fit = int((free_b - (4 << 30)) // (2 * 8 * ctx.Ng)) // 2 * 2
-    shape_note = "production launch shape (one PCG node group)"
+    shape_note = "production launch shape (one PCG node group" + (f": {sweep} Chebyshev node(s) of the sweep)" if 0 < sweep < cfg.n_cheb else ")")
     if fit < ncols:
         ncols = max(2, fit)
         shape_note = (f"{ncols} of the production launch's {n_all} columns (memory beside the PCG workspace); "

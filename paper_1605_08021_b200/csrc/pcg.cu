@@ -66,7 +66,7 @@ __global__ void k_pcg_init(int Ng, int nc, int nmu_p, const double* __restrict__
     X[i] = 0.0;
 }
 
-enum { SC_INIT = 0, SC_ALPHA = 1, SC_BETA = 2 };
+enum { SC_INIT = 0, SC_ALPHA = 1, SC_BETA = 2, SC_WARM = 3 };
 
 struct PcgScal {
     double* rz;      // r.z (current)
@@ -86,22 +86,27 @@ struct ScalHook {
     double tol2;
     int n_valid_mu;
     int nmu_p;
+    // warm start (node sweep): ||b||^2 per mu, from the first node's cold start; SC_INIT then also
+    // tests the warm residual against the tolerance.  nullptr: cold start (r0 = b).
+    const double* bb0;
     __device__ __forceinline__ bool tile_active(int n0, int n) const { return tile_active_w(n0, n, 32); }
     __device__ __forceinline__ bool tile_active_w(int n0, int n, int w) const {
-        if (mode == SC_INIT) return true;
+        if (mode == SC_INIT || mode == SC_WARM) return true;
         int a = 0;
         for (int c = n0; c < min(n, n0 + w); ++c) a |= s.active[c];
         return a != 0;
     }
     __device__ __forceinline__ void operator()(int j) const {
+        if (mode == SC_WARM) return;  // alpha = 1, active = 1 were set by k_warm_set
         if (mode == SC_INIT) {
-            const double rz = s.dots[2 * j], bb = s.dots[2 * j + 1];
+            const double rz = s.dots[2 * j], rr = s.dots[2 * j + 1];
+            const double bb = bb0 ? bb0[j % nmu_p] : rr;
             const bool valid = (j % nmu_p) < n_valid_mu && bb > 0.0;
             s.rz[j] = rz;
             s.bb[j] = bb;
-            s.active[j] = valid ? 1 : 0;
+            s.active[j] = (valid && (!bb0 || rr > tol2 * bb)) ? 1 : 0;
             s.iters[j] = 0;
-            s.res[j] = 0.0;
+            s.res[j] = (bb0 && bb > 0.0) ? sqrt(rr / bb) : 0.0;
             s.alpha[j] = 0.0;
             s.beta[j] = 0.0;
         } else if (mode == SC_ALPHA) {
@@ -444,6 +449,10 @@ __global__ void k_count_active(const int* __restrict__ active, int n, int* __res
 // Phi_c = Psi B_c with B_c(i, mu) = L(i, c) Psi(r_mu, i) is a genuine GEMM (N_g x N_occ x N_mu):
 // one DMMA GEMM per node whose epilogue accumulates W += 2f X_c (.) Phi_c (nodes in order).
 constexpr int W_MAXC = 32;
+constexpr int PCG_MAXGRP = 64;  // groups of a sequential node sweep (streams: PCG_MAXG)
+constexpr int PCG_SWEEP_DEF = 1;  // nodes per warm-started group of the sweep (A/B: ACP_PCG_SWEEP)
+constexpr int PCG_WARM_K = 3;
+constexpr double PCG_WARM_TOL = 1.0;  // warm-started groups stop at this fraction of the CG tolerance (A/B)
 constexpr int PCG_DEFG = 4;  // default group count for small batches (PCG_MAXG with ACP_PCG_GROUPS)
 __global__ void k_w_rhs(int Ng, int n_occ, int nc, int cnt, const double* __restrict__ Psi,
                         const double* __restrict__ L, const int* __restrict__ S, int mu_begin,
@@ -544,6 +553,40 @@ static void launch_nn_ep(acp_context* ctx, int M, int K, int n, const double* A,
 
 // One independent group of columns (a contiguous range of Chebyshev nodes) of the batch: its
 // buffers are column slices of the batch's, so groups never touch each other's data.
+// Node sweep (warm starts): every column active with alpha = 1 for the residual half-step.
+__global__ void k_warm_set(int n, int* __restrict__ active, double* __restrict__ alpha) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) {
+        active[j] = 1;
+        alpha[j] = 1.0;
+    }
+}
+
+// Initial guess for node c from the k solved nodes c0 - k .. c0 - 1: the solution zeta(eps~) of
+// Q(H - eps~)Q zeta = Q xi is analytic in eps~ (the premise of Eq. eqnparam's Chebyshev
+// interpolation), so the Lagrange polynomial through the solved nodes,
+// evaluated at node c, is close to zeta_c.  P_c = sum_i w_i X_i; X_c = the same (xset) or untouched.
+constexpr int WARM_KMAX = 8;
+__global__ void k_warm_guess(size_t tot, size_t node_stride, int c, int c0, int k, const double* __restrict__ shift_c,
+                             const double* __restrict__ X, double* __restrict__ P, double* __restrict__ Xc, int xset) {
+    __shared__ double w[WARM_KMAX];
+    if (threadIdx.x < k) {
+        const int i = c0 - k + threadIdx.x;
+        const double x = shift_c[c], xi = shift_c[i];
+        double v = 1.0;
+        for (int j = c0 - k; j < c0; ++j)
+            if (j != i) v *= (x - shift_c[j]) / (xi - shift_c[j]);
+        w[threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int q = 0; q < k; ++q) acc += w[q] * X[(size_t)(c0 - k + q) * node_stride + e];
+        P[(size_t)c * node_stride + e] = acc;
+        if (xset) Xc[(size_t)c * node_stride + e] = acc;
+    }
+}
+
 struct PcgGroup {
     double *R, *P, *Y, *X, *C, *shift, *dots;
     PcgScal s;
@@ -557,7 +600,7 @@ struct PcgGroup {
 // Enqueue the PCG of one group on ctx->stream: r0 = b, z0 = Q M r0, p0 = z0, then the iteration
 // loop (while-node graph).  Returns without waiting unless the host-driven loop is selected.
 static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, const double* V, PcgGroup& G,
-                              int nmu_p, double tol2, double tau, int max_iter) {
+                              int nmu_p, double tol2, double tau, int max_iter, const double* bb0 = nullptr) {
     const int Ng = ctx->Ng;
     double *R = G.R, *P = G.P, *Y = G.Y, *X = G.X, *C = G.C, *shift = G.shift, *dots = G.dots;
     PcgScal& s = G.s;
@@ -578,7 +621,7 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
         f.active = (mode == SC_INIT) ? nullptr : s.active;
         f.dots = dots;
         fourier_op(ctx, f);
-        const ScalHook hk{mode, s, tol2, nvalid, nmu_p};
+        const ScalHook hk{mode, s, tol2, nvalid, nmu_p, mode == SC_INIT ? bb0 : nullptr};
         ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ, hk),
                     "projection GEMM needs an even grid");
         if (mode == SC_INIT) {
@@ -589,7 +632,7 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
             launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpBetaP{Y, P, s.beta, s.active, Ng});
         }
     };
-    auto hamiltonian_half = [&]() {
+    auto hamiltonian_half = [&](int hmode = SC_ALPHA) {
         FopArgs f;
         f.X = P;
         f.Y = Y;
@@ -600,7 +643,7 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
         f.active = s.active;
         f.dots = dots;
         fourier_op(ctx, f);
-        const ScalHook hk{SC_ALPHA, s, tol2, nvalid, nmu_p};
+        const ScalHook hk{hmode, s, tol2, nvalid, nmu_p, nullptr};
         ACP_REQUIRE(launch_tn_cluster(ctx, Ng, n_occ, n, ctx->dV, Psi, Ng, Y, Ng, C, n_occ, hk),
                     "projection GEMM needs an even grid");
         if (x_in_beta)
@@ -609,7 +652,14 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
             launch_pcg_update(ctx, Ng, n_occ, n, Psi, Ng, C, n_occ, EpAlphaX{Y, P, X, R, s.alpha, s.active, Ng});
     };
 
-    // r0 = b, z0 = Q M r0, p0 = z0
+    if (bb0) {
+        // warm start: P holds the guess x0 (X = x0 too when K3 leaves X to EpBeta, else X = 0), R = b.
+        // One Hamiltonian half with alpha = 1 on every column: R = b - Q(H - eps~)Q x0, X = x0.
+        k_warm_set<<<cdiv(n, 256), 256, 0, ctx->stream>>>(n, s.active, s.alpha);
+        launched(ctx);
+        hamiltonian_half(SC_WARM);
+    }
+    // r0 = b (or the warm residual), z0 = Q M r0, p0 = z0
     precond_half(SC_INIT);
 
     // The whole iteration loop is ONE CUDA graph with a device-side while node: its body is
@@ -731,7 +781,7 @@ static void pcg_group_enqueue(acp_context* ctx, const double* Psi, int n_occ, co
 //   [4] unconverged columns, [5] max relative residual (double bits), [6] LU status,
 //   [8 + 2k] iterations of outer iteration k, [9 + 2k] spare.
 struct PcgLaunchCounts {
-    long long per_trip[PCG_MAXG];
+    long long per_trip[PCG_MAXGRP];
 };
 __global__ void k_pcg_accum_stats(int n, const int* __restrict__ iters, const double* __restrict__ res,
                                   const double* __restrict__ bb, const int* __restrict__ nact, int ngroups,
@@ -797,7 +847,7 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     s.active = ctx->wsi("pcg_active", n);
     s.iters = ctx->wsi("pcg_iters", n);
     s.dots = dots;
-    int* d_nact = ctx->wsi("pcg_nact", 2 * PCG_MAXG);  // per group: [0] active columns, [1] trips
+    int* d_nact = ctx->wsi("pcg_nact", 2 * PCG_MAXGRP);  // per group: [0] active columns, [1] trips
     int* h_nact = static_cast<int*>(ctx->pinned);
     // Two node groups on two streams: their kernels overlap, filling the latency gaps of each
     // other's small launches (configs[1]: one K1 launch is a single wave of 464 CTAs).
@@ -811,6 +861,18 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     if (const char* e = getenv("ACP_PCG_GROUPS")) ngroups = std::max(1, std::min(std::min(n_c, PCG_MAXG), atoi(e)));
     if (getenv("ACP_PCG_HOSTLOOP")) ngroups = 1;
     if (ngroups < 1) ngroups = 1;
+    // Node sweep (large batches): the nodes are solved `sweep` at a time, one group after the other
+    // on the one stream, each later group WARM-STARTED from the Lagrange extrapolation of up to
+    // WARM_KMAX already solved nodes (k_warm_guess) -- the same equations to the same tolerance
+    // from a closer start: fewer CG iterations per column, every group still thousands of columns
+    // wide.  ACP_PCG_SWEEP = nodes per group (0: off, all nodes in one cold-started batch).
+    // Measured (runs R6e, R6h; order-3 guess): c4g 8.12 vs 9.87 s per step, c3g 584 vs 617 ms;
+    // configs[2] (N_mu' ~ 592: 203.6 cold) 204-219 ms -- no gain below ~768 columns per node.
+    int sweep = ((size_t)n * Ng > ((size_t)16 << 20) && n_c >= 3 && nmu_p >= 768) ? PCG_SWEEP_DEF : 0;
+    if (const char* e = getenv("ACP_PCG_SWEEP")) sweep = std::max(0, atoi(e));
+    if (sweep >= n_c) sweep = 0;
+    if (sweep > 0) ngroups = std::min(PCG_MAXGRP, cdiv(n_c, sweep));
+    if (sweep > 0) sweep = cdiv(n_c, ngroups);
 
     k_batch_shift<<<cdiv(n, 256), 256, 0, ctx->stream>>>(d_shift_c, n_c, nmu_p, shift);
     launched(ctx);
@@ -820,10 +882,13 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         launched(ctx);
     }
     const double tol2 = tol * tol;
-    PcgGroup grp[PCG_MAXG];
-    int gc0[PCG_MAXG + 1];  // group g: nodes [g n_c / G, (g+1) n_c / G)
-    for (int g = 0; g <= ngroups; ++g) gc0[g] = (g * n_c / ngroups) * nmu_p;
-    for (int g = 0; g < ngroups; ++g) fourier_reserve(ctx, gc0[g + 1] - gc0[g], g);  // before any capture
+    PcgGroup grp[PCG_MAXGRP];
+    int gc0[PCG_MAXGRP + 1];  // group g: nodes [g n_c / G, (g+1) n_c / G)
+    for (int g = 0; g <= ngroups; ++g) gc0[g] = (sweep > 0 ? std::min(n_c, g * sweep) : g * n_c / ngroups) * nmu_p;
+    if (sweep > 0)
+        fourier_reserve(ctx, sweep * nmu_p, 0);  // the groups run one after the other on intermediate 0
+    else
+        for (int g = 0; g < ngroups; ++g) fourier_reserve(ctx, gc0[g + 1] - gc0[g], g);  // before any capture
     for (int g = 0; g < ngroups; ++g) {
         const int c0 = gc0[g], cn = gc0[g + 1] - gc0[g];
         PcgGroup& G = grp[g];
@@ -848,7 +913,35 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
         G.h_nact = h_nact + 2 * g;
         G.launches_per_trip = 0;
     }
-    if (ngroups == 1) {
+    if (sweep > 0) {
+        const size_t node_stride = (size_t)Ng * nmu_p;
+        // A tighter tolerance for the warm-started groups (ACP_PCG_WARM_TOL < 1) was tried when the
+        // order-8 guess missed the W bar on configs[2]; it did not help (the loss came from the
+        // extrapolation order, below) and costs 0.7 s per c4g step at 0.1 -- default 1.
+        double warm_tol = PCG_WARM_TOL;
+        if (const char* e = getenv("ACP_PCG_WARM_TOL")) warm_tol = atof(e);
+        // Solved nodes the guess extrapolates from.  High orders predict better but their large
+        // alternating weights amplify the solved nodes' own (near-gap) errors into the guess, and
+        // the residual test does not see them: configs[2] golden W (4 outers) 3e-10 cold, 3e-10 at
+        // k = 2 / 3, 1e-9 at k = 4, 4e-8 at k = 8 (run R6g).  Default 3.  ACP_PCG_WARM_K: A/B.
+        int warm_k = PCG_WARM_K;
+        if (const char* e = getenv("ACP_PCG_WARM_K")) warm_k = std::max(1, std::min(WARM_KMAX, atoi(e)));
+        const int xset = pcg_x_in_beta(n_occ) ? 1 : 0;
+        for (int g = 0; g < ngroups; ++g) {
+            const int c0 = gc0[g] / nmu_p, c1 = gc0[g + 1] / nmu_p;
+            if (g > 0) {
+                const int k = std::min(c0, warm_k);
+                for (int c = c0; c < c1; ++c) {
+                    k_warm_guess<<<148 * 8, 256, 0, ctx->stream>>>(node_stride, node_stride, c, c0, k, d_shift_c, X, P, X,
+                                                                    xset);
+                    launched(ctx);
+                }
+            }
+            pcg_group_enqueue(ctx, Psi, n_occ, V, grp[g], nmu_p, g > 0 ? tol2 * warm_tol * warm_tol : tol2, tau, max_iter,
+                              g > 0 ? s.bb : nullptr);
+        }
+        if (!grp[ngroups - 1].synced && !ctx->defer) ACP_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else if (ngroups == 1) {
         pcg_group_enqueue(ctx, Psi, n_occ, V, grp[0], nmu_p, tol2, tau, max_iter);
         if (!grp[0].synced && !ctx->defer) ACP_CUDA(cudaStreamSynchronize(ctx->stream));
     } else {
@@ -914,10 +1007,10 @@ void sternheimer_batch(acp_context* ctx, const double* Psi, int n_occ, const dou
     }
     if (ctx->defer) {
         // no host wait: accumulate the statistics on the device (read at the end of acp_dyson)
-        long long lpt[PCG_MAXG] = {};
+        long long lpt[PCG_MAXGRP] = {};
         for (int g = 0; g < ngroups; ++g) lpt[g] = grp[g].synced ? 0 : grp[g].launches_per_trip;
         PcgLaunchCounts lc;
-        for (int g = 0; g < PCG_MAXG; ++g) lc.per_trip[g] = lpt[g];
+        for (int g = 0; g < PCG_MAXGRP; ++g) lc.per_trip[g] = lpt[g];
         k_pcg_accum_stats<<<1, 256, 0, ctx->stream>>>(n, s.iters, s.res, s.bb, d_nact, ngroups, lc,
                                                         ctx->defer_iter, ctx->defer_stats);
         launched(ctx);
