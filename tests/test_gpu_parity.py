@@ -346,6 +346,50 @@ def test_apply_chi0_node_counts(n_cheb):
     assert rel(W_g.cpu().numpy().T, W_o) < 1e-9
 
 
+@pytest.mark.parametrize("sweep,order", [(1, 3), (2, 3), (1, 8), (3, 1)])
+def test_apply_chi0_node_sweep_matches_direct_solves(sysx, monkeypatch, sweep, order):
+    """The PCG node sweep (DESIGN reading R21: nodes solved group after group, later groups
+    warm-started from the Lagrange extrapolation of the solved nodes; the default only for
+    N_mu' >= 768) forced on the small systems: W against the oracle's direct compressed solves
+    (Eq. eqncompressU / eqnW) at the same bar as the cold batch, every column converged, and fewer
+    CG iterations than the cold batch."""
+    s = sysx
+    if s.cfg.n_cheb <= sweep:
+        pytest.skip("needs more Chebyshev nodes than the group size")
+    th, nu = s.draws(0, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    W_o = oacp.compressed_W(s.m, s.H, s.gs.Psi, s.gs.eps[: s.cfg.n_occ], S_o, Xi_o, s.cfg.n_cheb)
+    St, Xt = T(S_o, torch.int32), T(Xi_o.T)
+    monkeypatch.setenv("ACP_PCG_SWEEP", "0")
+    _, cold = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb, cg_tol=s.cfg.cg_tol)
+    monkeypatch.setenv("ACP_PCG_SWEEP", str(sweep))
+    monkeypatch.setenv("ACP_PCG_WARM_K", str(order))
+    W_g, info = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb, cg_tol=s.cfg.cg_tol)
+    assert info["n_solved"] == s.cfg.n_cheb * len(S_o)
+    assert info["max_rel_res"] <= s.cfg.cg_tol
+    assert rel(W_g.cpu().numpy().T, W_o) < 1e-9
+    assert info["total_iter"] < cold["total_iter"], (info["total_iter"], cold["total_iter"])
+
+
+def test_apply_chi0_node_sweep_sharding_is_bitwise(sysx, monkeypatch):
+    """The warm start is per column (a column's guess uses only its own mu at the other nodes), so
+    the RHS shards of the multi-GPU path reproduce the unsharded sweep bit for bit."""
+    s = sysx
+    if s.cfg.n_cheb < 2:
+        pytest.skip("one node")
+    monkeypatch.setenv("ACP_PCG_SWEEP", "1")
+    th, nu = s.draws(1, s.G.shape[1])
+    S_o, Xi_o, _ = oacp.compress(s.m, s.gs.Psi, s.G, th, nu, s.cfg.id_eps)
+    St, Xt = T(S_o, torch.int32), T(Xi_o.T)
+    W_full, _ = s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb)
+    n = len(S_o)
+    cut = (n // 2) & ~1
+    W_sh = torch.zeros_like(W_full)
+    s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb, mu_range=(0, cut), W=W_sh)
+    s.ctx.apply_chi0(s.Psi_t, s.eps_t, s.V_t, St, Xt, s.cfg.n_cheb, mu_range=(cut, n), W=W_sh)
+    assert torch.equal(W_full, W_sh)
+
+
 def test_apply_chi0_sharding_is_bitwise(sysx):
     """RHS sharding across GPUs (even shard sizes) reproduces the unsharded W bit for bit."""
     s = sysx
